@@ -1,0 +1,167 @@
+/*
+ * sbw.h -- C ABI of libsbw, the sm_100a (B200) S-box Walsh-spectrum and
+ * nonlinearity engine.  No torch types cross this boundary: plain pointers,
+ * sizes and a cudaStream_t passed as void*.
+ *
+ * The reference (`sboxeval`, pure Python + numpy, under /root/reference) has
+ * no native code; each entry point below names the reference function whose
+ * hot loop it replaces.  INTEGRATION.md shows the ctypes binding a
+ * maintainer would add to the reference package.
+ *
+ * Conventions (identical to the reference):
+ *   - masks v run over [v_lo, v_hi) with 1 <= v_lo <= v_hi <= 2^m; the v = 0
+ *     row is never stored (sbox.py:155-159);
+ *   - spectra are int32 in natural (Sylvester) order, unnormalised:
+ *     W(u,v) = sum_x (-1)^{popc(v & S(x)) + popc(u & x)} (walsh.py:56-70);
+ *   - per-component maxima are max over ALL u (u = 0 included) of |W(u,v)|
+ *     (walsh.py:101-102); NL_v = (2^n - max|W|) / 2 (walsh.py:107-114);
+ *   - the "key" is the 64-bit value (max|W| << 32) | (0xFFFFFFFF - v),
+ *     so an atomicMax picks the largest max|W| with ties to the SMALLEST v,
+ *     i.e. the reference's first-argmin (nonlinearity.py:44, :55).
+ *
+ * Device pointers are caller-owned and never freed by the library.  Calls
+ * are asynchronous on `stream` (NULL = legacy default stream) unless the
+ * name ends in _host.  Table entries are `table_bytes` wide (2 or 4):
+ * the host narrows SBox.table (uint32, sbox.py:64) to uint16 when m <= 16.
+ *
+ * Return codes: 0 = ok, < 0 = error; sbw_last_error() gives the message of
+ * the last failing call on the calling thread.
+ */
+#ifndef SBW_H_
+#define SBW_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SBW_ABI_VERSION 1
+
+#define SBW_OK 0
+#define SBW_EINVAL -1  /* ValueError in the reference (walsh.py:86-87, :216-217) */
+#define SBW_ECUDA -2   /* CUDA runtime failure (no reference analogue)          */
+#define SBW_EPARITY -3 /* AssertionError: odd spectrum gap (walsh.py:110-113)   */
+#define SBW_ERANGE -4  /* IndexError: mask / input out of range (walsh.py:63-66) */
+
+#define SBW_LAYOUT_MASK_MAJOR 0 /* out[(v - v_lo) * ld + u]  (WalshSpectrum.rows, walsh.py:32-44) */
+#define SBW_LAYOUT_X_MAJOR 1    /* out[u * ld + (v - v_lo)]  (build_polarity_xmajor, walsh.py:117-131) */
+
+typedef struct sbw_device_info {
+  int device;
+  int sm_count;
+  int cc_major;
+  int cc_minor;
+  int64_t smem_optin_bytes;
+  int64_t l2_bytes;
+  int64_t global_mem_bytes;
+  char name[128];
+} sbw_device_info_t;
+
+int sbw_abi_version(void);
+const char* sbw_last_error(void);
+int sbw_device_info(int device, sbw_device_info_t* out);
+/* Number of libsbw kernels launched by this process so far. */
+uint64_t sbw_launch_count(void);
+
+/*
+ * Fused component generation -> FWHT -> max|W|, spectrum never stored.
+ * Replaces the stream loop of fwht_fused (walsh.py:230-244) and the worker
+ * body of fwht_parallel (parallel.py:99-115): polarity_row (sbox.py:145-152)
+ * + fwht_column_in_place (walsh.py:73-104) + column_nonlinearity (:107-114).
+ *   d_max_abs[v - v_lo] <- max_u |W(u,v)|               (int32, device)
+ *   *d_key              <- atomicMax(key) over the range (device, may be NULL;
+ *                          caller initialises it, e.g. to 0)
+ * n, m in 1..24.  `scratch`/`scratch_bytes` is a device workspace required
+ * only for n >= 17 (size from sbw_nl_scratch_bytes); pass NULL/0 otherwise.
+ */
+int sbw_nl(const void* d_table, int table_bytes, int n, int m, uint32_t v_lo, uint32_t v_hi,
+           int32_t* d_max_abs, unsigned long long* d_key, void* scratch, size_t scratch_bytes,
+           void* stream);
+size_t sbw_nl_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi);
+
+/*
+ * Materialised spectrum rows for masks [v_lo, v_hi) in either layout, plus
+ * the per-component max|W| (d_max_abs may be NULL).  Replaces
+ * fwht_transposed (walsh.py:183-201), fwht_rowmajor (walsh.py:155-180) and
+ * fwht_fused(mode="retain") (walsh.py:220-229).  `ld` is the row pitch in
+ * elements (>= 2^n for mask-major, >= v_hi - v_lo for x-major).  The x-major
+ * layout needs a workspace of sbw_spectrum_scratch_bytes(...) bytes.
+ */
+int sbw_spectrum(const void* d_table, int table_bytes, int n, int m, uint32_t v_lo,
+                 uint32_t v_hi, int layout, int32_t* d_out, int64_t ld, int32_t* d_max_abs,
+                 void* scratch, size_t scratch_bytes, void* stream);
+size_t sbw_spectrum_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi, int layout);
+
+/*
+ * Polarity truth table (-1)^{g_v(x)} as int32, either layout.  Replaces
+ * polarity_row / polarity_truth_table (sbox.py:145-162) and
+ * build_polarity_xmajor (walsh.py:117-131).  Unlike the spectrum calls the
+ * range may start at v = 0 (the constant +1 row).
+ */
+int sbw_polarity(const void* d_table, int table_bytes, int n, int m, uint32_t v_lo,
+                 uint32_t v_hi, int layout, int32_t* d_out, int64_t ld, void* stream);
+
+/*
+ * Generic in-place int32 FWHT of `count` contiguous columns of length 2^k
+ * (k in 0..24), int32 wrap-around arithmetic exactly like numpy.  Replaces
+ * fwht_column_in_place (walsh.py:73-104) and transform_rows_in_place
+ * (walsh.py:140-152).  d_max_abs[c] (int64, may be NULL) receives the
+ * column's max of numpy-int32 |x| (k >= 1) or |x| (k == 0).
+ */
+int sbw_fwht_inplace(int32_t* d_data, int k, int64_t count, int64_t* d_max_abs, void* stream);
+
+/*
+ * Per-component max|W| -> NL_v = (2^n - max|W|) >> 1 as int64 (ColumnMaxima
+ * values, walsh.py:47-53 / :107-114).  *d_bad (device int64) receives the
+ * smallest index with an odd gap, or stays INT64_MAX (the library
+ * initialises it on `stream`).
+ */
+int sbw_maxabs_to_nl(const int32_t* d_max_abs, int64_t count, int n, int64_t* d_nl,
+                     int64_t* d_bad, void* stream);
+/* int64 variant for sbw_fwht_inplace maxima (transform_rows_in_place, walsh.py:148-152). */
+int sbw_maxabs64_to_nl(const int64_t* d_max_abs, int64_t count, int64_t pw, int64_t* d_nl,
+                       int64_t* d_bad, void* stream);
+
+/*
+ * Spectrum scan (nonlinearity_from_spectrum, nonlinearity.py:36-48):
+ * d_row_max[r] = max(rows[r].max(), -rows[r].min()) as int64, and
+ * atomicMax of the (row_max, smallest row) key into *d_key (may be NULL).
+ */
+int sbw_row_maxabs(const int32_t* d_rows, int64_t rows, int64_t cols, int64_t ld,
+                   int64_t* d_row_max, unsigned long long* d_key, void* stream);
+
+/* Direct evaluation W(u_i, v_i) of the defining sum (walsh_direct, walsh.py:56-70). */
+int sbw_walsh_direct(const void* d_table, int table_bytes, int n, int m, const uint32_t* d_u,
+                     const uint32_t* d_v, int64_t count, int32_t* d_out, void* stream);
+
+/*
+ * Affine-distance brute force (nonlinearity_bruteforce, nonlinearity.py:59-86),
+ * n, m <= 8: d_best[v - 1] = min over affine functions of the Hamming
+ * distance to g_v, for v in [1, 2^m).
+ */
+int sbw_nl_bruteforce(const void* d_table, int table_bytes, int n, int m, int32_t* d_best,
+                      void* stream);
+
+/*
+ * Host-buffer end-to-end call (what a plugin binding makes): copies the
+ * uint32 table host->device, runs sbw_nl over [v_lo, v_hi) on `device`,
+ * copies per-component NL (int64) device->host and returns
+ * out3 = {NL value, argmin_v, max|W|}.  Synchronous.
+ */
+int sbw_nl_host(const uint32_t* h_table, int n, int m, uint32_t v_lo, uint32_t v_hi,
+                int64_t* h_nl, int64_t* out3, int device);
+
+/*
+ * INT32 ALU peak microbenchmark on the current device: independent
+ * add/sub chains (IADD3 on the ALU pipe mixed with IMAD on the FMA pipe).
+ * Writes lane-ops per second and the kernel time.
+ */
+int sbw_int32_peak(double* ops_per_s, double* ms, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SBW_H_ */

@@ -1,0 +1,338 @@
+// extern "C" boundary of libsbw (declared in include/sbw.h).
+//
+// Argument validation mirrors the reference's exceptions: n, m in 1..24
+// (sbox.py:18, :60-63), mask ranges within [1, 2^m) (sbox.py:155-159),
+// power-of-two columns (walsh.py:86-87).  Budget checks (memory.py:66-68) stay
+// in the host package, before any launch.
+#include <climits>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+
+#include "sbw_internal.cuh"
+#include "sbw_launch.h"
+
+namespace sbw {
+
+namespace {
+thread_local char g_err[512] = "";
+std::atomic<uint64_t> g_launches{0};
+
+struct PropsCache {
+  std::mutex mu;
+  bool valid[64] = {};
+  DeviceProps p[64];
+} g_props;
+}  // namespace
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_error(cudaError_t e, const char* what) {
+  return set_error(SBW_ECUDA, "CUDA error %s (%s) in %s", cudaGetErrorName(e),
+                   cudaGetErrorString(e), what);
+}
+
+void count_launch(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+int device_props(DeviceProps* out) {
+  int dev = 0;
+  SBW_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return set_error(SBW_EINVAL, "device index %d unsupported", dev);
+  std::lock_guard<std::mutex> lk(g_props.mu);
+  if (!g_props.valid[dev]) {
+    DeviceProps p{};
+    p.device = dev;
+    int v = 0;
+    SBW_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+    p.sm_count = v;
+    SBW_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    p.smem_optin = size_t(v);
+    SBW_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev));
+    p.l2_bytes = size_t(v);
+    g_props.p[dev] = p;
+    g_props.valid[dev] = true;
+  }
+  *out = g_props.p[dev];
+  return SBW_OK;
+}
+
+}  // namespace sbw
+
+using namespace sbw;
+
+namespace {
+
+int check_nm(int n, int m) {
+  if (n < 1 || n > 24) return set_error(SBW_EINVAL, "n must be in 1..24, got %d", n);
+  if (m < 1 || m > 24) return set_error(SBW_EINVAL, "m must be in 1..24, got %d", m);
+  return SBW_OK;
+}
+
+int check_table(const void* t, int tbytes, int m) {
+  if (t == nullptr) return set_error(SBW_EINVAL, "null table pointer");
+  if (tbytes != 2 && tbytes != 4)
+    return set_error(SBW_EINVAL, "table entries must be 2 or 4 bytes, got %d", tbytes);
+  if (tbytes == 2 && m > 16)
+    return set_error(SBW_EINVAL, "m = %d needs a 4-byte table", m);
+  if ((reinterpret_cast<uintptr_t>(t) & 15u) != 0)
+    return set_error(SBW_EINVAL, "table pointer must be 16-byte aligned");
+  return SBW_OK;
+}
+
+int check_range(int m, uint32_t v_lo, uint32_t v_hi) {
+  const uint64_t top = uint64_t(1) << m;
+  if (v_lo < 1 || v_lo > v_hi || uint64_t(v_hi) > top)
+    return set_error(SBW_ERANGE, "mask range [%u, %u) outside [1, %llu)", v_lo, v_hi,
+                     (unsigned long long)top);
+  return SBW_OK;
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+int sbw_abi_version(void) { return SBW_ABI_VERSION; }
+
+const char* sbw_last_error(void) { return g_err; }
+
+uint64_t sbw_launch_count(void) { return g_launches.load(); }
+
+int sbw_device_info(int device, sbw_device_info_t* out) {
+  if (!out) return set_error(SBW_EINVAL, "null output");
+  cudaDeviceProp p;
+  SBW_CUDA_CHECK(cudaGetDeviceProperties(&p, device));
+  memset(out, 0, sizeof(*out));
+  out->device = device;
+  out->sm_count = p.multiProcessorCount;
+  out->cc_major = p.major;
+  out->cc_minor = p.minor;
+  out->smem_optin_bytes = int64_t(p.sharedMemPerBlockOptin);
+  out->l2_bytes = int64_t(p.l2CacheSize);
+  out->global_mem_bytes = int64_t(p.totalGlobalMem);
+  snprintf(out->name, sizeof(out->name), "%s", p.name);
+  return SBW_OK;
+}
+
+size_t sbw_nl_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi) {
+  (void)m;
+  return k3_scratch_bytes(n, v_lo, v_hi);
+}
+
+int sbw_nl(const void* d_table, int table_bytes, int n, int m, uint32_t v_lo, uint32_t v_hi,
+           int32_t* d_max_abs, unsigned long long* d_key, void* scratch, size_t scratch_bytes,
+           void* stream) {
+  if (int rc = check_nm(n, m)) return rc;
+  if (int rc = check_table(d_table, table_bytes, m)) return rc;
+  if (int rc = check_range(m, v_lo, v_hi)) return rc;
+  if (!d_max_abs) return set_error(SBW_EINVAL, "null max_abs output");
+  if (n <= 16)
+    return launch_fused_onchip(d_table, table_bytes, n, v_lo, v_hi, d_max_abs, d_key, nullptr, 0,
+                               as_stream(stream));
+  return launch_k3(d_table, table_bytes, n, v_lo, v_hi, d_max_abs, d_key, nullptr, 0, scratch,
+                   scratch_bytes, as_stream(stream));
+}
+
+size_t sbw_spectrum_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi, int layout) {
+  (void)m;
+  size_t s = k3_scratch_bytes(n, v_lo, v_hi);
+  if (layout == SBW_LAYOUT_X_MAJOR) s += (size_t(v_hi) - v_lo) * (size_t(4) << n);
+  return s;
+}
+
+int sbw_spectrum(const void* d_table, int table_bytes, int n, int m, uint32_t v_lo,
+                 uint32_t v_hi, int layout, int32_t* d_out, int64_t ld, int32_t* d_max_abs,
+                 void* scratch, size_t scratch_bytes, void* stream) {
+  if (int rc = check_nm(n, m)) return rc;
+  if (int rc = check_table(d_table, table_bytes, m)) return rc;
+  if (int rc = check_range(m, v_lo, v_hi)) return rc;
+  if (!d_out) return set_error(SBW_EINVAL, "null output");
+  const int64_t rows = int64_t(v_hi) - int64_t(v_lo), cols = int64_t(1) << n;
+  cudaStream_t st = as_stream(stream);
+  int32_t* mx = d_max_abs;
+  if (rows == 0) return SBW_OK;
+  if (layout != SBW_LAYOUT_MASK_MAJOR && layout != SBW_LAYOUT_X_MAJOR)
+    return set_error(SBW_EINVAL, "layout must be 0 (mask-major) or 1 (x-major)");
+  if (layout == SBW_LAYOUT_MASK_MAJOR && ld < cols)
+    return set_error(SBW_EINVAL, "ld %lld < 2^n", (long long)ld);
+  if (layout == SBW_LAYOUT_X_MAJOR && ld < rows)
+    return set_error(SBW_EINVAL, "ld %lld < number of masks", (long long)ld);
+  const size_t k3 = k3_scratch_bytes(n, v_lo, v_hi);
+  const size_t need = sbw_spectrum_scratch_bytes(n, m, v_lo, v_hi, layout);
+  if (need && (scratch == nullptr || scratch_bytes < need))
+    return set_error(SBW_EINVAL, "spectrum needs %zu scratch bytes, got %zu", need, scratch_bytes);
+  int32_t* own_mx = nullptr;
+  if (mx == nullptr) {
+    SBW_CUDA_CHECK(cudaMallocAsync(&own_mx, sizeof(int32_t) * rows, st));
+    mx = own_mx;
+  }
+  int32_t* rows_out = d_out;
+  int64_t rows_ld = ld;
+  if (layout == SBW_LAYOUT_X_MAJOR) {
+    rows_out = reinterpret_cast<int32_t*>(static_cast<char*>(scratch) + k3);
+    rows_ld = cols;
+  }
+  int rc;
+  if (n <= 16)
+    rc = launch_fused_onchip(d_table, table_bytes, n, v_lo, v_hi, mx, nullptr, rows_out, rows_ld,
+                             st);
+  else
+    rc = launch_k3(d_table, table_bytes, n, v_lo, v_hi, mx, nullptr, rows_out, rows_ld, scratch,
+                   k3, st);
+  if (rc == SBW_OK && layout == SBW_LAYOUT_X_MAJOR)
+    rc = launch_transpose_i32(rows_out, rows, cols, cols, d_out, ld, st);
+  if (own_mx) cudaFreeAsync(own_mx, st);
+  return rc;
+}
+
+int sbw_polarity(const void* d_table, int table_bytes, int n, int m, uint32_t v_lo,
+                 uint32_t v_hi, int layout, int32_t* d_out, int64_t ld, void* stream) {
+  if (int rc = check_nm(n, m)) return rc;
+  if (int rc = check_table(d_table, table_bytes, m)) return rc;
+  // polarity rows may include the constant v = 0 row (polarity_row(s, 0))
+  if (v_lo > v_hi || uint64_t(v_hi) > (uint64_t(1) << m))
+    return set_error(SBW_ERANGE, "mask range [%u, %u) outside [0, 2^%d)", v_lo, v_hi, m);
+  if (!d_out) return set_error(SBW_EINVAL, "null output");
+  if (layout != SBW_LAYOUT_MASK_MAJOR && layout != SBW_LAYOUT_X_MAJOR)
+    return set_error(SBW_EINVAL, "layout must be 0 (mask-major) or 1 (x-major)");
+  return launch_polarity(d_table, table_bytes, n, v_lo, v_hi, layout, d_out, ld,
+                         as_stream(stream));
+}
+
+int sbw_fwht_inplace(int32_t* d_data, int k, int64_t count, int64_t* d_max_abs, void* stream) {
+  if (k < 0 || k > 30) return set_error(SBW_EINVAL, "column length must be 2^k, k in 0..30");
+  if (count < 0) return set_error(SBW_EINVAL, "negative column count");
+  if (count > 0 && !d_data) return set_error(SBW_EINVAL, "null data");
+  return inplace_fwht(d_data, k, count, reinterpret_cast<long long*>(d_max_abs),
+                      as_stream(stream));
+}
+
+__global__ void k_fill_ll(long long* p, long long v) { *p = v; }
+
+int sbw_maxabs_to_nl(const int32_t* d_max_abs, int64_t count, int n, int64_t* d_nl,
+                     int64_t* d_bad, void* stream) {
+  if (n < 0 || n > 30) return set_error(SBW_EINVAL, "bad n");
+  cudaStream_t st = as_stream(stream);
+  k_fill_ll<<<1, 1, 0, st>>>(reinterpret_cast<long long*>(d_bad), LLONG_MAX);
+  SBW_LAUNCH_CHECK("k_fill_ll");
+  return launch_maxabs_to_nl(d_max_abs, count, n, reinterpret_cast<long long*>(d_nl),
+                             reinterpret_cast<long long*>(d_bad), st);
+}
+
+int sbw_maxabs64_to_nl(const int64_t* d_max_abs, int64_t count, int64_t pw, int64_t* d_nl,
+                       int64_t* d_bad, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  k_fill_ll<<<1, 1, 0, st>>>(reinterpret_cast<long long*>(d_bad), LLONG_MAX);
+  SBW_LAUNCH_CHECK("k_fill_ll");
+  return launch_maxabs64_to_nl(reinterpret_cast<const long long*>(d_max_abs), count, pw,
+                               reinterpret_cast<long long*>(d_nl),
+                               reinterpret_cast<long long*>(d_bad), st);
+}
+
+int sbw_row_maxabs(const int32_t* d_rows, int64_t rows, int64_t cols, int64_t ld,
+                   int64_t* d_row_max, unsigned long long* d_key, void* stream) {
+  if (rows < 0 || cols < 1 || ld < cols) return set_error(SBW_EINVAL, "bad spectrum shape");
+  return launch_row_maxabs(d_rows, rows, cols, ld, reinterpret_cast<long long*>(d_row_max), d_key,
+                           as_stream(stream));
+}
+
+int sbw_walsh_direct(const void* d_table, int table_bytes, int n, int m, const uint32_t* d_u,
+                     const uint32_t* d_v, int64_t count, int32_t* d_out, void* stream) {
+  if (int rc = check_nm(n, m)) return rc;
+  if (int rc = check_table(d_table, table_bytes, m)) return rc;
+  return launch_walsh_direct(d_table, table_bytes, n, d_u, d_v, count, d_out, as_stream(stream));
+}
+
+int sbw_nl_bruteforce(const void* d_table, int table_bytes, int n, int m, int32_t* d_best,
+                      void* stream) {
+  if (int rc = check_nm(n, m)) return rc;
+  if (n > 8 || m > 8) return set_error(SBW_EINVAL, "brute force capped at 8 bits, got %dx%d", n, m);
+  if (int rc = check_table(d_table, table_bytes, m)) return rc;
+  return launch_bruteforce(d_table, table_bytes, n, m, d_best, as_stream(stream));
+}
+
+int sbw_nl_host(const uint32_t* h_table, int n, int m, uint32_t v_lo, uint32_t v_hi,
+                int64_t* h_nl, int64_t* out3, int device) {
+  if (int rc = check_nm(n, m)) return rc;
+  if (int rc = check_range(m, v_lo, v_hi)) return rc;
+  if (!h_table) return set_error(SBW_EINVAL, "null host table");
+  SBW_CUDA_CHECK(cudaSetDevice(device));
+  cudaStream_t st;
+  SBW_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const int64_t nx = int64_t(1) << n, nv = int64_t(v_hi) - int64_t(v_lo);
+  const int tb = m <= 16 ? 2 : 4;
+  // narrow the uint32 table on the host side of the copy: a staging buffer
+  void* h_stage = nullptr;
+  void* d_table = nullptr;
+  int32_t* d_mx = nullptr;
+  long long* d_nl = nullptr;
+  long long* d_bad = nullptr;
+  unsigned long long* d_key = nullptr;
+  void* scratch = nullptr;
+  const size_t sb = k3_scratch_bytes(n, v_lo, v_hi);
+  int rc = SBW_OK;
+  long long bad = LLONG_MAX;
+  unsigned long long key = 0;
+  auto fail = [&](cudaError_t e, const char* w) { rc = cuda_error(e, w); };
+  cudaError_t e;
+  if ((e = cudaMallocHost(&h_stage, size_t(nx) * tb)) != cudaSuccess) { fail(e, "cudaMallocHost"); goto done; }
+  if (tb == 2) {
+    uint16_t* s = static_cast<uint16_t*>(h_stage);
+    for (int64_t i = 0; i < nx; ++i) s[i] = uint16_t(h_table[i]);
+  } else {
+    memcpy(h_stage, h_table, size_t(nx) * 4);
+  }
+  if ((e = cudaMallocAsync(&d_table, size_t(nx) * tb + 16, st)) != cudaSuccess) { fail(e, "malloc table"); goto done; }
+  if ((e = cudaMallocAsync(&d_mx, sizeof(int32_t) * (nv + 1), st)) != cudaSuccess) { fail(e, "malloc max"); goto done; }
+  if ((e = cudaMallocAsync(&d_nl, sizeof(long long) * (nv + 1), st)) != cudaSuccess) { fail(e, "malloc nl"); goto done; }
+  if ((e = cudaMallocAsync(&d_bad, sizeof(long long), st)) != cudaSuccess) { fail(e, "malloc bad"); goto done; }
+  if ((e = cudaMallocAsync(&d_key, sizeof(unsigned long long), st)) != cudaSuccess) { fail(e, "malloc key"); goto done; }
+  if (sb && (e = cudaMallocAsync(&scratch, sb, st)) != cudaSuccess) { fail(e, "malloc scratch"); goto done; }
+  if ((e = cudaMemcpyAsync(d_table, h_stage, size_t(nx) * tb, cudaMemcpyHostToDevice, st)) != cudaSuccess) { fail(e, "H2D table"); goto done; }
+  if ((e = cudaMemsetAsync(d_key, 0, sizeof(unsigned long long), st)) != cudaSuccess) { fail(e, "memset key"); goto done; }
+  rc = sbw_nl(d_table, tb, n, m, v_lo, v_hi, d_mx, d_key, scratch, sb, st);
+  if (rc) goto done;
+  rc = sbw_maxabs_to_nl(d_mx, nv, n, reinterpret_cast<int64_t*>(d_nl), reinterpret_cast<int64_t*>(d_bad), st);
+  if (rc) goto done;
+  if (h_nl && (e = cudaMemcpyAsync(h_nl, d_nl, sizeof(long long) * nv, cudaMemcpyDeviceToHost, st)) != cudaSuccess) { fail(e, "D2H nl"); goto done; }
+  if ((e = cudaMemcpyAsync(&key, d_key, sizeof(key), cudaMemcpyDeviceToHost, st)) != cudaSuccess) { fail(e, "D2H key"); goto done; }
+  if ((e = cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st)) != cudaSuccess) { fail(e, "D2H bad"); goto done; }
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { fail(e, "sync"); goto done; }
+  if (bad != LLONG_MAX) {
+    rc = set_error(SBW_EPARITY, "odd spectrum gap at mask %lld", (long long)(v_lo + bad));
+    goto done;
+  }
+  if (out3) {
+    const int64_t mxw = int64_t(key >> 32);
+    out3[0] = (nx - mxw) >> 1;
+    out3[1] = int64_t(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
+    out3[2] = mxw;
+  }
+done:
+  if (scratch) cudaFreeAsync(scratch, st);
+  if (d_key) cudaFreeAsync(d_key, st);
+  if (d_bad) cudaFreeAsync(d_bad, st);
+  if (d_nl) cudaFreeAsync(d_nl, st);
+  if (d_mx) cudaFreeAsync(d_mx, st);
+  if (d_table) cudaFreeAsync(d_table, st);
+  cudaStreamSynchronize(st);
+  if (h_stage) cudaFreeHost(h_stage);
+  cudaStreamDestroy(st);
+  return rc;
+}
+
+int sbw_int32_peak(double* ops_per_s, double* ms, void* stream) {
+  if (!ops_per_s) return set_error(SBW_EINVAL, "null output");
+  return run_int32_peak(ops_per_s, ms, as_stream(stream));
+}
+
+}  // extern "C"

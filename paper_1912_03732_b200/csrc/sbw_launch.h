@@ -1,0 +1,45 @@
+// Host-side launchers shared between the libsbw translation units.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace sbw {
+
+// Fused on-chip path (n <= 16): NL (out == nullptr) or mask-major SPEC rows.
+int launch_fused_onchip(const void* table, int tbytes, int n, uint32_t v_lo, uint32_t v_hi,
+                        int32_t* max_abs, unsigned long long* key, int32_t* out, int64_t ld,
+                        cudaStream_t st);
+
+// Multi-pass path (n >= 17): pass A (emit) + pass B per L2-sized batch.
+size_t k3_scratch_bytes(int n, uint32_t v_lo, uint32_t v_hi);
+int launch_k3(const void* table, int tbytes, int n, uint32_t v_lo, uint32_t v_hi,
+              int32_t* max_abs, unsigned long long* key, int32_t* out, int64_t ld, void* scratch,
+              size_t scratch_bytes, cudaStream_t st);
+
+// Pass A only (exposed for the launcher above).
+int launch_emit_tile(const void* table, int tbytes, int n, uint32_t v_first, int64_t n_comp,
+                     uint32_t* emit, cudaStream_t st);
+
+// Misc kernels.
+int launch_transpose_i32(const int32_t* in, int64_t rows, int64_t cols, int64_t ld_in,
+                         int32_t* out, int64_t ld_out, cudaStream_t st);
+int launch_fill_i32(int32_t* p, int64_t count, int32_t value, cudaStream_t st);
+int inplace_fwht(int32_t* d, int k, int64_t count, long long* max_abs, cudaStream_t st);
+int launch_polarity(const void* table, int tbytes, int n, uint32_t v_lo, uint32_t v_hi,
+                    int layout, int32_t* out, int64_t ld, cudaStream_t st);
+int launch_maxabs_to_nl(const int32_t* mx, int64_t count, int n, long long* nl, long long* bad,
+                        cudaStream_t st);
+int launch_maxabs64_to_nl(const long long* mx, int64_t count, long long pw, long long* nl,
+                          long long* bad, cudaStream_t st);
+int launch_row_maxabs(const int32_t* rows, int64_t nrows, int64_t cols, int64_t ld,
+                      long long* row_max, unsigned long long* key, cudaStream_t st);
+int launch_walsh_direct(const void* table, int tbytes, int n, const uint32_t* u,
+                        const uint32_t* v, int64_t count, int32_t* out, cudaStream_t st);
+int launch_bruteforce(const void* table, int tbytes, int n, int m, int32_t* best,
+                      cudaStream_t st);
+int run_int32_peak(double* ops_per_s, double* ms_out, cudaStream_t st);
+
+}  // namespace sbw

@@ -1,0 +1,465 @@
+// Supporting kernels of libsbw: the generic int32 in-place FWHT, polarity
+// truth tables, the layout transpose, the reducers, the direct-sum and
+// affine-distance checkers and the INT32 peak microbenchmark.
+#include <climits>
+
+#include "sbw_internal.cuh"
+#include "sbw_launch.h"
+
+namespace sbw {
+
+// ---------------------------------------------------------------------------
+// Generic int32 FWHT (fwht_column_in_place, walsh.py:73-104;
+// transform_rows_in_place, walsh.py:140-152).  General int32 input with
+// numpy's wrap-around arithmetic, so stages run in int32 on global memory in
+// passes of up to 6 bits: element e = hi*2^(b0+NB) + i*2^b0 + lo.
+// ---------------------------------------------------------------------------
+template <int NB>
+__global__ void __launch_bounds__(256) k_inplace_pass(int32_t* __restrict__ d, int k, int b0,
+                                                      int64_t count, long long* max_abs) {
+  constexpr int L = 1 << NB;
+  const int64_t per_col = int64_t(1) << (k - NB);
+  const int64_t total = count * per_col;
+  const int64_t lo_mask = (int64_t(1) << b0) - 1;
+  // warp-uniform loop control so the warp-level reduction below is safe
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t wb = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); wb < total;
+       wb += stride) {
+    const int64_t t = wb + (threadIdx.x & 31);
+    const bool ok = t < total;
+    const int64_t col = ok ? t / per_col : 0;
+    int mx = INT_MIN;
+    if (ok) {
+      const int64_t r = t - col * per_col;
+      const int64_t lo = r & lo_mask, hi = r >> b0;
+      int32_t* p = d + (col << k) + (hi << (b0 + NB)) + lo;
+      int e[L];
+#pragma unroll
+      for (int i = 0; i < L; ++i) e[i] = p[int64_t(i) << b0];
+      // wrap-around adds: do the arithmetic in uint32 (well-defined overflow)
+#pragma unroll
+      for (int s = 1; s < L; s <<= 1) {
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+          if ((i & s) == 0) {
+            const uint32_t a = uint32_t(e[i]), b = uint32_t(e[i + s]);
+            e[i] = int(a + b);
+            e[i + s] = int(a - b);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < L; ++i) {
+        p[int64_t(i) << b0] = e[i];
+        mx = max(mx, wrap_abs(e[i]));
+      }
+    }
+    if (max_abs) {
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      if (ok) {
+        const long long col0 = __shfl_sync(m, col, __ffs(m) - 1);
+        if (__all_sync(m, col == col0)) {
+          const int wm = __reduce_max_sync(m, unsigned(mx) ^ 0x80000000u) ^ 0x80000000u;
+          if ((threadIdx.x & 31) == __ffs(m) - 1) atomicMax(max_abs + col, (long long)wm);
+        } else {
+          atomicMax(max_abs + col, (long long)mx);
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_fill_i64(long long* p, int64_t count, long long v) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_fill_i32(int32_t* p, int64_t count, int32_t v) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+// length-1 columns: no stage runs; the reference returns abs(int(col[0]))
+// as a Python int (walsh.py:88-89), i.e. the true absolute value.
+__global__ void k_len1_abs(const int32_t* d, int64_t count, long long* max_abs) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const long long x = d[i];
+    max_abs[i] = x < 0 ? -x : x;
+  }
+}
+
+int grid_for(int64_t work, int per_block, int cap_per_sm = 8) {
+  DeviceProps dp;
+  if (device_props(&dp)) return 1;
+  int64_t g = (work + per_block - 1) / per_block;
+  const int64_t cap = int64_t(dp.sm_count) * cap_per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return int(g);
+}
+
+int launch_fill_i32(int32_t* p, int64_t count, int32_t value, cudaStream_t st) {
+  if (count <= 0) return SBW_OK;
+  k_fill_i32<<<grid_for(count, 256), 256, 0, st>>>(p, count, value);
+  SBW_LAUNCH_CHECK("k_fill_i32");
+  return SBW_OK;
+}
+
+int inplace_fwht(int32_t* d, int k, int64_t count, long long* max_abs, cudaStream_t st) {
+  if (count <= 0) return SBW_OK;
+  if (k == 0) {
+    if (max_abs) {
+      k_len1_abs<<<grid_for(count, 256), 256, 0, st>>>(d, count, max_abs);
+      SBW_LAUNCH_CHECK("k_len1_abs");
+    }
+    return SBW_OK;
+  }
+  if (max_abs) {
+    k_fill_i64<<<grid_for(count, 256), 256, 0, st>>>(max_abs, count, (long long)INT_MIN);
+    SBW_LAUNCH_CHECK("k_fill_i64");
+  }
+  int b0 = 0;
+  while (b0 < k) {
+    const int nb = (k - b0) < 6 ? (k - b0) : 6;
+    const bool last = b0 + nb == k;
+    long long* mx = last ? max_abs : nullptr;
+    const int64_t tasks = count << (k - nb);
+    const int grid = grid_for(tasks, 256);
+    switch (nb) {
+      case 1: k_inplace_pass<1><<<grid, 256, 0, st>>>(d, k, b0, count, mx); break;
+      case 2: k_inplace_pass<2><<<grid, 256, 0, st>>>(d, k, b0, count, mx); break;
+      case 3: k_inplace_pass<3><<<grid, 256, 0, st>>>(d, k, b0, count, mx); break;
+      case 4: k_inplace_pass<4><<<grid, 256, 0, st>>>(d, k, b0, count, mx); break;
+      case 5: k_inplace_pass<5><<<grid, 256, 0, st>>>(d, k, b0, count, mx); break;
+      default: k_inplace_pass<6><<<grid, 256, 0, st>>>(d, k, b0, count, mx); break;
+    }
+    SBW_LAUNCH_CHECK("k_inplace_pass");
+    b0 += nb;
+  }
+  return SBW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Polarity truth table (polarity_row / polarity_truth_table, sbox.py:145-162;
+// x-major build_polarity_xmajor, walsh.py:117-131).
+// ---------------------------------------------------------------------------
+template <typename TT>
+__global__ void k_polarity(const TT* __restrict__ table, int n, uint32_t v_lo, int64_t nv,
+                           int layout, int32_t* __restrict__ out, int64_t ld) {
+  const int64_t nx = int64_t(1) << n;
+  const int64_t total = nv * nx;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    if (layout == SBW_LAYOUT_MASK_MAJOR) {
+      const int64_t r = i >> n, x = i & (nx - 1);
+      out[r * ld + x] = polarity(uint32_t(table[x]), v_lo + uint32_t(r));
+    } else {
+      const int64_t x = i / nv, r = i - x * nv;
+      out[x * ld + r] = polarity(uint32_t(table[x]), v_lo + uint32_t(r));
+    }
+  }
+}
+
+int launch_polarity(const void* table, int tbytes, int n, uint32_t v_lo, uint32_t v_hi,
+                    int layout, int32_t* out, int64_t ld, cudaStream_t st) {
+  const int64_t nv = int64_t(v_hi) - int64_t(v_lo);
+  if (nv <= 0) return SBW_OK;
+  const int grid = grid_for(nv << n, 256, 16);
+  if (tbytes == 2)
+    k_polarity<uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(table), n, v_lo, nv,
+                                                layout, out, ld);
+  else
+    k_polarity<uint32_t><<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(table), n, v_lo, nv,
+                                                layout, out, ld);
+  SBW_LAUNCH_CHECK("k_polarity");
+  return SBW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// 32x32 tiled transpose: mask-major rows -> x-major (walsh.py:174 is the
+// reference's inverse copy `np.ascontiguousarray(wt.T)`).
+// ---------------------------------------------------------------------------
+__global__ void k_transpose(const int32_t* __restrict__ in, int64_t rows, int64_t cols,
+                            int64_t ld_in, int32_t* __restrict__ out, int64_t ld_out) {
+  __shared__ int32_t t[32][33];
+  const int64_t tiles_c = (cols + 31) / 32;
+  const int64_t tiles = ((rows + 31) / 32) * tiles_c;
+  for (int64_t b = blockIdx.x; b < tiles; b += gridDim.x) {
+    const int64_t r0 = (b / tiles_c) * 32, c0 = (b % tiles_c) * 32;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+      const int64_t r = r0 + j, c = c0 + threadIdx.x;
+      if (r < rows && c < cols) t[j][threadIdx.x] = in[r * ld_in + c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+      const int64_t c = c0 + j, r = r0 + threadIdx.x;
+      if (r < rows && c < cols) out[c * ld_out + r] = t[threadIdx.x][j];
+    }
+    __syncthreads();
+  }
+}
+
+int launch_transpose_i32(const int32_t* in, int64_t rows, int64_t cols, int64_t ld_in,
+                         int32_t* out, int64_t ld_out, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return SBW_OK;
+  const int64_t tiles = ((rows + 31) / 32) * ((cols + 31) / 32);
+  k_transpose<<<grid_for(tiles, 1, 16), dim3(32, 8), 0, st>>>(in, rows, cols, ld_in, out, ld_out);
+  SBW_LAUNCH_CHECK("k_transpose");
+  return SBW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Reducers.
+// ---------------------------------------------------------------------------
+// max|W| -> NL with the odd-gap check (column_nonlinearity, walsh.py:107-114)
+__global__ void k_maxabs_to_nl(const int32_t* mx, int64_t count, long long pw, long long* nl,
+                               long long* bad) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const long long diff = pw - (long long)mx[i];
+    if (diff & 1) atomicMin(bad, (long long)i);  // caller initialises *bad = LLONG_MAX
+    nl[i] = diff >> 1;
+  }
+}
+__global__ void k_maxabs64_to_nl(const long long* mx, int64_t count, long long pw,
+                                 long long* nl, long long* bad) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const long long diff = pw - mx[i];
+    if (diff & 1) atomicMin(bad, (long long)i);
+    nl[i] = diff >> 1;
+  }
+}
+
+int launch_maxabs_to_nl(const int32_t* mx, int64_t count, int n, long long* nl, long long* bad,
+                        cudaStream_t st) {
+  if (count <= 0) return SBW_OK;
+  k_maxabs_to_nl<<<grid_for(count, 256), 256, 0, st>>>(mx, count, 1ll << n, nl, bad);
+  SBW_LAUNCH_CHECK("k_maxabs_to_nl");
+  return SBW_OK;
+}
+int launch_maxabs64_to_nl(const long long* mx, int64_t count, long long pw, long long* nl,
+                          long long* bad, cudaStream_t st) {
+  if (count <= 0) return SBW_OK;
+  k_maxabs64_to_nl<<<grid_for(count, 256), 256, 0, st>>>(mx, count, pw, nl, bad);
+  SBW_LAUNCH_CHECK("k_maxabs64_to_nl");
+  return SBW_OK;
+}
+
+// spectrum scan: row_max = max(rows.max, -rows.min) in int64 (nonlinearity.py:41-43)
+__global__ void __launch_bounds__(256) k_row_maxabs(const int32_t* __restrict__ rows, int64_t nrows,
+                                                    int64_t cols, int64_t ld, long long* row_max,
+                                                    unsigned long long* key) {
+  __shared__ int s_hi[8], s_lo[8];
+  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+    const int32_t* p = rows + r * ld;
+    int hi = INT_MIN, lo = INT_MAX;
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+      const int x = p[c];
+      hi = max(hi, x);
+      lo = min(lo, x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s_hi[threadIdx.x >> 5] = hi;
+      s_lo[threadIdx.x >> 5] = lo;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+        hi = max(hi, s_hi[w]);
+        lo = min(lo, s_lo[w]);
+      }
+      const long long m = max((long long)hi, -(long long)lo);
+      row_max[r] = m;
+      if (key)
+        atomicMax(key, (static_cast<unsigned long long>(m) << 32) |
+                           (0xFFFFFFFFull - static_cast<unsigned long long>(r)));
+    }
+    __syncthreads();
+  }
+}
+
+int launch_row_maxabs(const int32_t* rows, int64_t nrows, int64_t cols, int64_t ld,
+                      long long* row_max, unsigned long long* key, cudaStream_t st) {
+  if (nrows <= 0) return SBW_OK;
+  k_row_maxabs<<<grid_for(nrows, 1, 16), 256, 0, st>>>(rows, nrows, cols, ld, row_max, key);
+  SBW_LAUNCH_CHECK("k_row_maxabs");
+  return SBW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Direct sum W(u,v) (walsh_direct, walsh.py:56-70): one CTA per pair.
+// ---------------------------------------------------------------------------
+template <typename TT>
+__global__ void __launch_bounds__(256) k_walsh_direct(const TT* __restrict__ table, int n,
+                                                      const uint32_t* u, const uint32_t* v,
+                                                      int64_t count, int32_t* out) {
+  __shared__ long long s[8];
+  const int64_t nx = int64_t(1) << n;
+  for (int64_t p = blockIdx.x; p < count; p += gridDim.x) {
+    const uint32_t uu = u[p], vv = v[p];
+    long long ones = 0;
+    for (int64_t x = threadIdx.x; x < nx; x += blockDim.x)
+      ones += (__popc(uint32_t(table[x]) & vv) ^ __popc(uint32_t(x) & uu)) & 1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ones += __shfl_xor_sync(0xffffffffu, ones, o);
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = ones;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long tot = 0;
+      for (int w = 0; w < int(blockDim.x >> 5); ++w) tot += s[w];
+      out[p] = int32_t(nx - 2 * tot);
+    }
+    __syncthreads();
+  }
+}
+
+int launch_walsh_direct(const void* table, int tbytes, int n, const uint32_t* u,
+                        const uint32_t* v, int64_t count, int32_t* out, cudaStream_t st) {
+  if (count <= 0) return SBW_OK;
+  const int grid = grid_for(count, 1, 16);
+  if (tbytes == 2)
+    k_walsh_direct<uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(table), n, u, v,
+                                                    count, out);
+  else
+    k_walsh_direct<uint32_t><<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(table), n, u, v,
+                                                    count, out);
+  SBW_LAUNCH_CHECK("k_walsh_direct");
+  return SBW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Affine-distance brute force (nonlinearity_bruteforce, nonlinearity.py:59-86)
+// for n, m <= 8: g_v and every linear function as 2^n-bit strings; one CTA
+// per mask, one thread per linear mask w.
+// ---------------------------------------------------------------------------
+template <typename TT>
+__global__ void __launch_bounds__(256) k_bruteforce(const TT* __restrict__ table, int n, int m,
+                                                    int32_t* best) {
+  __shared__ uint32_t g[8];
+  __shared__ int s_min[8];
+  const int nx = 1 << n;
+  const int words = (nx + 31) / 32;
+  for (int v = blockIdx.x + 1; v < (1 << m); v += gridDim.x) {
+    if (threadIdx.x < 8) g[threadIdx.x] = 0;
+    __syncthreads();
+    for (int x = threadIdx.x; x < nx; x += blockDim.x)
+      if (__popc(uint32_t(table[x]) & uint32_t(v)) & 1) atomicOr(&g[x >> 5], 1u << (x & 31));
+    __syncthreads();
+    int mine = nx;
+    for (int w = threadIdx.x; w < nx; w += blockDim.x) {
+      int d = 0;
+      for (int k = 0; k < words; ++k) {
+        uint32_t lin = 0;
+        const int cnt = nx - 32 * k < 32 ? nx - 32 * k : 32;
+        for (int b = 0; b < cnt; ++b) lin |= uint32_t(__popc(uint32_t(32 * k + b) & uint32_t(w)) & 1) << b;
+        d += __popc(lin ^ g[k]);
+      }
+      mine = min(mine, min(d, nx - d));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine = min(mine, __shfl_xor_sync(0xffffffffu, mine, o));
+    if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int b = nx;
+      for (int w = 0; w < int(blockDim.x >> 5); ++w) b = min(b, s_min[w]);
+      best[v - 1] = b;
+    }
+    __syncthreads();
+  }
+}
+
+int launch_bruteforce(const void* table, int tbytes, int n, int m, int32_t* best,
+                      cudaStream_t st) {
+  const int grid = grid_for((1 << m) - 1, 1, 16);
+  if (tbytes == 2)
+    k_bruteforce<uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(table), n, m, best);
+  else
+    k_bruteforce<uint32_t><<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(table), n, m, best);
+  SBW_LAUNCH_CHECK("k_bruteforce");
+  return SBW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// INT32 ALU peak microbenchmark.  8 independent dependency chains per
+// thread; MODE 0: add/sub pairs (IADD3, ALU pipe), MODE 1: multiply-add with
+// a runtime multiplier (IMAD, FMA pipe), MODE 2: both interleaved.  Each
+// executed lane-instruction counts as one integer op.
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(512) k_int32_peak(int iters, int mul, int32_t* sink) {
+  int x[8], y[8], z[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    x[i] = threadIdx.x + i;
+    y[i] = blockIdx.x * 7 + i;
+    z[i] = threadIdx.x ^ (i * 977);
+  }
+  const int c = mul, d = mul ^ 0x5bd1e995;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (MODE != 1) {
+          x[i] = x[i] + y[i];
+          y[i] = y[i] - x[i];
+        }
+        if (MODE != 0) z[i] = z[i] * c + d;
+      }
+    }
+  }
+  int s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s ^= x[i] ^ y[i] ^ z[i];
+  if (s == 0x7fffffff) sink[0] = s;
+}
+
+int run_int32_peak(double* ops_per_s, double* ms_out, cudaStream_t st) {
+  DeviceProps dp;
+  if (int rc = device_props(&dp)) return rc;
+  int32_t* sink = nullptr;
+  SBW_CUDA_CHECK(cudaMallocAsync(&sink, sizeof(int32_t), st));
+  cudaEvent_t e0, e1;
+  SBW_CUDA_CHECK(cudaEventCreate(&e0));
+  SBW_CUDA_CHECK(cudaEventCreate(&e1));
+  const int blocks = dp.sm_count * 4, threads = 512, iters = 4096;
+  double best = 0, best_ms = 0;
+  for (int mode = 0; mode < 3; ++mode) {
+    for (int rep = 0; rep < 3; ++rep) {
+      SBW_CUDA_CHECK(cudaEventRecord(e0, st));
+      if (mode == 0) k_int32_peak<0><<<blocks, threads, 0, st>>>(iters, 3, sink);
+      if (mode == 1) k_int32_peak<1><<<blocks, threads, 0, st>>>(iters, 3, sink);
+      if (mode == 2) k_int32_peak<2><<<blocks, threads, 0, st>>>(iters, 3, sink);
+      SBW_LAUNCH_CHECK("k_int32_peak");
+      SBW_CUDA_CHECK(cudaEventRecord(e1, st));
+      SBW_CUDA_CHECK(cudaEventSynchronize(e1));
+      float ms = 0;
+      SBW_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+      const double per_iter = mode == 0 ? 256.0 : (mode == 1 ? 128.0 : 384.0);
+      const double ops = double(blocks) * threads * iters * per_iter;
+      const double rate = ops / (ms * 1e-3);
+      if (rep > 0 && rate > best) {
+        best = rate;
+        best_ms = ms;
+      }
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  SBW_CUDA_CHECK(cudaFreeAsync(sink, st));
+  *ops_per_s = best;
+  if (ms_out) *ms_out = best_ms;
+  return SBW_OK;
+}
+
+}  // namespace sbw

@@ -1,0 +1,163 @@
+"""Mask-range sharding: the reference's column-parallel engine, GPU-first.
+
+`partition_columns` keeps the reference's balanced contiguous ranges
+(parallel.py:38-57).  `fwht_parallel` (parallel.py:64-133) maps those
+ranges -- the reference's thread-pool "workers" -- onto the visible GPUs
+round-robin as logical shards: every shard is one libsbw launch over its
+mask range, results land in disjoint slots, so output is bit-identical for
+any shard count.  `evaluate_distributed` is the multi-process form (one rank
+per GPU, torch.distributed): each rank owns one range, the per-component
+values are all-gathered and the (max|W|, smallest v) key is max-reduced --
+the only exchange on the path.
+"""
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from . import device as _dev
+from .accounting import charged, check_budget, memory_estimate
+from .records import ColumnMaxima, ColumnPartition, NonlinearityResult, SBox, WalshSpectrum
+from .transforms import component_max_abs_device, decode_key, maxabs_to_nl, spectrum_device
+
+
+def partition_columns(total_columns: int, workers: int) -> ColumnPartition:
+    """Split masks 1..total_columns into <= workers balanced contiguous ranges.
+
+    Sizes differ by at most one, the leading ranges take the remainder, and
+    more workers than columns degrade to singleton ranges.
+    """
+    if total_columns < 1:
+        raise ValueError(f"total_columns must be >= 1, got {total_columns}")
+    if workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+    k = min(workers, total_columns)
+    q, r = divmod(total_columns, k)
+    bounds = [1]
+    for i in range(k):
+        bounds.append(bounds[-1] + q + (1 if i < r else 0))
+    return ColumnPartition(tuple(zip(bounds[:-1], bounds[1:])), workers)
+
+
+def default_workers() -> int:
+    """Default logical shard count: one per visible GPU (at least 1)."""
+    try:
+        torch = _dev.torch_mod()
+        return max(1, torch.cuda.device_count())
+    except Exception:  # noqa: BLE001 - no torch/CUDA: still a valid count
+        return 1
+
+
+def _devices():
+    torch = _dev.torch_mod()
+    _dev.require_device()
+    return [torch.device("cuda", i) for i in range(torch.cuda.device_count())]
+
+
+def fwht_parallel(s: SBox, workers: int | None = None, mode: str = "retain",
+                  max_bytes: int | None = None,
+                  timings: dict | None = None) -> tuple[WalshSpectrum | None, ColumnMaxima]:
+    """Fused transform over `workers` mask-range shards spread across the GPUs.
+
+    Bit-identical to fwht_fused(s, mode) for every shard count.
+    """
+    if mode not in ("retain", "stream"):
+        raise ValueError(f"mode must be 'retain' or 'stream', got {mode!r}")
+    if workers is None:
+        workers = default_workers()
+    if workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+    part = partition_columns((1 << s.m) - 1, workers)
+    t0 = time.perf_counter()
+    if mode == "retain":
+        check_budget(((1 << s.m) - 1) * (1 << s.n) * 4, max_bytes)
+    else:
+        check_budget(memory_estimate(s.n, s.m, mode="stream", workers=len(part.ranges)),
+                     max_bytes)
+    devs = _devices()
+    values = np.empty((1 << s.m) - 1, dtype=np.int64)
+    rows = None
+    t1 = time.perf_counter()
+    pending = []
+    nbytes = ((1 << s.m) - 1) * (1 << s.n) * 4 if mode == "retain" else 0
+    with charged(nbytes):
+        if mode == "retain":
+            rows = np.empty(((1 << s.m) - 1, 1 << s.n), dtype=np.int32)
+        for i, (lo, hi) in enumerate(part.ranges):
+            dev = devs[i % len(devs)]
+            if mode == "retain":
+                spec, mx = spectrum_device(s, lo, hi, layout="mask", device=dev)
+            else:
+                spec, (mx, _key) = None, component_max_abs_device(s, lo, hi, device=dev)
+            pending.append((lo, hi, spec, mx))
+        for lo, hi, spec, mx in pending:  # completion barrier, in range order
+            values[lo - 1:hi - 1] = maxabs_to_nl(mx, s.n)
+            if spec is not None:
+                rows[lo - 1:hi - 1] = spec.cpu().numpy()
+        t2 = time.perf_counter()
+    if timings is not None:
+        timings["build_s"] = t1 - t0
+        timings["transform_s"] = t2 - t1
+    spectrum = WalshSpectrum(s.n, s.m, rows) if rows is not None else None
+    return spectrum, ColumnMaxima(s.n, s.m, values)
+
+
+# ---------------------------------------------------------------------------
+# multi-process (one rank per GPU) evaluation
+# ---------------------------------------------------------------------------
+def _gpu_shard(s: SBox, lo: int, hi: int):
+    """Default shard compute: fused NL on this rank's GPU -> (NL int64, key)."""
+    mx, key = component_max_abs_device(s, lo, hi)
+    return maxabs_to_nl(mx, s.n), int(key.item())
+
+
+def evaluate_distributed(s: SBox, group=None, compute=None,
+                         return_values: bool = True) -> tuple[NonlinearityResult, ColumnMaxima | None]:
+    """Whole-S-box NL with the masks sharded over the ranks of `group`.
+
+    Rank r owns partition_columns(2^m - 1, world)[r] (the reference's static
+    partition, parallel.py:38-57).  Exchange: one all-reduce(MAX) of the
+    packed (max|W| << 32 | ~v) key and, if `return_values`, one all-gather of
+    the padded per-component NL shards.  `compute(s, lo, hi) -> (nl_int64,
+    key)` defaults to the GPU; tests inject the CPU oracle to exercise the
+    exchange on gloo.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    total = (1 << s.m) - 1
+    part = partition_columns(total, world)
+    ranges = list(part.ranges) + [(total + 1, total + 1)] * (world - len(part.ranges))
+    lo, hi = ranges[rank]
+    compute = compute or _gpu_shard
+    if hi > lo:
+        nl, key = compute(s, lo, hi)
+    else:
+        nl, key = np.zeros(0, dtype=np.int64), 0
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    key_t = torch.tensor([key], dtype=torch.int64, device=dev)
+    dist.all_reduce(key_t, op=dist.ReduceOp.MAX, group=group)
+    k = int(key_t.item())
+    mxw = k >> 32
+    v = 0xFFFFFFFF - (k & 0xFFFFFFFF)
+    gap = (1 << s.n) - mxw
+    if gap & 1:
+        raise AssertionError("spectrum maximum has wrong parity")
+    result = NonlinearityResult(gap >> 1, v, "distributed")
+    cm = None
+    if return_values:
+        width = max(h - l for l, h in ranges)
+        buf = torch.full((width,), -1, dtype=torch.int64, device=dev)
+        buf[: hi - lo] = torch.from_numpy(np.asarray(nl, dtype=np.int64)).to(dev)
+        parts = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(parts, buf, group=group)
+        values = np.empty(total, dtype=np.int64)
+        for (l, h), p in zip(ranges, parts):
+            if h > l:
+                values[l - 1:h - 1] = p[: h - l].cpu().numpy()
+        cm = ColumnMaxima(s.n, s.m, values)
+    return result, cm

@@ -1,0 +1,302 @@
+"""Walsh spectra and fused per-component nonlinearity on the GPU.
+
+Public functions keep the reference's names, signatures, return types and
+exceptions (pkg/src/sboxeval/walsh.py:56-248) so the module is a drop-in;
+their bodies call libsbw's sm_100a kernels through device.py:
+
+  fwht_fused(mode="stream")  -> sbw_nl        (generate + FWHT + max, fused)
+  fwht_fused(mode="retain")  -> sbw_spectrum  (mask-major rows + maxima)
+  fwht_transposed            -> sbw_spectrum  (mask-major)
+  fwht_rowmajor              -> sbw_spectrum  (x-major store, returned
+                                               mask-major like walsh.py:174)
+  fwht_column_in_place       -> sbw_fwht_inplace
+  transform_rows_in_place    -> sbw_fwht_inplace + sbw_maxabs64_to_nl
+  walsh_direct               -> sbw_walsh_direct
+
+Device-resident variants (`*_device`) return torch tensors for callers that
+keep the (possibly 16 GiB) spectrum on the GPU.
+"""
+from __future__ import annotations
+
+import time
+from typing import IO
+
+import numpy as np
+
+from . import device as _dev
+from .accounting import charged, check_budget, memory_estimate
+from .records import ColumnMaxima, SBox, WalshSpectrum
+
+INT64_MAX = (1 << 63) - 1
+
+
+# ---------------------------------------------------------------------------
+# device-level building blocks
+# ---------------------------------------------------------------------------
+def _scratch(nbytes: int, dev):
+    torch = _dev.torch_mod()
+    if nbytes == 0:
+        return None
+    return torch.empty(nbytes, dtype=torch.uint8, device=dev)
+
+
+def component_max_abs_device(s: SBox, v_lo: int = 1, v_hi: int | None = None, device=None):
+    """Fused path: (max_abs int32[v_hi - v_lo], key uint64 as int64[1]) on the device.
+
+    key = (max|W| << 32) | (0xFFFFFFFF - v): max over the range, ties -> smallest v.
+    """
+    torch = _dev.torch_mod()
+    dev = _dev.require_device(device)
+    if v_hi is None:
+        v_hi = 1 << s.m
+    lib = _dev.load_library()
+    tab = _dev.device_table(s, dev)
+    mx = torch.empty(max(1, v_hi - v_lo), dtype=torch.int32, device=dev)
+    key = torch.zeros(1, dtype=torch.int64, device=dev)
+    nbytes = lib.sbw_nl_scratch_bytes(s.n, s.m, v_lo, v_hi)
+    scratch = _scratch(nbytes, dev)
+    with charged(nbytes):
+        _dev.check(lib.sbw_nl(_dev.ptr(tab), _dev.table_bytes(s.m), s.n, s.m, v_lo, v_hi,
+                              _dev.ptr(mx), _dev.ptr(key), _dev.ptr(scratch), nbytes,
+                              _dev.stream_handle(dev)))
+    return mx[: v_hi - v_lo], key
+
+
+def spectrum_device(s: SBox, v_lo: int = 1, v_hi: int | None = None, layout: str = "mask",
+                    device=None, out=None):
+    """Materialised spectrum on the device.
+
+    layout "mask": int32 [v_hi - v_lo, 2^n], rows[v - v_lo][u] = W(u, v);
+    layout "x":    int32 [2^n, v_hi - v_lo], the reference's x-major store
+                   wt[u][v - v_lo] (walsh.py:117-131).
+    Returns (spectrum tensor, max_abs int32 tensor).
+    """
+    torch = _dev.torch_mod()
+    dev = _dev.require_device(device)
+    if v_hi is None:
+        v_hi = 1 << s.m
+    lay = {"mask": _dev.LAYOUT_MASK_MAJOR, "x": _dev.LAYOUT_X_MAJOR}.get(layout)
+    if lay is None:
+        raise ValueError(f"layout must be 'mask' or 'x', got {layout!r}")
+    rows = v_hi - v_lo
+    shape = (rows, 1 << s.n) if lay == _dev.LAYOUT_MASK_MAJOR else (1 << s.n, rows)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.int32, device=dev)
+    elif tuple(out.shape) != shape or out.dtype != torch.int32 or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous int32 tensor of shape {shape}")
+    mx = torch.empty(max(1, rows), dtype=torch.int32, device=dev)
+    lib = _dev.load_library()
+    tab = _dev.device_table(s, dev)
+    nbytes = lib.sbw_spectrum_scratch_bytes(s.n, s.m, v_lo, v_hi, lay)
+    scratch = _scratch(nbytes, dev)
+    _dev.check(lib.sbw_spectrum(_dev.ptr(tab), _dev.table_bytes(s.m), s.n, s.m, v_lo, v_hi, lay,
+                                _dev.ptr(out), shape[1], _dev.ptr(mx), _dev.ptr(scratch), nbytes,
+                                _dev.stream_handle(dev)))
+    return out, mx[:rows]
+
+
+def maxabs_to_nl(max_abs, n: int) -> np.ndarray:
+    """Device max|W| -> host int64 NL per component (walsh.py:107-114)."""
+    torch = _dev.torch_mod()
+    dev = max_abs.device
+    count = max_abs.numel()
+    nl = torch.empty(max(1, count), dtype=torch.int64, device=dev)
+    bad = torch.empty(1, dtype=torch.int64, device=dev)
+    _dev.check(_dev.load_library().sbw_maxabs_to_nl(_dev.ptr(max_abs), count, n, _dev.ptr(nl),
+                                                    _dev.ptr(bad), _dev.stream_handle(dev)))
+    b = int(bad.item())
+    if b != INT64_MAX:
+        raise AssertionError(f"odd spectrum gap at component {b}: not a genuine Walsh column")
+    return nl[:count].cpu().numpy()
+
+
+def decode_key(key, n: int) -> tuple[int, int, int]:
+    """(NL, argmin_v, max|W|) from the packed device key."""
+    k = int(key.item()) & 0xFFFFFFFFFFFFFFFF
+    mx = k >> 32
+    v = 0xFFFFFFFF - (k & 0xFFFFFFFF)
+    gap = (1 << n) - mx
+    if gap & 1:
+        raise AssertionError("spectrum maximum has wrong parity")
+    return gap >> 1, v, mx
+
+
+def _sync(dev) -> None:
+    _dev.torch_mod().cuda.synchronize(dev)
+
+
+# ---------------------------------------------------------------------------
+# reference-compatible API
+# ---------------------------------------------------------------------------
+def walsh_direct(s: SBox, u: int, v: int) -> int:
+    """W(u, v) from the defining sum, evaluated on the GPU (walsh.py:56-70)."""
+    if not 0 <= u < (1 << s.n):
+        raise IndexError(f"input mask {u} out of range 0..{(1 << s.n) - 1}")
+    if not 0 <= v < (1 << s.m):
+        raise IndexError(f"output mask {v} out of range 0..{(1 << s.m) - 1}")
+    return int(walsh_direct_many(s, [u], [v])[0])
+
+
+def walsh_direct_many(s: SBox, us, vs, device=None) -> np.ndarray:
+    """Vectorised direct sums W(us[i], vs[i]) (GPU spot checker)."""
+    torch = _dev.torch_mod()
+    dev = _dev.require_device(device)
+    u = torch.as_tensor(np.asarray(us, dtype=np.uint32).view(np.int32)).to(dev)
+    v = torch.as_tensor(np.asarray(vs, dtype=np.uint32).view(np.int32)).to(dev)
+    out = torch.empty(max(1, u.numel()), dtype=torch.int32, device=dev)
+    tab = _dev.device_table(s, dev)
+    _dev.check(_dev.load_library().sbw_walsh_direct(
+        _dev.ptr(tab), _dev.table_bytes(s.m), s.n, s.m, _dev.ptr(u), _dev.ptr(v), u.numel(),
+        _dev.ptr(out), _dev.stream_handle(dev)))
+    return out[: u.numel()].cpu().numpy()
+
+
+def fwht_column_in_place(col: np.ndarray) -> tuple[np.ndarray, int]:
+    """In-place natural-order WHT of one int32 column (walsh.py:73-104).
+
+    Any uniformly strided 1-D int32 view is accepted; returns the column and
+    its max |entry| (numpy-int32 semantics, final stage; |x| for length 1).
+    """
+    length = col.shape[0]
+    if length == 0 or (length & (length - 1)) != 0:
+        raise ValueError(f"column length must be a power of two, got {length}")
+    if col.dtype != np.int32:
+        raise TypeError(f"column must be int32, got {col.dtype}")
+    mx = _inplace_rows(col.reshape(1, length))
+    return col, int(mx[0])
+
+
+def _inplace_rows(rows2d: np.ndarray) -> np.ndarray:
+    """Transform the rows of a (possibly strided) int32 matrix in place on the GPU."""
+    torch = _dev.torch_mod()
+    dev = _dev.require_device()
+    count, length = rows2d.shape
+    k = length.bit_length() - 1
+    d = torch.from_numpy(np.ascontiguousarray(rows2d)).to(dev)
+    mx = torch.empty(max(1, count), dtype=torch.int64, device=dev)
+    _dev.check(_dev.load_library().sbw_fwht_inplace(_dev.ptr(d), k, count, _dev.ptr(mx),
+                                                    _dev.stream_handle(dev)))
+    rows2d[...] = d.cpu().numpy()
+    return mx[:count].cpu().numpy()
+
+
+def transform_rows_in_place(rows: np.ndarray, maxima_out: np.ndarray | None = None) -> None:
+    """Butterfly every row of a mask-major store (walsh.py:140-152).
+
+    With `maxima_out`, row i's (2^k - max|W|) / 2 goes to maxima_out[i]; an
+    odd gap raises AssertionError like column_nonlinearity (walsh.py:107-114).
+    """
+    if rows.ndim != 2:
+        raise ValueError("rows must be a 2-D array")
+    count, length = rows.shape
+    if count == 0:
+        return
+    if length == 0 or (length & (length - 1)) != 0:
+        raise ValueError(f"column length must be a power of two, got {length}")
+    if rows.dtype != np.int32:
+        raise TypeError(f"rows must be int32, got {rows.dtype}")
+    mx = _inplace_rows(rows)
+    if maxima_out is not None:
+        gaps = length - mx
+        odd = np.flatnonzero(gaps & 1)
+        if odd.size:
+            raise AssertionError(
+                f"odd spectrum gap {int(gaps[odd[0]])}: column is not a genuine Walsh column")
+        maxima_out[:count] = gaps >> 1
+
+
+def _host_rows(t) -> np.ndarray:
+    return t.cpu().numpy()
+
+
+def fwht_rowmajor(s: SBox, max_bytes: int | None = None,
+                  timings: dict | None = None) -> WalshSpectrum:
+    """Spectrum through the x-major ("row", paper Alg. 1) store (walsh.py:155-180).
+
+    The GPU builds the x-major wt[u][v-1] matrix directly, then returns the
+    mask-major contiguous copy exactly as the reference does (walsh.py:174).
+    """
+    check_budget(memory_estimate(s.n, s.m, mode="retain"), max_bytes)
+    t0 = time.perf_counter()
+    dev = _dev.require_device()
+    torch = _dev.torch_mod()
+    nbytes = ((1 << s.m) - 1) * (1 << s.n) * 4
+    with charged(nbytes):
+        t1 = time.perf_counter()
+        wt, _ = spectrum_device(s, layout="x", device=dev)
+        rows_t = wt.t().contiguous()
+        del wt
+        _sync(dev)
+        t2 = time.perf_counter()
+        rows = _host_rows(rows_t)
+    del rows_t
+    torch.cuda.empty_cache() if nbytes > (1 << 30) else None
+    if timings is not None:
+        timings["build_s"] = t1 - t0
+        timings["transform_s"] = t2 - t1
+    return WalshSpectrum(s.n, s.m, rows)
+
+
+def fwht_transposed(s: SBox, max_bytes: int | None = None,
+                    timings: dict | None = None) -> WalshSpectrum:
+    """Spectrum through the mask-major store (walsh.py:183-201)."""
+    check_budget(((1 << s.m) - 1) * (1 << s.n) * 4, max_bytes)
+    t0 = time.perf_counter()
+    dev = _dev.require_device()
+    nbytes = ((1 << s.m) - 1) * (1 << s.n) * 4
+    with charged(nbytes):
+        t1 = time.perf_counter()
+        spec, _ = spectrum_device(s, layout="mask", device=dev)
+        _sync(dev)
+        t2 = time.perf_counter()
+        rows = _host_rows(spec)
+    if timings is not None:
+        timings["build_s"] = t1 - t0
+        timings["transform_s"] = t2 - t1
+    return WalshSpectrum(s.n, s.m, rows)
+
+
+def fwht_fused(s: SBox, mode: str = "retain", max_bytes: int | None = None,
+               timings: dict | None = None) -> tuple[WalshSpectrum | None, ColumnMaxima]:
+    """Transform fused with per-component max|W| (walsh.py:204-248, paper Alg. 3).
+
+    retain: spectrum materialised (mask-major) and returned with the maxima;
+    stream: generate -> FWHT -> max fused on chip, no spectrum anywhere.
+    """
+    if mode not in ("retain", "stream"):
+        raise ValueError(f"mode must be 'retain' or 'stream', got {mode!r}")
+    t0 = time.perf_counter()
+    if mode == "retain":
+        check_budget(((1 << s.m) - 1) * (1 << s.n) * 4, max_bytes)
+        dev = _dev.require_device()
+        nbytes = ((1 << s.m) - 1) * (1 << s.n) * 4
+        with charged(nbytes):
+            t1 = time.perf_counter()
+            spec, mx = spectrum_device(s, layout="mask", device=dev)
+            _sync(dev)
+            t2 = time.perf_counter()
+            rows = _host_rows(spec)
+        del spec
+        values = maxabs_to_nl(mx, s.n)
+        spectrum = WalshSpectrum(s.n, s.m, rows)
+    else:
+        check_budget(memory_estimate(s.n, s.m, mode="stream", workers=1), max_bytes)
+        dev = _dev.require_device()
+        t1 = time.perf_counter()
+        mx, _key = component_max_abs_device(s, device=dev)
+        _sync(dev)
+        t2 = time.perf_counter()
+        values = maxabs_to_nl(mx, s.n)
+        spectrum = None
+    if timings is not None:
+        timings["build_s"] = t1 - t0
+        timings["transform_s"] = t2 - t1
+    return spectrum, ColumnMaxima(s.n, s.m, values)
+
+
+def write_spectrum(w: WalshSpectrum, stream: IO[str]) -> None:
+    """Text dump: header "n m", then one line per mask v ascending (walsh.py:251-256)."""
+    stream.write(f"{w.n} {w.m}\n")
+    for row in w.rows:
+        stream.write(" ".join(map(str, row.tolist())))
+        stream.write("\n")

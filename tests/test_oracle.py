@@ -1,0 +1,142 @@
+"""Pin the CPU oracle (oracle/sbw_oracle.py) to the reference's own outputs.
+
+tests/golden/* were produced by tests/golden/make_golden.py running the
+reference package itself; every oracle function the GPU tests rely on is
+checked here against them.  CPU only.
+"""
+import numpy as np
+import pytest
+
+from oracle import sbw_oracle as orc
+from tests.util import sha
+
+CFG = {"8x8": (8, 8, True), "12x12": (12, 12, True), "16x16": (16, 16, True),
+       "20x20": (20, 20, False), "24x16": (24, 16, False)}
+
+
+@pytest.mark.parametrize("name", list(CFG))
+def test_seeded_tables_match_reference(golden, name):
+    n, m, bij = CFG[name]
+    t = orc.gen_table(n, m, 0, bij)
+    g = golden["configs"][name]
+    assert sha(t) == g["sha_table_u32"]
+    assert t[:4].tolist() == g["table_head"]
+
+
+def test_aes_spectrum_and_maxima(golden):
+    from paper_1912_03732_b200 import AES_SBOX
+
+    t = np.array(AES_SBOX, dtype=np.uint32)
+    rows = orc.spectrum(t, 8, 1, 256)
+    g = golden["aes"]
+    assert sha(rows) == g["sha_mask_major"]
+    assert sha(np.ascontiguousarray(rows.T)) == g["sha_x_major"]
+    nl = orc.component_nl(t, 8, 1, 256)
+    assert sha(nl) == g["sha_maxima_i64"]
+    assert orc.nl_from_maxima(nl) == (g["nl"], g["argmin_v"]) == (112, 1)
+    assert orc.nl_from_spectrum(rows, 8) == (112, 1)
+    assert int(np.abs(rows).max()) == 32
+
+
+@pytest.mark.parametrize("name", ["8x8", "12x12"])
+def test_materialised_configs(golden, golden_arrays, name):
+    n, m, bij = CFG[name]
+    t = orc.gen_table(n, m, 0, bij)
+    g = golden["configs"][name]
+    rows = orc.spectrum(t, n, 1, 1 << m)
+    assert sha(rows) == g["sha_mask_major"]
+    assert sha(np.ascontiguousarray(rows.T)) == g["sha_x_major"]
+    assert rows[0, :8].tolist() == g["w_v1_head"]
+    assert rows[-1, :8].tolist() == g["w_vlast_head"]
+    nl = orc.component_nl(t, n, 1, 1 << m)
+    assert sha(nl) == g["sha_maxima_i64"]
+    assert np.array_equal(nl, golden_arrays[f"maxima_{name}"])
+    assert orc.nl_from_maxima(nl) == (g["nl"], g["argmin_v"])
+    assert orc.nl_from_spectrum(rows, n) == (g["nl"], g["argmin_v"])
+
+
+def test_16x16_maxima_subset(golden, golden_arrays):
+    t = orc.gen_table(16, 16, 0, True)
+    full = golden_arrays["maxima_16x16"]
+    assert sha(full) == golden["configs"]["16x16"]["sha_maxima_i64"]
+    assert orc.nl_from_maxima(full) == (31942, 44828)
+    assert np.array_equal(orc.component_nl(t, 16, 1, 65), full[:64])
+    assert np.array_equal(orc.component_nl(t, 16, 44828, 44829), full[44827:44828])
+    assert np.array_equal(orc.component_nl(t, 16, 65535, 65536), full[-1:])
+
+
+@pytest.mark.parametrize("name,masks", [("20x20", 8), ("24x16", 2)])
+def test_large_config_subsets(golden, name, masks):
+    n, m, bij = CFG[name]
+    t = orc.gen_table(n, m, 0, bij)
+    sub = [r for r in golden["configs"][name]["subset"] if r["v"] <= masks]
+    for rec in sub:
+        v = rec["v"]
+        row = orc.spectrum(t, n, v, v + 1)[0]
+        assert int(np.abs(row).max()) == rec["max_abs"]
+        assert int(np.argmax(np.abs(row.astype(np.int64)))) == rec["argmax_u"]
+        assert row[:8].tolist() == rec["w_head"]
+        assert orc.column_nl(1 << n, rec["max_abs"]) == rec["nl"]
+
+
+def test_small_sweep(golden):
+    for rec in golden["small"]["sweep"]:
+        n, m = rec["n"], rec["m"]
+        t = orc.gen_table(n, m, rec["seed"], rec["bijective"])
+        assert sha(t) == rec["sha_table_u32"]
+        rows = orc.spectrum(t, n, 1, 1 << m)
+        assert sha(rows) == rec["sha_mask_major"], rec
+        nl = orc.component_nl(t, n, 1, 1 << m)
+        assert sha(nl) == rec["sha_maxima_i64"]
+        assert orc.nl_from_maxima(nl) == (rec["nl"], rec["argmin_v"])
+        if "nl_bruteforce" in rec and n <= 6 and m <= 6:
+            assert orc.nl_bruteforce(t, n, m)[0] == rec["nl_bruteforce"]
+
+
+def test_specials(golden):
+    from paper_1912_03732_b200 import identity_sbox
+
+    for rec in golden["small"]["specials"]:
+        if rec["table"] is not None:
+            t = np.array(rec["table"], dtype=np.uint32)
+        else:
+            t = identity_sbox(rec["n"]).table
+        rows = orc.spectrum(t, rec["n"], 1, 1 << rec["m"])
+        assert sha(rows) == rec["sha_mask_major"], rec["label"]
+        nl = orc.component_nl(t, rec["n"], 1, 1 << rec["m"])
+        assert orc.nl_from_maxima(nl) == (rec["nl"], rec["argmin_v"])
+
+
+def test_general_columns(golden, golden_arrays):
+    for rec in golden["small"]["columns"]:
+        key = "col_in_wrap" if rec.get("label") == "wrap" else f"col_in_{rec['k']}"
+        out, mx = orc.fwht_column(golden_arrays[key])
+        assert sha(out) == rec["sha_out"], rec
+        assert mx == rec["max_abs"], rec
+
+
+def test_known_answer_columns():
+    out, mx = orc.fwht_column(np.array([1, 1, 1, -1], dtype=np.int32))
+    assert out.tolist() == [2, 2, 2, -2] and mx == 2
+    out, mx = orc.fwht_column(np.array([-7], dtype=np.int32))
+    assert out.tolist() == [-7] and mx == 7
+    with pytest.raises(ValueError, match="power of two"):
+        orc.fwht_column(np.ones(6, dtype=np.int32))
+
+
+def test_walsh_direct_matches_spectrum():
+    t = orc.gen_table(5, 4, 9)
+    rows = orc.spectrum(t, 5, 1, 16)
+    for v in range(1, 16):
+        for u in range(32):
+            assert orc.walsh_direct(t, 5, u, v) == rows[v - 1, u]
+
+
+def test_stream_loop_equals_batched():
+    t = orc.gen_table(9, 7, 3)
+    assert np.array_equal(orc.stream_loop(t, 9, 1, 128), orc.component_nl(t, 9, 1, 128))
+
+
+def test_partition():
+    assert [b - a for a, b in orc.partition_columns(15, 8)] == [2, 2, 2, 2, 2, 2, 2, 1]
+    assert orc.partition_columns(3, 8) == ((1, 2), (2, 3), (3, 4))
