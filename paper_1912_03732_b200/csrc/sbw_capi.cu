@@ -119,13 +119,12 @@ int sbw_device_info(int device, sbw_device_info_t* out) {
   out->smem_optin_bytes = int64_t(p.sharedMemPerBlockOptin);
   out->l2_bytes = int64_t(p.l2CacheSize);
   out->global_mem_bytes = int64_t(p.totalGlobalMem);
-  snprintf(out->name, sizeof(out->name), "%s", p.name);
+  snprintf(out->name, sizeof(out->name), "%.127s", p.name);
   return SBW_OK;
 }
 
 size_t sbw_nl_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi) {
-  (void)m;
-  return k3_scratch_bytes(n, v_lo, v_hi);
+  return nl_scratch_bytes(n, m, v_lo, v_hi);
 }
 
 int sbw_nl(const void* d_table, int table_bytes, int n, int m, uint32_t v_lo, uint32_t v_hi,
@@ -135,16 +134,19 @@ int sbw_nl(const void* d_table, int table_bytes, int n, int m, uint32_t v_lo, ui
   if (int rc = check_table(d_table, table_bytes, m)) return rc;
   if (int rc = check_range(m, v_lo, v_hi)) return rc;
   if (!d_max_abs) return set_error(SBW_EINVAL, "null max_abs output");
+  const size_t need = nl_scratch_bytes(n, m, v_lo, v_hi);
+  if (need && (scratch == nullptr || scratch_bytes < need))
+    return set_error(SBW_EINVAL, "sbw_nl(n=%d, m=%d) needs %zu scratch bytes, got %zu", n, m, need,
+                     scratch_bytes);
   if (n <= 16)
-    return launch_fused_onchip(d_table, table_bytes, n, v_lo, v_hi, d_max_abs, d_key, nullptr, 0,
-                               as_stream(stream));
-  return launch_k3(d_table, table_bytes, n, v_lo, v_hi, d_max_abs, d_key, nullptr, 0, scratch,
+    return launch_fused_onchip(d_table, table_bytes, n, m, v_lo, v_hi, d_max_abs, d_key, nullptr,
+                               0, scratch, as_stream(stream));
+  return launch_k3(d_table, table_bytes, n, m, v_lo, v_hi, d_max_abs, d_key, nullptr, 0, scratch,
                    scratch_bytes, as_stream(stream));
 }
 
 size_t sbw_spectrum_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi, int layout) {
-  (void)m;
-  size_t s = k3_scratch_bytes(n, v_lo, v_hi);
+  size_t s = nl_scratch_bytes(n, m, v_lo, v_hi);
   if (layout == SBW_LAYOUT_X_MAJOR) s += (size_t(v_hi) - v_lo) * (size_t(4) << n);
   return s;
 }
@@ -164,9 +166,12 @@ int sbw_spectrum(const void* d_table, int table_bytes, int n, int m, uint32_t v_
     return set_error(SBW_EINVAL, "layout must be 0 (mask-major) or 1 (x-major)");
   if (layout == SBW_LAYOUT_MASK_MAJOR && ld < cols)
     return set_error(SBW_EINVAL, "ld %lld < 2^n", (long long)ld);
+  if (layout == SBW_LAYOUT_MASK_MAJOR && n >= 7 &&
+      ((ld & 1) || (reinterpret_cast<uintptr_t>(d_out) & 7)))
+    return set_error(SBW_EINVAL, "mask-major output needs an even ld and 8-byte alignment");
   if (layout == SBW_LAYOUT_X_MAJOR && ld < rows)
     return set_error(SBW_EINVAL, "ld %lld < number of masks", (long long)ld);
-  const size_t k3 = k3_scratch_bytes(n, v_lo, v_hi);
+  const size_t k3 = nl_scratch_bytes(n, m, v_lo, v_hi);
   const size_t need = sbw_spectrum_scratch_bytes(n, m, v_lo, v_hi, layout);
   if (need && (scratch == nullptr || scratch_bytes < need))
     return set_error(SBW_EINVAL, "spectrum needs %zu scratch bytes, got %zu", need, scratch_bytes);
@@ -183,10 +188,10 @@ int sbw_spectrum(const void* d_table, int table_bytes, int n, int m, uint32_t v_
   }
   int rc;
   if (n <= 16)
-    rc = launch_fused_onchip(d_table, table_bytes, n, v_lo, v_hi, mx, nullptr, rows_out, rows_ld,
-                             st);
+    rc = launch_fused_onchip(d_table, table_bytes, n, m, v_lo, v_hi, mx, nullptr, rows_out,
+                             rows_ld, scratch, st);
   else
-    rc = launch_k3(d_table, table_bytes, n, v_lo, v_hi, mx, nullptr, rows_out, rows_ld, scratch,
+    rc = launch_k3(d_table, table_bytes, n, m, v_lo, v_hi, mx, nullptr, rows_out, rows_ld, scratch,
                    k3, st);
   if (rc == SBW_OK && layout == SBW_LAYOUT_X_MAJOR)
     rc = launch_transpose_i32(rows_out, rows, cols, cols, d_out, ld, st);
@@ -260,74 +265,90 @@ int sbw_nl_bruteforce(const void* d_table, int table_bytes, int n, int m, int32_
   return launch_bruteforce(d_table, table_bytes, n, m, d_best, as_stream(stream));
 }
 
+namespace {
+// Per-device cached workspace for the host-buffer entry point, so repeated
+// calls pay only the copies and the kernels (not allocation).
+struct HostCallWs {
+  std::mutex mu;
+  cudaStream_t st = nullptr;
+  void* h_stage = nullptr;   // pinned: narrowed table in, NL out
+  size_t h_bytes = 0;
+  void* d_buf = nullptr;     // table | max_abs | nl | bad | key | scratch
+  size_t d_bytes = 0;
+};
+HostCallWs g_host_ws[64];
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+}  // namespace
+
 int sbw_nl_host(const uint32_t* h_table, int n, int m, uint32_t v_lo, uint32_t v_hi,
                 int64_t* h_nl, int64_t* out3, int device) {
   if (int rc = check_nm(n, m)) return rc;
   if (int rc = check_range(m, v_lo, v_hi)) return rc;
   if (!h_table) return set_error(SBW_EINVAL, "null host table");
+  if (device < 0 || device >= 64) return set_error(SBW_EINVAL, "bad device %d", device);
   SBW_CUDA_CHECK(cudaSetDevice(device));
-  cudaStream_t st;
-  SBW_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  HostCallWs& ws = g_host_ws[device];
+  std::lock_guard<std::mutex> lk(ws.mu);
+  if (!ws.st) SBW_CUDA_CHECK(cudaStreamCreateWithFlags(&ws.st, cudaStreamNonBlocking));
+  cudaStream_t st = ws.st;
   const int64_t nx = int64_t(1) << n, nv = int64_t(v_hi) - int64_t(v_lo);
   const int tb = m <= 16 ? 2 : 4;
-  // narrow the uint32 table on the host side of the copy: a staging buffer
-  void* h_stage = nullptr;
-  void* d_table = nullptr;
-  int32_t* d_mx = nullptr;
-  long long* d_nl = nullptr;
-  long long* d_bad = nullptr;
-  unsigned long long* d_key = nullptr;
-  void* scratch = nullptr;
-  const size_t sb = k3_scratch_bytes(n, v_lo, v_hi);
-  int rc = SBW_OK;
-  long long bad = LLONG_MAX;
-  unsigned long long key = 0;
-  auto fail = [&](cudaError_t e, const char* w) { rc = cuda_error(e, w); };
-  cudaError_t e;
-  if ((e = cudaMallocHost(&h_stage, size_t(nx) * tb)) != cudaSuccess) { fail(e, "cudaMallocHost"); goto done; }
+  const size_t tbl = align_up(size_t(nx) * tb), mxb = align_up(sizeof(int32_t) * nv),
+               nlb = align_up(sizeof(int64_t) * nv), small = 256;
+  const size_t sb = nl_scratch_bytes(n, m, v_lo, v_hi);
+  const size_t dneed = tbl + mxb + nlb + 2 * small + sb;
+  const size_t hneed = (tbl > nlb ? tbl : nlb) + 2 * small;
+  if (ws.h_bytes < hneed) {
+    if (ws.h_stage) cudaFreeHost(ws.h_stage);
+    ws.h_stage = nullptr;
+    ws.h_bytes = 0;
+    SBW_CUDA_CHECK(cudaMallocHost(&ws.h_stage, hneed));
+    ws.h_bytes = hneed;
+  }
+  if (ws.d_bytes < dneed) {
+    if (ws.d_buf) cudaFree(ws.d_buf);
+    ws.d_buf = nullptr;
+    ws.d_bytes = 0;
+    SBW_CUDA_CHECK(cudaMalloc(&ws.d_buf, dneed));
+    ws.d_bytes = dneed;
+  }
+  char* d = static_cast<char*>(ws.d_buf);
+  void* d_table = d;
+  int32_t* d_mx = reinterpret_cast<int32_t*>(d + tbl);
+  int64_t* d_nl = reinterpret_cast<int64_t*>(d + tbl + mxb);
+  int64_t* d_bad = reinterpret_cast<int64_t*>(d + tbl + mxb + nlb);
+  unsigned long long* d_key = reinterpret_cast<unsigned long long*>(d + tbl + mxb + nlb + small);
+  void* scratch = sb ? d + tbl + mxb + nlb + 2 * small : nullptr;
+  char* h = static_cast<char*>(ws.h_stage);
+  long long* h_bad = reinterpret_cast<long long*>(h + (tbl > nlb ? tbl : nlb));
+  unsigned long long* h_key = reinterpret_cast<unsigned long long*>(h_bad + 32);
+  // narrow the caller's uint32 table into pinned staging, then one H2D copy
   if (tb == 2) {
-    uint16_t* s = static_cast<uint16_t*>(h_stage);
-    for (int64_t i = 0; i < nx; ++i) s[i] = uint16_t(h_table[i]);
+    uint16_t* s16 = reinterpret_cast<uint16_t*>(h);
+    for (int64_t i = 0; i < nx; ++i) s16[i] = uint16_t(h_table[i]);
   } else {
-    memcpy(h_stage, h_table, size_t(nx) * 4);
+    memcpy(h, h_table, size_t(nx) * 4);
   }
-  if ((e = cudaMallocAsync(&d_table, size_t(nx) * tb + 16, st)) != cudaSuccess) { fail(e, "malloc table"); goto done; }
-  if ((e = cudaMallocAsync(&d_mx, sizeof(int32_t) * (nv + 1), st)) != cudaSuccess) { fail(e, "malloc max"); goto done; }
-  if ((e = cudaMallocAsync(&d_nl, sizeof(long long) * (nv + 1), st)) != cudaSuccess) { fail(e, "malloc nl"); goto done; }
-  if ((e = cudaMallocAsync(&d_bad, sizeof(long long), st)) != cudaSuccess) { fail(e, "malloc bad"); goto done; }
-  if ((e = cudaMallocAsync(&d_key, sizeof(unsigned long long), st)) != cudaSuccess) { fail(e, "malloc key"); goto done; }
-  if (sb && (e = cudaMallocAsync(&scratch, sb, st)) != cudaSuccess) { fail(e, "malloc scratch"); goto done; }
-  if ((e = cudaMemcpyAsync(d_table, h_stage, size_t(nx) * tb, cudaMemcpyHostToDevice, st)) != cudaSuccess) { fail(e, "H2D table"); goto done; }
-  if ((e = cudaMemsetAsync(d_key, 0, sizeof(unsigned long long), st)) != cudaSuccess) { fail(e, "memset key"); goto done; }
-  rc = sbw_nl(d_table, tb, n, m, v_lo, v_hi, d_mx, d_key, scratch, sb, st);
-  if (rc) goto done;
-  rc = sbw_maxabs_to_nl(d_mx, nv, n, reinterpret_cast<int64_t*>(d_nl), reinterpret_cast<int64_t*>(d_bad), st);
-  if (rc) goto done;
-  if (h_nl && (e = cudaMemcpyAsync(h_nl, d_nl, sizeof(long long) * nv, cudaMemcpyDeviceToHost, st)) != cudaSuccess) { fail(e, "D2H nl"); goto done; }
-  if ((e = cudaMemcpyAsync(&key, d_key, sizeof(key), cudaMemcpyDeviceToHost, st)) != cudaSuccess) { fail(e, "D2H key"); goto done; }
-  if ((e = cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st)) != cudaSuccess) { fail(e, "D2H bad"); goto done; }
-  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { fail(e, "sync"); goto done; }
-  if (bad != LLONG_MAX) {
-    rc = set_error(SBW_EPARITY, "odd spectrum gap at mask %lld", (long long)(v_lo + bad));
-    goto done;
-  }
+  SBW_CUDA_CHECK(cudaMemcpyAsync(d_table, h, size_t(nx) * tb, cudaMemcpyHostToDevice, st));
+  SBW_CUDA_CHECK(cudaMemsetAsync(d_key, 0, sizeof(unsigned long long), st));
+  if (int rc = sbw_nl(d_table, tb, n, m, v_lo, v_hi, d_mx, d_key, scratch, sb, st)) return rc;
+  if (int rc = sbw_maxabs_to_nl(d_mx, nv, n, d_nl, d_bad, st)) return rc;
+  // the staging buffer is reused for the results once the table copy is done
+  SBW_CUDA_CHECK(cudaMemcpyAsync(h, d_nl, sizeof(int64_t) * nv, cudaMemcpyDeviceToHost, st));
+  SBW_CUDA_CHECK(cudaMemcpyAsync(h_bad, d_bad, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  SBW_CUDA_CHECK(cudaMemcpyAsync(h_key, d_key, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  SBW_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (*h_bad != LLONG_MAX)
+    return set_error(SBW_EPARITY, "odd spectrum gap at mask %lld", (long long)(v_lo + *h_bad));
+  if (h_nl) memcpy(h_nl, h, sizeof(int64_t) * nv);
   if (out3) {
-    const int64_t mxw = int64_t(key >> 32);
+    const int64_t mxw = int64_t(*h_key >> 32);
     out3[0] = (nx - mxw) >> 1;
-    out3[1] = int64_t(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
+    out3[1] = int64_t(0xFFFFFFFFull - (*h_key & 0xFFFFFFFFull));
     out3[2] = mxw;
   }
-done:
-  if (scratch) cudaFreeAsync(scratch, st);
-  if (d_key) cudaFreeAsync(d_key, st);
-  if (d_bad) cudaFreeAsync(d_bad, st);
-  if (d_nl) cudaFreeAsync(d_nl, st);
-  if (d_mx) cudaFreeAsync(d_mx, st);
-  if (d_table) cudaFreeAsync(d_table, st);
-  cudaStreamSynchronize(st);
-  if (h_stage) cudaFreeHost(h_stage);
-  cudaStreamDestroy(st);
-  return rc;
+  return SBW_OK;
 }
 
 int sbw_int32_peak(double* ops_per_s, double* ms, void* stream) {

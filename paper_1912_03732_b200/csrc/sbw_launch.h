@@ -8,20 +8,30 @@
 
 namespace sbw {
 
-// Fused on-chip path (n <= 16): NL (out == nullptr) or mask-major SPEC rows.
-int launch_fused_onchip(const void* table, int tbytes, int n, uint32_t v_lo, uint32_t v_hi,
-                        int32_t* max_abs, unsigned long long* key, int32_t* out, int64_t ld,
-                        cudaStream_t st);
+// Bit planes of the S-box (bit x of plane i = bit i of S(x)), n >= 7.
+size_t planes_bytes(int n, int m);
+int build_planes(const void* table, int tbytes, int n, int m, uint32_t* planes, cudaStream_t st);
 
-// Multi-pass path (n >= 17): pass A (emit) + pass B per L2-sized batch.
-size_t k3_scratch_bytes(int n, uint32_t v_lo, uint32_t v_hi);
-int launch_k3(const void* table, int tbytes, int n, uint32_t v_lo, uint32_t v_hi,
+// Fused on-chip path (n <= 16): NL (out == nullptr) or mask-major SPEC rows.
+// `scratch` holds the bit planes (planes_bytes(n, m)) for n >= 7.
+int launch_fused_onchip(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32_t v_hi,
+                        int32_t* max_abs, unsigned long long* key, int32_t* out, int64_t ld,
+                        void* scratch, cudaStream_t st);
+
+// Multi-pass path (n >= 17): planes, then pass A (emit) + pass B per L2-sized batch.
+size_t k3_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi);
+int launch_k3(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32_t v_hi,
               int32_t* max_abs, unsigned long long* key, int32_t* out, int64_t ld, void* scratch,
               size_t scratch_bytes, cudaStream_t st);
 
 // Pass A only (exposed for the launcher above).
-int launch_emit_tile(const void* table, int tbytes, int n, uint32_t v_first, int64_t n_comp,
+int launch_emit_tile(const uint32_t* planes, int n, int m, uint32_t v_first, int64_t n_comp,
                      uint32_t* emit, cudaStream_t st);
+
+// Total workspace of sbw_nl (planes + multi-pass scratch).
+inline size_t nl_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi) {
+  return n >= 17 ? k3_scratch_bytes(n, m, v_lo, v_hi) : planes_bytes(n, m);
+}
 
 // Misc kernels.
 int launch_transpose_i32(const int32_t* in, int64_t rows, int64_t cols, int64_t ld_in,

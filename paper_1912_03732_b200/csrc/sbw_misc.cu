@@ -393,7 +393,8 @@ int launch_bruteforce(const void* table, int tbytes, int n, int m, int32_t* best
 // INT32 ALU peak microbenchmark.  8 independent dependency chains per
 // thread; MODE 0: add/sub pairs (IADD3, ALU pipe), MODE 1: multiply-add with
 // a runtime multiplier (IMAD, FMA pipe), MODE 2: both interleaved.  Each
-// executed lane-instruction counts as one integer op.
+// executed lane-instruction counts as one integer op.  MODE 0 alternates
+// add and xor (IADD3 / LOP3) so no algebraic folding is possible.
 // ---------------------------------------------------------------------------
 template <int MODE>
 __global__ void __launch_bounds__(512) k_int32_peak(int iters, int mul, int32_t* sink) {
@@ -410,11 +411,12 @@ __global__ void __launch_bounds__(512) k_int32_peak(int iters, int mul, int32_t*
     for (int r = 0; r < 16; ++r) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
+        // volatile asm keeps the compiler from folding the linear chains
         if (MODE != 1) {
-          x[i] = x[i] + y[i];
-          y[i] = y[i] - x[i];
+          asm volatile("add.s32 %0, %0, %1;" : "+r"(x[i]) : "r"(y[i]));
+          asm volatile("xor.b32 %0, %0, %1;" : "+r"(y[i]) : "r"(x[i]));
         }
-        if (MODE != 0) z[i] = z[i] * c + d;
+        if (MODE != 0) asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(z[i]) : "r"(c), "r"(d));
       }
     }
   }

@@ -65,30 +65,33 @@ int dispatch_h(int h, const PassBArgs& a, cudaStream_t st) {
 
 }  // namespace
 
-size_t k3_scratch_bytes(int n, uint32_t v_lo, uint32_t v_hi) {
+size_t k3_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi) {
   if (n < 17) return 0;
-  return size_t(batch_components(n, v_lo, v_hi)) * (size_t(2) << n);
+  return planes_bytes(n, m) + size_t(batch_components(n, v_lo, v_hi)) * (size_t(2) << n);
 }
 
-int launch_k3(const void* table, int tbytes, int n, uint32_t v_lo, uint32_t v_hi,
+int launch_k3(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32_t v_hi,
               int32_t* max_abs, unsigned long long* key, int32_t* out, int64_t ld, void* scratch,
               size_t scratch_bytes, cudaStream_t st) {
   if (n < 17 || n > 24) return set_error(SBW_EINVAL, "multi-pass path needs n in 17..24");
   if (v_hi <= v_lo) return SBW_OK;
   const int64_t bb = batch_components(n, v_lo, v_hi);
-  if (scratch == nullptr || scratch_bytes < size_t(bb) * (size_t(2) << n))
-    return set_error(SBW_EINVAL, "n=%d needs a scratch workspace of %zu bytes, got %zu", n,
-                     size_t(bb) * (size_t(2) << n), scratch_bytes);
+  const size_t need = k3_scratch_bytes(n, m, v_lo, v_hi);
+  if (scratch == nullptr || scratch_bytes < need)
+    return set_error(SBW_EINVAL, "n=%d needs a scratch workspace of %zu bytes, got %zu", n, need,
+                     scratch_bytes);
+  uint32_t* planes = static_cast<uint32_t*>(scratch);
+  uint32_t* emit = reinterpret_cast<uint32_t*>(static_cast<char*>(scratch) + planes_bytes(n, m));
+  if (int rc = build_planes(table, tbytes, n, m, planes, st)) return rc;
   SBW_CUDA_CHECK(cudaMemsetAsync(max_abs, 0, sizeof(int32_t) * (size_t(v_hi) - v_lo), st));
   for (int64_t c0 = 0; c0 < int64_t(v_hi) - int64_t(v_lo); c0 += bb) {
     const int64_t nc = (int64_t(v_hi) - int64_t(v_lo) - c0) < bb
                            ? (int64_t(v_hi) - int64_t(v_lo) - c0)
                            : bb;
     const uint32_t vf = v_lo + uint32_t(c0);
-    if (int rc = launch_emit_tile(table, tbytes, n, vf, nc, static_cast<uint32_t*>(scratch), st))
-      return rc;
+    if (int rc = launch_emit_tile(planes, n, m, vf, nc, emit, st)) return rc;
     PassBArgs a{};
-    a.scratch = static_cast<const uint32_t*>(scratch);
+    a.scratch = emit;
     a.n = n;
     a.n_comp = nc;
     a.out_row0 = c0;

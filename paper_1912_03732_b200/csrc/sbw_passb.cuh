@@ -1,8 +1,9 @@
 // Multi-pass path for n = 17..24 ("K3"), pass B.
 //
-// Pass A (k_fused_tile<15, ..., MODE_EMIT>) leaves, for every component of
-// the current batch, 2^(n-15) blocks of 2^15 partial transforms (x bits
-// 0..14 done) as halved int16 in an L2-sized scratch buffer.  Pass B runs the
+// Pass A (k_tile_simd<15, MODE_EMIT>) leaves, for every component of the
+// current batch, 2^(n-15) blocks of 2^15 partial transforms (x bits 0..14
+// done) in an L2-sized scratch buffer, each as the biased u16
+// s = (v + 2^15) / 2 in [0, 2^15]; pass B works on v / 2 = s - 2^14 in int32.  Pass B runs the
 // remaining H = n - 15 stages over x bits 15..n-1, i.e. across blocks, and
 // fuses max|W| into the top stage exactly like the on-chip kernel.  The
 // reference does all n stages on one numpy array per mask (walsh.py:91-103);
@@ -13,7 +14,7 @@
 //           runs two register passes over it.
 #pragma once
 
-#include "sbw_fused.cuh"
+#include "sbw_tile_simd.cuh"
 
 namespace sbw {
 
@@ -30,6 +31,9 @@ struct PassBArgs {
 };
 
 constexpr int kPassBThreads = 256;
+
+__device__ __forceinline__ int lo_half(uint32_t u) { return int(u & 0xFFFFu) - 16384; }
+__device__ __forceinline__ int hi_half(uint32_t u) { return int(u >> 16) - 16384; }
 
 // Reduce a per-thread partial max over the CTA and publish it (all threads of
 // a CTA belong to the same component by construction).
@@ -63,8 +67,8 @@ __global__ void __launch_bounds__(kPassBThreads) k_passb_regs(PassBArgs a) {
 #pragma unroll
     for (int i = 0; i < NI; ++i) {
       const uint32_t u = __ldcs(src + (int64_t(i) << 14));
-      e[2 * i] = lo16(u);
-      e[2 * i + 1] = hi16(u);
+      e[2 * i] = lo_half(u);
+      e[2 * i + 1] = hi_half(u);
     }
     fwht_regs_until<2 * NI, 2, NI>(e);
     int mx = 0;
@@ -109,7 +113,7 @@ __global__ void __launch_bounds__(512, 1) k_passb_smem(PassBArgs a) {
     const uint32_t* src = a.scratch + (comp << (a.n - 1)) + col0;
     for (int r = threadIdx.x >> 5; r < R; r += blockDim.x >> 5) {
       const uint32_t u = __ldcs(src + (int64_t(r) << 14) + lane);
-      tile[r * 32 + lane] = make_int2(lo16(u), hi16(u));
+      tile[r * 32 + lane] = make_int2(lo_half(u), hi_half(u));
     }
     __syncthreads();
     // B1: row bits 0..4 for every (row-high, column) task

@@ -1,7 +1,7 @@
-// Instantiation and dispatch of the fused on-chip kernels (n = 1..16) and of
-// pass A of the multi-pass path.  See sbw_fused.cuh for the algorithm.
-#include "sbw_fused.cuh"
+// Dispatch of the fused on-chip kernels (n = 1..16) and of pass A of the
+// multi-pass path; bit-plane construction.  See sbw_tile_simd.cuh.
 #include "sbw_launch.h"
+#include "sbw_tile_simd.cuh"
 
 namespace sbw {
 
@@ -9,9 +9,25 @@ namespace {
 
 constexpr size_t kTileSmem = size_t(kTileWords) * sizeof(uint32_t);  // 128 KiB
 
-template <int N, typename TT, int MODE>
-int run_tile(const FusedArgs& a, cudaStream_t st) {
-  auto kern = k_fused_tile<N, TT, MODE>;
+// planes[i][w] bit b = bit i of S(32 w + b): one warp per 32 inputs, a ballot per plane.
+template <typename TT>
+__global__ void __launch_bounds__(256) k_build_planes(const TT* __restrict__ table, int n, int m,
+                                                      uint32_t* __restrict__ planes) {
+  const int64_t words = (int64_t(1) << n) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < words; w += warps) {
+    const uint32_t s = uint32_t(table[(w << 5) + lane]);
+    for (int i = 0; i < m; ++i) {
+      const uint32_t b = __ballot_sync(0xffffffffu, (s >> i) & 1u);
+      if (lane == 0) planes[int64_t(i) * words + w] = b;
+    }
+  }
+}
+
+template <int N, int MODE>
+int run_tile(const TileArgs& a, int64_t ntiles, cudaStream_t st) {
+  auto kern = k_tile_simd<N, MODE>;
   DeviceProps dp;
   if (int rc = device_props(&dp)) return rc;
   // per (instantiation, device); the attribute call is idempotent, so a race is benign
@@ -21,12 +37,10 @@ int run_tile(const FusedArgs& a, cudaStream_t st) {
                                         int(kTileSmem)));
     attr_done |= 1ull << (dp.device & 63);
   }
-  constexpr int C = 1 << (16 - N);
-  const int64_t ntiles = (a.n_items + C - 1) / C;
   const int grid = int(ntiles < dp.sm_count ? ntiles : dp.sm_count);
-  if (grid == 0) return SBW_OK;
+  if (grid <= 0) return SBW_OK;
   kern<<<grid, kTileThreads, kTileSmem, st>>>(a);
-  SBW_LAUNCH_CHECK("k_fused_tile");
+  SBW_LAUNCH_CHECK("k_tile_simd");
   return SBW_OK;
 }
 
@@ -44,7 +58,7 @@ int run_small(const FusedArgs& a, cudaStream_t st) {
 }
 
 template <typename TT, int MODE>
-int dispatch_n(int n, const FusedArgs& a, cudaStream_t st) {
+int dispatch_small(int n, const FusedArgs& a, cudaStream_t st) {
   switch (n) {
     case 1: return run_small<1, TT, MODE>(a, st);
     case 2: return run_small<2, TT, MODE>(a, st);
@@ -52,54 +66,103 @@ int dispatch_n(int n, const FusedArgs& a, cudaStream_t st) {
     case 4: return run_small<4, TT, MODE>(a, st);
     case 5: return run_small<5, TT, MODE>(a, st);
     case 6: return run_small<6, TT, MODE>(a, st);
-    case 7: return run_tile<7, TT, MODE>(a, st);
-    case 8: return run_tile<8, TT, MODE>(a, st);
-    case 9: return run_tile<9, TT, MODE>(a, st);
-    case 10: return run_tile<10, TT, MODE>(a, st);
-    case 11: return run_tile<11, TT, MODE>(a, st);
-    case 12: return run_tile<12, TT, MODE>(a, st);
-    case 13: return run_tile<13, TT, MODE>(a, st);
-    case 14: return run_tile<14, TT, MODE>(a, st);
-    case 15: return run_tile<15, TT, MODE>(a, st);
-    case 16: return run_tile<16, TT, MODE>(a, st);
-    default: return set_error(SBW_EINVAL, "on-chip path needs n in 1..16, got %d", n);
+    default: return set_error(SBW_EINVAL, "small path needs n in 1..6, got %d", n);
+  }
+}
+
+template <int MODE>
+int dispatch_tile(int n, const TileArgs& a, int64_t nt, cudaStream_t st) {
+  switch (n) {
+    case 7: return run_tile<7, MODE>(a, nt, st);
+    case 8: return run_tile<8, MODE>(a, nt, st);
+    case 9: return run_tile<9, MODE>(a, nt, st);
+    case 10: return run_tile<10, MODE>(a, nt, st);
+    case 11: return run_tile<11, MODE>(a, nt, st);
+    case 12: return run_tile<12, MODE>(a, nt, st);
+    case 13: return run_tile<13, MODE>(a, nt, st);
+    case 14: return run_tile<14, MODE>(a, nt, st);
+    case 15: return run_tile<15, MODE>(a, nt, st);
+    case 16: return run_tile<16, MODE>(a, nt, st);
+    default: return set_error(SBW_EINVAL, "tile path needs n in 7..16, got %d", n);
   }
 }
 
 }  // namespace
 
-int launch_fused_onchip(const void* table, int tbytes, int n, uint32_t v_lo, uint32_t v_hi,
+size_t planes_bytes(int n, int m) {
+  if (n < 7) return 0;
+  const size_t b = size_t(m) * ((size_t(1) << n) / 8);
+  return (b + 255) & ~size_t(255);
+}
+
+int build_planes(const void* table, int tbytes, int n, int m, uint32_t* planes, cudaStream_t st) {
+  if (n < 5) return set_error(SBW_EINVAL, "bit planes need n >= 5");
+  const int64_t words = (int64_t(1) << n) >> 5;
+  DeviceProps dp;
+  if (int rc = device_props(&dp)) return rc;
+  int64_t blocks = (words + 7) / 8;
+  if (blocks > int64_t(dp.sm_count) * 16) blocks = int64_t(dp.sm_count) * 16;
+  if (tbytes == 2)
+    k_build_planes<uint16_t><<<int(blocks), 256, 0, st>>>(static_cast<const uint16_t*>(table), n,
+                                                          m, planes);
+  else
+    k_build_planes<uint32_t><<<int(blocks), 256, 0, st>>>(static_cast<const uint32_t*>(table), n,
+                                                          m, planes);
+  SBW_LAUNCH_CHECK("k_build_planes");
+  return SBW_OK;
+}
+
+int launch_fused_onchip(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32_t v_hi,
                         int32_t* max_abs, unsigned long long* key, int32_t* out, int64_t ld,
-                        cudaStream_t st) {
-  FusedArgs a{};
-  a.table = table;
-  a.v_first = v_lo;
-  a.nbl = 0;
-  a.n_items = int64_t(v_hi) - int64_t(v_lo);
+                        void* scratch, cudaStream_t st) {
+  if (v_hi <= v_lo) return SBW_OK;
+  if (n <= 6) {
+    FusedArgs a{};
+    a.table = table;
+    a.v_first = v_lo;
+    a.n_items = int64_t(v_hi) - int64_t(v_lo);
+    a.max_abs = max_abs;
+    a.key = key;
+    a.out = out;
+    a.ld = ld;
+    if (out)
+      return tbytes == 2 ? dispatch_small<uint16_t, MODE_SPEC>(n, a, st)
+                         : dispatch_small<uint32_t, MODE_SPEC>(n, a, st);
+    return tbytes == 2 ? dispatch_small<uint16_t, MODE_NL>(n, a, st)
+                       : dispatch_small<uint32_t, MODE_NL>(n, a, st);
+  }
+  uint32_t* planes = static_cast<uint32_t*>(scratch);
+  if (int rc = build_planes(table, tbytes, n, m, planes, st)) return rc;
+  TileArgs a{};
+  a.planes = planes;
+  a.plane_words = (int64_t(1) << n) >> 5;
+  a.m = m;
+  a.v_lo = v_lo;
+  a.v_hi = v_hi;
+  const int j = 16 - n;
+  a.t_begin = int64_t(v_lo) >> j;
+  a.t_count = ((int64_t(v_hi) - 1) >> j) + 1 - a.t_begin;
   a.max_abs = max_abs;
   a.key = key;
   a.out = out;
   a.ld = ld;
-  a.emit = nullptr;
-  if (a.n_items <= 0) return SBW_OK;
-  if (out) {
-    return tbytes == 2 ? dispatch_n<uint16_t, MODE_SPEC>(n, a, st)
-                       : dispatch_n<uint32_t, MODE_SPEC>(n, a, st);
-  }
-  return tbytes == 2 ? dispatch_n<uint16_t, MODE_NL>(n, a, st)
-                     : dispatch_n<uint32_t, MODE_NL>(n, a, st);
+  return out ? dispatch_tile<MODE_SPEC>(n, a, a.t_count, st)
+             : dispatch_tile<MODE_NL>(n, a, a.t_count, st);
 }
 
-int launch_emit_tile(const void* table, int tbytes, int n, uint32_t v_first, int64_t n_comp,
+int launch_emit_tile(const uint32_t* planes, int n, int m, uint32_t v_first, int64_t n_comp,
                      uint32_t* emit, cudaStream_t st) {
-  FusedArgs a{};
-  a.table = table;
+  TileArgs a{};
+  a.planes = planes;
+  a.plane_words = (int64_t(1) << n) >> 5;
+  a.m = m;
   a.v_first = v_first;
-  a.nbl = n - 15;
-  a.n_items = n_comp << (n - 15);
+  a.n_comp = n_comp;
+  a.n_full = n;
   a.emit = emit;
-  return tbytes == 2 ? run_tile<15, uint16_t, MODE_EMIT>(a, st)
-                     : run_tile<15, uint32_t, MODE_EMIT>(a, st);
+  a.t_begin = 0;
+  a.t_count = n_comp << (n - 16);  // (block pair, component) tiles
+  return run_tile<15, MODE_EMIT>(a, a.t_count, st);
 }
 
 }  // namespace sbw
