@@ -17,7 +17,7 @@
 
 namespace sbw {
 
-constexpr int kTileThreads = 512;
+constexpr int kTileThreads = 1024;
 constexpr int kTileWords = 1 << 15;  // 2^16 int16 elements as 32-bit pairs
 
 enum FusedMode { MODE_NL = 0, MODE_SPEC = 1, MODE_EMIT = 2 };

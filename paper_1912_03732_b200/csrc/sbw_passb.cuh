@@ -96,35 +96,32 @@ __global__ void __launch_bounds__(kPassBThreads) k_passb_regs(PassBArgs a) {
   }
 }
 
-// H = 6..9.  A CTA owns (component, 32 pair-columns) x 2^H rows in smem as
-// int32 pairs; pass B1 handles row bits 0..4, pass B2 row bits 5..H-1.
+// H = 6..9.  A CTA owns (component, 32 pair-columns) x 2^H rows.  Pass B1
+// reads row bits 0..4 straight from the scratch (32 independent coalesced
+// loads in flight per thread), runs those 5 stages and parks int32 pairs in
+// shared memory; pass B2 runs row bits 5..H-1 with the fused top stage.
 template <int H, int MODE>
 __global__ void __launch_bounds__(512, 1) k_passb_smem(PassBArgs a) {
-  constexpr int R = 1 << H;            // rows
   constexpr int H2 = H - 5;
   constexpr int N2 = 1 << H2;
-  extern __shared__ int2 tile[];       // [R][32] pairs
+  extern __shared__ int2 tile[];       // [2^H rows][32 columns] int32 pairs
   __shared__ int s_red[16];
   const int64_t chunks = (int64_t(1) << 14) / 32;
-  const int lane = threadIdx.x & 31;
   for (int64_t b = blockIdx.x; b < a.n_comp * chunks; b += gridDim.x) {
     const int64_t comp = b / chunks;
     const int64_t col0 = (b % chunks) * 32;
     const uint32_t* src = a.scratch + (comp << (a.n - 1)) + col0;
-    for (int r = threadIdx.x >> 5; r < R; r += blockDim.x >> 5) {
-      const uint32_t u = __ldcs(src + (int64_t(r) << 14) + lane);
-      tile[r * 32 + lane] = make_int2(lo_half(u), hi_half(u));
-    }
-    __syncthreads();
-    // B1: row bits 0..4 for every (row-high, column) task
+    // B1: task = (column c, row-high rh); rows (rh << 5) | i
     for (int task = threadIdx.x; task < 32 * N2; task += blockDim.x) {
       const int c = task & 31, rh = task >> 5;
+      uint32_t u[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) u[i] = __ldcs(src + (int64_t((rh << 5) | i) << 14) + c);
       int e[64];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const int2 p = tile[((rh << 5) | i) * 32 + c];
-        e[2 * i] = p.x;
-        e[2 * i + 1] = p.y;
+        e[2 * i] = lo_half(u[i]);
+        e[2 * i + 1] = hi_half(u[i]);
       }
       fwht_regs<64, 2>(e);
 #pragma unroll

@@ -183,8 +183,9 @@ __device__ __forceinline__ void tile_last_pass(const TileArgs& a, uint32_t (&E)[
   }
 }
 
-template <int N, int MODE>
-__global__ void __launch_bounds__(kTileThreads, 1) k_tile_simd(TileArgs a) {
+template <int N, int MODE, int THREADS = kTileThreads>
+__global__ void __launch_bounds__(THREADS, 1) k_tile_simd(TileArgs a) {
+  constexpr int ROUNDS = 1024 / THREADS;         // pass-1 tasks per thread
   static_assert(N >= 7 && N <= 16, "tile kernel covers n = 7..16");
   static_assert(MODE != MODE_EMIT || N == 15, "EMIT works on 2^15 blocks");
   constexpr int J = 16 - N;
@@ -200,17 +201,22 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_simd(TileArgs a) {
   const int64_t t_lo = a.t_begin + (a.t_count * blockIdx.x) / gridDim.x;
   const int64_t t_hi = a.t_begin + (a.t_count * (blockIdx.x + 1)) / gridDim.x;
 
-  // generation state of the two pass-1 tasks this thread owns
-  uint32_t g_v[2] = {0, 0}, g_w0[2] = {0, 0}, g_w1[2] = {0, 0};
-  int64_t g_cw[2] = {-1, -1};
+  // generation state of the pass-1 tasks this thread owns
+  uint32_t g_v[ROUNDS], g_w0[ROUNDS], g_w1[ROUNDS];
+  int64_t g_cw[ROUNDS];
+#pragma unroll
+  for (int r = 0; r < ROUNDS; ++r) {
+    g_v[r] = g_w0[r] = g_w1[r] = 0;
+    g_cw[r] = -1;
+  }
 
   for (int64_t t = t_lo; t < t_hi; ++t) {
     if (tid < C) s_max[tid] = 0;
 
     // ---------------- pass 1: generation + x bits 0..5 ---------------------
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int task = r * kTileThreads + tid;
+    for (int r = 0; r < ROUNDS; ++r) {
+      const int task = r * THREADS + tid;
       const int p0 = task << 6;
       const int slot = p0 >> N;
       const int x0 = p0 & XMASK;
@@ -286,16 +292,19 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_simd(TileArgs a) {
       constexpr int NI = 1 << B2;
       constexpr int NT = kTileWords >> B2;
       constexpr bool LAST = (B3 == 0);
-      for (int task = tid; task < NT; task += kTileThreads) {
+      for (int task = tid; task < NT; task += THREADS) {
         const int lo = task & 31, hi = task >> 5;
         const int wb = (hi << (5 + B2)) | lo;
+        // phys(wb | i << 5) = (P ^ ((i & 7) << 2)) + (i << 5), P = phys(wb):
+        // at most 8 base pointers, the rest are immediate offsets
+        const int P = phys_word(wb);
         uint32_t E[NI];
 #pragma unroll
-        for (int i = 0; i < NI; ++i) E[i] = sm[phys_word(wb | (i << 5))];
+        for (int i = 0; i < NI; ++i) E[i] = sm[(P ^ ((i & 7) << 2)) + (i << 5)];
         if constexpr (!LAST) {
           stages16<NI, 0, B2, 6>(E);
 #pragma unroll
-          for (int i = 0; i < NI; ++i) sm[phys_word(wb | (i << 5))] = E[i];
+          for (int i = 0; i < NI; ++i) sm[(P ^ ((i & 7) << 2)) + (i << 5)] = E[i];
         } else {
           tile_last_pass<N, MODE, NI, 5, 6>(a, E, wb, t, s_max);
         }
@@ -307,12 +316,14 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_simd(TileArgs a) {
     if constexpr (B3 > 0) {
       constexpr int NI = 1 << B3;
       constexpr int NT = kTileWords >> B3;
-      for (int task = tid; task < NT; task += kTileThreads) {
+      for (int task = tid; task < NT; task += THREADS) {
         const int lo = task & 1023, hi = task >> 10;
         const int wb = (hi << (10 + B3)) | lo;
+        // the swizzle depends on word bits 5..7 only, so phys(wb | i << 10) = phys(wb) + (i << 10)
+        const uint32_t* base = sm + phys_word(wb);
         uint32_t E[NI];
 #pragma unroll
-        for (int i = 0; i < NI; ++i) E[i] = sm[phys_word(wb | (i << 10))];
+        for (int i = 0; i < NI; ++i) E[i] = base[i << 10];
         tile_last_pass<N, MODE, NI, 10, 11>(a, E, wb, t, s_max);
       }
       __syncthreads();
