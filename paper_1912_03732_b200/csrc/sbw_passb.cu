@@ -6,6 +6,7 @@
 #include "sbw_passb.cuh"
 #include "sbw_launch.h"
 
+#include <cstdlib>
 #include <mutex>
 
 namespace sbw {
@@ -120,6 +121,13 @@ int launch_k3(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32
   K3Streams* ks = nullptr;
   if (int rc = k3_streams(dp.device, &ks)) return rc;
   std::lock_guard<std::mutex> launch_lock(g_k3_launch_mu[dp.device & 63]);
+  static const bool single = getenv("SBW_K3_SINGLE_STREAM") != nullptr;  // debugging aid
+  K3Streams one = *ks;
+  if (single) {
+    one.a = st;
+    one.b = st;
+    ks = &one;
+  }
   // fork: both aux streams start after everything already queued on `st`
   SBW_CUDA_CHECK(cudaEventRecord(ks->fork, st));
   SBW_CUDA_CHECK(cudaStreamWaitEvent(ks->a, ks->fork, 0));

@@ -123,10 +123,17 @@ def table_bytes(m: int) -> int:
 
 
 # ---------------------------------------------------------------------------
-# device copies of S-box tables, cached per (SBox object, device)
+# device copies of S-box tables, cached per (SBox object identity, device).
+# Keyed by id() with a weakref guard: a WeakKeyDictionary would compare keys
+# with SBox.__eq__ (a full table comparison) on every lookup.
 # ---------------------------------------------------------------------------
-_table_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_table_cache: dict = {}
 _cache_mu = threading.Lock()
+
+
+def _evict(key_id: int) -> None:
+    with _cache_mu:
+        _table_cache.pop(key_id, None)
 
 
 def device_table(s, device, cache: bool = True):
@@ -136,12 +143,12 @@ def device_table(s, device, cache: bool = True):
     support); the kernels reinterpret them.
     """
     torch = torch_mod()
-    key = (device.type, device.index)
+    dkey = (device.type, device.index)
     if cache:
         with _cache_mu:
-            per = _table_cache.get(s)
-            if per is not None and key in per:
-                return per[key]
+            hit = _table_cache.get(id(s))
+            if hit is not None and hit[0]() is s and dkey in hit[1]:
+                return hit[1][dkey]
     if table_bytes(s.m) == 2:
         host = np.ascontiguousarray(s.table.astype(np.uint16)).view(np.int16)
     else:
@@ -149,7 +156,12 @@ def device_table(s, device, cache: bool = True):
     t = torch.from_numpy(host.copy()).to(device, non_blocking=False)
     if cache:
         with _cache_mu:
-            _table_cache.setdefault(s, {})[key] = t
+            hit = _table_cache.get(id(s))
+            if hit is None or hit[0]() is not s:
+                hit = (weakref.ref(s), {})
+                _table_cache[id(s)] = hit
+                weakref.finalize(s, _evict, id(s))
+            hit[1][dkey] = t
     return t
 
 
