@@ -24,9 +24,6 @@ int launch_k3(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32
               int32_t* max_abs, unsigned long long* key, int32_t* out, int64_t ld, void* scratch,
               size_t scratch_bytes, cudaStream_t st);
 
-// Pass A only (exposed for the launcher above).
-int launch_emit_tile(const uint32_t* planes, int n, int m, uint32_t v_first, int64_t n_comp,
-                     uint32_t* emit, cudaStream_t st);
 
 // Total workspace of sbw_nl (planes + multi-pass scratch).
 inline size_t nl_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi) {

@@ -9,9 +9,11 @@
 // reference does all n stages on one numpy array per mask (walsh.py:91-103);
 // stage order is free because the butterflies of different bits commute.
 //
-//   H <= 5: registers only; a thread owns one int16 pair column of 2^H rows.
-//   H  > 5: a CTA stages a [2^H rows x 64 x] int32 tile in shared memory and
-//           runs two register passes over it.
+//   H <= 5: registers only; a thread owns one pair column of 2^H rows.
+//   H  > 5: a CTA stages a [2^H rows x 32 pair-columns] int32 tile in shared
+//           memory and runs two register passes over it.
+// Both run inside the persistent k3_persistent kernel below, interleaved with
+// pass A so the scratch of in-flight components stays L2-resident.
 #pragma once
 
 #include "sbw_tile_simd.cuh"
@@ -29,8 +31,6 @@ struct PassBArgs {
   int32_t* out;              // materialised rows (may be null)
   int64_t ld;
 };
-
-constexpr int kPassBThreads = 256;
 
 __device__ __forceinline__ int lo_half(uint32_t u) { return int(u & 0xFFFFu) - 16384; }
 __device__ __forceinline__ int hi_half(uint32_t u) { return int(u >> 16) - 16384; }
@@ -52,118 +52,209 @@ __device__ __forceinline__ void cta_publish_max(int mx, int* s_red, int32_t* slo
   __syncthreads();
 }
 
-// H <= 5.  Grid: one CTA per (component, chunk of 256 pair-columns).
-template <int H, int MODE>
-__global__ void __launch_bounds__(kPassBThreads) k_passb_regs(PassBArgs a) {
+// ---- pass-B chunk bodies (called by every thread of the CTA) --------------
+// Scratch reads use ld.global.cg: the persistent kernel reuses ring slots, so
+// an SM's L1 may hold lines of an older component.
+
+// H <= 5: THREADS pair-columns of one component, 2^H rows each, in registers.
+template <int H, int MODE, int THREADS>
+__device__ __forceinline__ void passb_regs_chunk(const PassBArgs& a, int64_t comp, int64_t chunk,
+                                                 int* s_red) {
   constexpr int NI = 1 << H;
-  __shared__ int s_red[kPassBThreads / 32];
-  const int64_t cols = int64_t(1) << 14;                   // pair-columns per component
-  const int64_t chunks = cols / kPassBThreads;
-  for (int64_t b = blockIdx.x; b < a.n_comp * chunks; b += gridDim.x) {
-    const int64_t comp = b / chunks;
-    const int64_t col = (b % chunks) * kPassBThreads + threadIdx.x;
-    const uint32_t* src = a.scratch + (comp << (a.n - 1)) + col;
-    int e[2 * NI];
+  const int64_t col = chunk * THREADS + threadIdx.x;
+  const uint32_t* src = a.scratch + (comp << (a.n - 1)) + col;
+  uint32_t u[NI];
 #pragma unroll
-    for (int i = 0; i < NI; ++i) {
-      const uint32_t u = __ldcs(src + (int64_t(i) << 14));
-      e[2 * i] = lo_half(u);
-      e[2 * i + 1] = hi_half(u);
-    }
-    fwht_regs_until<2 * NI, 2, NI>(e);
-    int mx = 0;
-    if constexpr (MODE == MODE_NL) {
+  for (int i = 0; i < NI; ++i) u[i] = __ldcg(src + (int64_t(i) << 14));
+  int e[2 * NI];
 #pragma unroll
-      for (int k = 0; k < NI; ++k) mx = max(mx, abs(e[k]) + abs(e[k + NI]));
-      mx *= 2;  // values are halved
-    } else {
-#pragma unroll
-      for (int k = 0; k < NI; ++k) {
-        const int p = e[k], q = e[k + NI];
-        e[k] = 2 * (p + q);
-        e[k + NI] = 2 * (p - q);
-        mx = max(mx, max(abs(e[k]), abs(e[k + NI])));
-      }
-      int32_t* dst = a.out + (a.out_row0 + comp) * a.ld + 2 * col;
-#pragma unroll
-      for (int i = 0; i < NI; ++i) {
-        dst[int64_t(i) << 15] = e[2 * i];
-        dst[(int64_t(i) << 15) + 1] = e[2 * i + 1];
-      }
-    }
-    cta_publish_max(mx, s_red, a.max_abs + a.out_row0 + comp, a.key,
-                    a.v_first + uint32_t(comp));
+  for (int i = 0; i < NI; ++i) {
+    e[2 * i] = lo_half(u[i]);
+    e[2 * i + 1] = hi_half(u[i]);
   }
+  fwht_regs_until<2 * NI, 2, NI>(e);
+  int mx = 0;
+  if constexpr (MODE == MODE_NL) {
+#pragma unroll
+    for (int k = 0; k < NI; ++k) mx = max(mx, abs(e[k]) + abs(e[k + NI]));
+    mx *= 2;  // values are halved
+  } else {
+#pragma unroll
+    for (int k = 0; k < NI; ++k) {
+      const int p = e[k], q = e[k + NI];
+      e[k] = 2 * (p + q);
+      e[k + NI] = 2 * (p - q);
+      mx = max(mx, max(abs(e[k]), abs(e[k + NI])));
+    }
+    int32_t* dst = a.out + (a.out_row0 + comp) * a.ld + 2 * col;
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      *reinterpret_cast<int2*>(dst + (int64_t(i) << 15)) = make_int2(e[2 * i], e[2 * i + 1]);
+  }
+  cta_publish_max(mx, s_red, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
 }
 
-// H = 6..9.  A CTA owns (component, 32 pair-columns) x 2^H rows.  Pass B1
-// reads row bits 0..4 straight from the scratch (32 independent coalesced
-// loads in flight per thread), runs those 5 stages and parks int32 pairs in
-// shared memory; pass B2 runs row bits 5..H-1 with the fused top stage.
+// H = 6..9: 32 pair-columns x 2^H rows.  B1 reads row bits 0..4 straight from
+// the scratch (32 independent loads in flight per task) and parks int32 pairs
+// in shared memory; B2 runs row bits 5..H-1 with the fused top stage.
 template <int H, int MODE>
-__global__ void __launch_bounds__(512, 1) k_passb_smem(PassBArgs a) {
+__device__ __forceinline__ void passb_smem_chunk(const PassBArgs& a, int64_t comp, int64_t chunk,
+                                                 int2* tile, int* s_red) {
   constexpr int H2 = H - 5;
   constexpr int N2 = 1 << H2;
-  extern __shared__ int2 tile[];       // [2^H rows][32 columns] int32 pairs
-  __shared__ int s_red[16];
-  const int64_t chunks = (int64_t(1) << 14) / 32;
-  for (int64_t b = blockIdx.x; b < a.n_comp * chunks; b += gridDim.x) {
-    const int64_t comp = b / chunks;
-    const int64_t col0 = (b % chunks) * 32;
-    const uint32_t* src = a.scratch + (comp << (a.n - 1)) + col0;
-    // B1: task = (column c, row-high rh); rows (rh << 5) | i
-    for (int task = threadIdx.x; task < 32 * N2; task += blockDim.x) {
-      const int c = task & 31, rh = task >> 5;
-      uint32_t u[32];
+  const int64_t col0 = chunk * 32;
+  const uint32_t* src = a.scratch + (comp << (a.n - 1)) + col0;
+  for (int task = threadIdx.x; task < 32 * N2; task += blockDim.x) {
+    const int c = task & 31, rh = task >> 5;
+    uint32_t u[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) u[i] = __ldcs(src + (int64_t((rh << 5) | i) << 14) + c);
-      int e[64];
+    for (int i = 0; i < 32; ++i) u[i] = __ldcg(src + (int64_t((rh << 5) | i) << 14) + c);
+    int e[64];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        e[2 * i] = lo_half(u[i]);
-        e[2 * i + 1] = hi_half(u[i]);
-      }
-      fwht_regs<64, 2>(e);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) tile[((rh << 5) | i) * 32 + c] = make_int2(e[2 * i], e[2 * i + 1]);
+    for (int i = 0; i < 32; ++i) {
+      e[2 * i] = lo_half(u[i]);
+      e[2 * i + 1] = hi_half(u[i]);
     }
-    __syncthreads();
-    // B2: row bits 5..H-1, fused top stage
-    int mx = 0;
-    for (int task = threadIdx.x; task < 32 * 32; task += blockDim.x) {
-      const int c = task & 31, rl = task >> 5;
-      int e[2 * N2];
+    fwht_regs<64, 2>(e);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) tile[((rh << 5) | i) * 32 + c] = make_int2(e[2 * i], e[2 * i + 1]);
+  }
+  __syncthreads();
+  int mx = 0;
+  for (int task = threadIdx.x; task < 32 * 32; task += blockDim.x) {
+    const int c = task & 31, rl = task >> 5;
+    int e[2 * N2];
+#pragma unroll
+    for (int i = 0; i < N2; ++i) {
+      const int2 p = tile[((i << 5) | rl) * 32 + c];
+      e[2 * i] = p.x;
+      e[2 * i + 1] = p.y;
+    }
+    fwht_regs_until<2 * N2, 2, N2>(e);
+    if constexpr (MODE == MODE_NL) {
+      int m2 = 0;
+#pragma unroll
+      for (int k = 0; k < N2; ++k) m2 = max(m2, abs(e[k]) + abs(e[k + N2]));
+      mx = max(mx, 2 * m2);
+    } else {
+#pragma unroll
+      for (int k = 0; k < N2; ++k) {
+        const int p = e[k], q = e[k + N2];
+        e[k] = 2 * (p + q);
+        e[k + N2] = 2 * (p - q);
+        mx = max(mx, max(abs(e[k]), abs(e[k + N2])));
+      }
+      int32_t* dst = a.out + (a.out_row0 + comp) * a.ld + 2 * (col0 + c);
 #pragma unroll
       for (int i = 0; i < N2; ++i) {
-        const int2 p = tile[((i << 5) | rl) * 32 + c];
-        e[2 * i] = p.x;
-        e[2 * i + 1] = p.y;
-      }
-      fwht_regs_until<2 * N2, 2, N2>(e);
-      if constexpr (MODE == MODE_NL) {
-        int m2 = 0;
-#pragma unroll
-        for (int k = 0; k < N2; ++k) m2 = max(m2, abs(e[k]) + abs(e[k + N2]));
-        mx = max(mx, 2 * m2);
-      } else {
-#pragma unroll
-        for (int k = 0; k < N2; ++k) {
-          const int p = e[k], q = e[k + N2];
-          e[k] = 2 * (p + q);
-          e[k + N2] = 2 * (p - q);
-          mx = max(mx, max(abs(e[k]), abs(e[k + N2])));
-        }
-        int32_t* dst = a.out + (a.out_row0 + comp) * a.ld + 2 * (col0 + c);
-#pragma unroll
-        for (int i = 0; i < N2; ++i) {
-          const int64_t row = (int64_t(i) << 5) | rl;
-          dst[row << 15] = e[2 * i];
-          dst[(row << 15) + 1] = e[2 * i + 1];
-        }
+        const int64_t row = (int64_t(i) << 5) | rl;
+        *reinterpret_cast<int2*>(dst + (row << 15)) = make_int2(e[2 * i], e[2 * i + 1]);
       }
     }
-    cta_publish_max(mx, s_red, a.max_abs + a.out_row0 + comp, a.key,
-                    a.v_first + uint32_t(comp));
+  }
+  cta_publish_max(mx, s_red, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
+}
+
+// ---- persistent multi-pass kernel ------------------------------------------
+// One CTA per SM pulls work items from a global counter in a fixed order:
+//   A(0) .. A(D-1) | A(D) B(0) | A(D+1) B(1) | ... | B(C-D) .. B(C-1)
+// where A(c) = the 2^(n-16) pass-A tiles of component c and B(c) = its pass-B
+// chunks, and the lookahead D puts several waves of items between A(c) and
+// B(c).  B(c) waits (acquire) until all A(c) tiles are published; A(c) waits
+// until B(c - R) (R > D) has released ring slot c % R.  Every item waits only
+// on items dequeued before it by running CTAs, so progress is guaranteed, and
+// at most R components of scratch are live, which keeps them in L2.
+struct K3Args {
+  TileArgs ta;              // planes etc.; EMIT fields are set per item
+  PassBArgs pb;             // n, max_abs, key, out, ld; per-item fields set per item
+  uint32_t v_lo;
+  int64_t ncomp;
+  uint32_t* ring;           // R slots of 2^(n-1) u16-pair words
+  int ring_slots;
+  int64_t lookahead;        // D: B(c) is queued after A(c + D); 1 <= D < R, D <= ncomp
+  unsigned int* counters;   // [0] = queue head, [1 + c] = A done, [1 + ncomp + c] = B done
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void wait_counter(const unsigned* p, unsigned target) {
+  if (threadIdx.x == 0) {
+    while (ld_acquire(p) < target) __nanosleep(256);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void release_counter(unsigned* p) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(p, 1u);
+}
+
+template <int H, int MODE>
+__global__ void __launch_bounds__(512, 1) k3_persistent(K3Args a) {
+  constexpr int THREADS = 512;
+  constexpr int64_t NA = int64_t(1) << (H - 1);        // pass-A tiles per component
+  constexpr int64_t NB = H <= 5 ? (int64_t(1) << 14) / THREADS : (int64_t(1) << 14) / 32;
+  extern __shared__ uint4 smem4[];
+  __shared__ int s_max[2];
+  __shared__ int s_red[THREADS / 32];
+  __shared__ long long s_item;
+  const int64_t total = a.ncomp * (NA + NB);
+  unsigned* head = a.counters;
+  unsigned* done_a = a.counters + 1;
+  unsigned* done_b = a.counters + 1 + a.ncomp;
+  const int64_t slot_words = int64_t(1) << (a.pb.n - 1);
+  GenState<1024 / THREADS> gs;
+  gs.reset();
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(head, 1u);
+    __syncthreads();
+    const int64_t item = s_item;
+    __syncthreads();
+    if (item >= total) break;
+    // decode the item (see the sequence above)
+    const int64_t D = a.lookahead, C = a.ncomp;
+    int64_t c, k;
+    bool is_a;
+    if (item < D * NA) {
+      c = item / NA, k = item - c * NA, is_a = true;
+    } else if (item - D * NA < (C - D) * (NA + NB)) {
+      const int64_t r = item - D * NA;
+      const int64_t j = D + r / (NA + NB), off = r - (j - D) * (NA + NB);
+      is_a = off < NA;
+      c = is_a ? j : j - D;
+      k = is_a ? off : off - NA;
+    } else {
+      const int64_t r = item - D * NA - (C - D) * (NA + NB);
+      c = C - D + r / NB, k = r - (c - (C - D)) * NB, is_a = false;
+    }
+    uint32_t* slot = a.ring + (c % a.ring_slots) * slot_words;
+    if (is_a) {
+      if (c >= a.ring_slots) wait_counter(done_b + (c - a.ring_slots), unsigned(NB));
+      TileArgs ta = a.ta;
+      ta.v_first = a.v_lo + uint32_t(c);
+      ta.n_comp = 1;
+      ta.emit = slot;
+      tile_body<15, MODE_EMIT, THREADS>(ta, k, smem4, s_max, gs);
+      release_counter(done_a + c);
+    } else {
+      wait_counter(done_a + c, unsigned(NA));
+      PassBArgs pb = a.pb;
+      pb.scratch = slot;
+      pb.n_comp = 1;
+      pb.out_row0 = c;
+      pb.v_first = a.v_lo + uint32_t(c);
+      if constexpr (H <= 5) {
+        passb_regs_chunk<H, MODE, THREADS>(pb, 0, k, s_red);
+      } else {
+        passb_smem_chunk<H, MODE>(pb, 0, k, reinterpret_cast<int2*>(smem4), s_red);
+      }
+      release_counter(done_b + c);
+    }
   }
 }
 

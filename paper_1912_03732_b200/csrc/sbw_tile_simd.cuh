@@ -238,8 +238,26 @@ __device__ __forceinline__ void tile_last_pass(const TileArgs& a, uint32_t (&E)[
   }
 }
 
-template <int N, int MODE, int THREADS = kTileThreads>
-__global__ void __launch_bounds__(THREADS, 1) k_tile_simd(TileArgs a) {
+// Per-thread generation state of the pass-1 tasks (bits of the previous mask).
+template <int ROUNDS>
+struct GenState {
+  uint32_t v[ROUNDS], w0[ROUNDS], w1[ROUNDS];
+  int64_t cw[ROUNDS];
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int r = 0; r < ROUNDS; ++r) {
+      v[r] = w0[r] = w1[r] = 0;
+      cw[r] = -1;
+    }
+  }
+};
+
+// One tile t (see the file comment): three passes over the shared-memory
+// tile, result published per component (NL / SPEC) or emitted (EMIT).  Must be
+// called by all THREADS threads of the CTA.
+template <int N, int MODE, int THREADS>
+__device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* smem4, int* s_max,
+                                          GenState<1024 / THREADS>& gs) {
   constexpr int ROUNDS = 1024 / THREADS;         // pass-1 tasks per thread
   static_assert(N >= 7 && N <= 16, "tile kernel covers n = 7..16");
   static_assert(MODE != MODE_EMIT || N == 15, "EMIT works on 2^15 blocks");
@@ -248,163 +266,162 @@ __global__ void __launch_bounds__(THREADS, 1) k_tile_simd(TileArgs a) {
   constexpr int B2 = (N - 6) < 5 ? (N - 6) : 5;  // x bits in pass 2
   constexpr int B3 = N > 11 ? N - 11 : 0;        // x bits in pass 3
   constexpr int XMASK = (1 << N) - 1;
-  extern __shared__ uint4 smem4[];
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
-  __shared__ int s_max[C];
-
   const int tid = threadIdx.x;
-  const int64_t t_lo = a.t_begin + (a.t_count * blockIdx.x) / gridDim.x;
-  const int64_t t_hi = a.t_begin + (a.t_count * (blockIdx.x + 1)) / gridDim.x;
+  uint32_t* g_v = gs.v;
+  uint32_t* g_w0 = gs.w0;
+  uint32_t* g_w1 = gs.w1;
+  int64_t* g_cw = gs.cw;
+  if (tid < C) s_max[tid] = 0;
 
-  // generation state of the pass-1 tasks this thread owns
-  uint32_t g_v[ROUNDS], g_w0[ROUNDS], g_w1[ROUNDS];
-  int64_t g_cw[ROUNDS];
+  // ---------------- pass 1: generation + x bits 0..5 ---------------------
 #pragma unroll
   for (int r = 0; r < ROUNDS; ++r) {
-    g_v[r] = g_w0[r] = g_w1[r] = 0;
-    g_cw[r] = -1;
-  }
-
-  for (int64_t t = t_lo; t < t_hi; ++t) {
-    if (tid < C) s_max[tid] = 0;
-
-    // ---------------- pass 1: generation + x bits 0..5 ---------------------
-#pragma unroll
-    for (int r = 0; r < ROUNDS; ++r) {
-      const int task = r * THREADS + tid;
-      const int p0 = task << 6;
-      const int slot = p0 >> N;
-      const int x0 = p0 & XMASK;
-      uint32_t v = 0;
-      int64_t cw = 0;
-      bool valid;
-      if constexpr (MODE == MODE_EMIT) {
-        const int64_t bp = t / a.n_comp, ci = t - bp * a.n_comp;
-        v = a.v_first + uint32_t(ci);
-        cw = ((2 * bp + slot) * (int64_t(1) << 15) + x0) >> 5;
-        valid = true;
-      } else {
-        const int64_t vv = t * C + slot;
-        v = uint32_t(vv);
-        cw = x0 >> 5;
-        valid = vv >= a.v_lo && vv < a.v_hi;
-      }
-      uint32_t w0 = 0, w1 = 0;
-      if (valid) {
-        uint32_t delta = v;
-        if (cw == g_cw[r]) {
-          delta = v ^ g_v[r];
-          w0 = g_w0[r];
-          w1 = g_w1[r];
-        }
-        apply_planes(a.planes, a.plane_words, delta, cw, w0, w1);
-        g_v[r] = v;
-        g_w0[r] = w0;
-        g_w1[r] = w1;
-        g_cw[r] = cw;
-      }
-      // bytes: R[h*8 + r'] lane l <- 1 - g(x), x = 32h + 8l + r'  (s at k = 0)
-      uint32_t R[16];
-      const uint32_t n0 = ~w0, n1 = ~w1;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        R[q] = (n0 >> q) & 0x01010101u;
-        R[8 + q] = (n1 >> q) & 0x01010101u;
-      }
-      // byte stages on register bits (x bits 0,1,2,5), k = 0..3
-#pragma unroll
-      for (int i = 0; i < 16; ++i) if (!(i & 1)) bfly8<0>(R[i], R[i | 1]);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) if (!(i & 2)) bfly8<1>(R[i], R[i | 2]);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) if (!(i & 4)) bfly8<2>(R[i], R[i | 4]);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) if (!(i & 8)) bfly8<3>(R[i], R[i | 8]);
-      // unpack: H[q], q = (x1, x2, x3, x4, x5) bits 0..4; 16-bit lane = x0.
-      // source bytes: R[(x5 << 3) | (x2 << 2) | (x1 << 1) | x0], byte lane (x4 << 1) | x3.
-      // Values are <= 16 after 4 stages, so PRMT sign-replicate yields 0x00.
-      uint32_t H[32];
-#pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        const int x1 = q & 1, x2 = (q >> 1) & 1, l = (q >> 2) & 3, x5 = (q >> 4) & 1;
-        const int i0 = (x5 << 3) | (x2 << 2) | (x1 << 1);
-        const uint32_t sel = uint32_t(l) | (uint32_t(8 | l) << 4) | (uint32_t(4 + l) << 8) |
-                             (uint32_t(8 | (4 + l)) << 12);
-        H[q] = prmt(R[i0], R[i0 | 1], sel);
-      }
-      // 16-bit stages on x3 (H bit 2) and x4 (H bit 3), k = 4, 5
-      stages16<32, 2, 4, 4>(H);
-      // store: task's 32 words as 8 x 16 B, chunk-swizzled
-      uint4* dst = smem4 + (task << 3);
-#pragma unroll
-      for (int c4 = 0; c4 < 8; ++c4)
-        dst[c4 ^ (task & 7)] = make_uint4(H[4 * c4], H[4 * c4 + 1], H[4 * c4 + 2], H[4 * c4 + 3]);
+    const int task = r * THREADS + tid;
+    const int p0 = task << 6;
+    const int slot = p0 >> N;
+    const int x0 = p0 & XMASK;
+    uint32_t v = 0;
+    int64_t cw = 0;
+    bool valid;
+    if constexpr (MODE == MODE_EMIT) {
+      const int64_t bp = t / a.n_comp, ci = t - bp * a.n_comp;
+      v = a.v_first + uint32_t(ci);
+      cw = ((2 * bp + slot) * (int64_t(1) << 15) + x0) >> 5;
+      valid = true;
+    } else {
+      const int64_t vv = t * C + slot;
+      v = uint32_t(vv);
+      cw = x0 >> 5;
+      valid = vv >= a.v_lo && vv < a.v_hi;
     }
-    __syncthreads();
+    uint32_t w0 = 0, w1 = 0;
+    if (valid) {
+      uint32_t delta = v;
+      if (cw == g_cw[r]) {
+        delta = v ^ g_v[r];
+        w0 = g_w0[r];
+        w1 = g_w1[r];
+      }
+      apply_planes(a.planes, a.plane_words, delta, cw, w0, w1);
+      g_v[r] = v;
+      g_w0[r] = w0;
+      g_w1[r] = w1;
+      g_cw[r] = cw;
+    }
+    // bytes: R[h*8 + r'] lane l <- 1 - g(x), x = 32h + 8l + r'  (s at k = 0)
+    uint32_t R[16];
+    const uint32_t n0 = ~w0, n1 = ~w1;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      R[q] = (n0 >> q) & 0x01010101u;
+      R[8 + q] = (n1 >> q) & 0x01010101u;
+    }
+    // byte stages on register bits (x bits 0,1,2,5), k = 0..3
+#pragma unroll
+    for (int i = 0; i < 16; ++i) if (!(i & 1)) bfly8<0>(R[i], R[i | 1]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) if (!(i & 2)) bfly8<1>(R[i], R[i | 2]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) if (!(i & 4)) bfly8<2>(R[i], R[i | 4]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) if (!(i & 8)) bfly8<3>(R[i], R[i | 8]);
+    // unpack: H[q], q = (x1, x2, x3, x4, x5) bits 0..4; 16-bit lane = x0.
+    // source bytes: R[(x5 << 3) | (x2 << 2) | (x1 << 1) | x0], byte lane (x4 << 1) | x3.
+    // Values are <= 16 after 4 stages, so PRMT sign-replicate yields 0x00.
+    uint32_t H[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int x1 = q & 1, x2 = (q >> 1) & 1, l = (q >> 2) & 3, x5 = (q >> 4) & 1;
+      const int i0 = (x5 << 3) | (x2 << 2) | (x1 << 1);
+      const uint32_t sel = uint32_t(l) | (uint32_t(8 | l) << 4) | (uint32_t(4 + l) << 8) |
+                           (uint32_t(8 | (4 + l)) << 12);
+      H[q] = prmt(R[i0], R[i0 | 1], sel);
+    }
+    // 16-bit stages on x3 (H bit 2) and x4 (H bit 3), k = 4, 5
+    stages16<32, 2, 4, 4>(H);
+    // store: task's 32 words as 8 x 16 B, chunk-swizzled
+    uint4* dst = smem4 + (task << 3);
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4)
+      dst[c4 ^ (task & 7)] = make_uint4(H[4 * c4], H[4 * c4 + 1], H[4 * c4 + 2], H[4 * c4 + 3]);
+  }
+  __syncthreads();
 
-    // ---------------- pass 2: x bits 6 .. 6+B2-1 ---------------------------
-    {
-      constexpr int NI = 1 << B2;
-      constexpr int NT = kTileWords >> B2;
-      constexpr bool LAST = (B3 == 0);
-      for (int task = tid; task < NT; task += THREADS) {
-        const int lo = task & 31, hi = task >> 5;
-        const int wb = (hi << (5 + B2)) | lo;
-        // phys(wb | i << 5) = (P ^ ((i & 7) << 2)) + (i << 5), P = phys(wb):
-        // at most 8 base pointers, the rest are immediate offsets
-        const int P = phys_word(wb);
-        uint32_t E[NI];
+  // ---------------- pass 2: x bits 6 .. 6+B2-1 ---------------------------
+  {
+    constexpr int NI = 1 << B2;
+    constexpr int NT = kTileWords >> B2;
+    constexpr bool LAST = (B3 == 0);
+    for (int task = tid; task < NT; task += THREADS) {
+      const int lo = task & 31, hi = task >> 5;
+      const int wb = (hi << (5 + B2)) | lo;
+      // phys(wb | i << 5) = (P ^ ((i & 7) << 2)) + (i << 5), P = phys(wb):
+      // at most 8 base pointers, the rest are immediate offsets
+      const int P = phys_word(wb);
+      uint32_t E[NI];
 #pragma unroll
-        for (int i = 0; i < NI; ++i) E[i] = sm[(P ^ ((i & 7) << 2)) + (i << 5)];
-        if constexpr (!LAST) {
+      for (int i = 0; i < NI; ++i) E[i] = sm[(P ^ ((i & 7) << 2)) + (i << 5)];
+      if constexpr (!LAST) {
 #if SBW_PASS2_FP16
-          // stages k = 6..10 as exact fp16x2 add/sub on the FMA pipe
+        // stages k = 6..10 as exact fp16x2 add/sub on the FMA pipe
 #pragma unroll
-          for (int i = 0; i < NI; ++i) E[i] = to_signed_h2<6>(E[i]);
-          stages_h2<NI, 0, B2>(E);
+        for (int i = 0; i < NI; ++i) E[i] = to_signed_h2<6>(E[i]);
+        stages_h2<NI, 0, B2>(E);
 #pragma unroll
-          for (int i = 0; i < NI; ++i) E[i] = to_biased_h2<6 + B2>(E[i]);
+        for (int i = 0; i < NI; ++i) E[i] = to_biased_h2<6 + B2>(E[i]);
 #else
-          stages16<NI, 0, B2, 6>(E);
+        stages16<NI, 0, B2, 6>(E);
 #endif
 #pragma unroll
-          for (int i = 0; i < NI; ++i) sm[(P ^ ((i & 7) << 2)) + (i << 5)] = E[i];
-        } else {
-          tile_last_pass<N, MODE, NI, 5, 6>(a, E, wb, t, s_max);
-        }
+        for (int i = 0; i < NI; ++i) sm[(P ^ ((i & 7) << 2)) + (i << 5)] = E[i];
+      } else {
+        tile_last_pass<N, MODE, NI, 5, 6>(a, E, wb, t, s_max);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---------------- pass 3: x bits 11 .. N-1 ------------------------------
+  if constexpr (B3 > 0) {
+    constexpr int NI = 1 << B3;
+    constexpr int NT = kTileWords >> B3;
+    for (int task = tid; task < NT; task += THREADS) {
+      const int lo = task & 1023, hi = task >> 10;
+      const int wb = (hi << (10 + B3)) | lo;
+      // the swizzle depends on word bits 5..7 only, so phys(wb | i << 10) = phys(wb) + (i << 10)
+      const uint32_t* base = sm + phys_word(wb);
+      uint32_t E[NI];
+#pragma unroll
+      for (int i = 0; i < NI; ++i) E[i] = base[i << 10];
+      tile_last_pass<N, MODE, NI, 10, 11>(a, E, wb, t, s_max);
+    }
+    __syncthreads();
+  }
+
+  if constexpr (MODE != MODE_EMIT) {
+    if (tid < C) {
+      const int64_t vv = t * C + tid;
+      if (vv >= a.v_lo && vv < a.v_hi) {
+        const int mx = s_max[tid];
+        a.max_abs[vv - a.v_lo] = mx;
+        if (a.key) atomicMax(a.key, nl_key(mx, uint32_t(vv)));
       }
     }
     __syncthreads();
-
-    // ---------------- pass 3: x bits 11 .. N-1 ------------------------------
-    if constexpr (B3 > 0) {
-      constexpr int NI = 1 << B3;
-      constexpr int NT = kTileWords >> B3;
-      for (int task = tid; task < NT; task += THREADS) {
-        const int lo = task & 1023, hi = task >> 10;
-        const int wb = (hi << (10 + B3)) | lo;
-        // the swizzle depends on word bits 5..7 only, so phys(wb | i << 10) = phys(wb) + (i << 10)
-        const uint32_t* base = sm + phys_word(wb);
-        uint32_t E[NI];
-#pragma unroll
-        for (int i = 0; i < NI; ++i) E[i] = base[i << 10];
-        tile_last_pass<N, MODE, NI, 10, 11>(a, E, wb, t, s_max);
-      }
-      __syncthreads();
-    }
-
-    if constexpr (MODE != MODE_EMIT) {
-      if (tid < C) {
-        const int64_t vv = t * C + tid;
-        if (vv >= a.v_lo && vv < a.v_hi) {
-          const int mx = s_max[tid];
-          a.max_abs[vv - a.v_lo] = mx;
-          if (a.key) atomicMax(a.key, nl_key(mx, uint32_t(vv)));
-        }
-      }
-      __syncthreads();
-    }
   }
+}
+
+template <int N, int MODE, int THREADS = kTileThreads>
+__global__ void __launch_bounds__(THREADS, 1) k_tile_simd(TileArgs a) {
+  constexpr int C = 1 << (16 - N);
+  extern __shared__ uint4 smem4[];
+  __shared__ int s_max[C];
+  const int64_t t_lo = a.t_begin + (a.t_count * blockIdx.x) / gridDim.x;
+  const int64_t t_hi = a.t_begin + (a.t_count * (blockIdx.x + 1)) / gridDim.x;
+  GenState<1024 / THREADS> gs;
+  gs.reset();
+  for (int64_t t = t_lo; t < t_hi; ++t) tile_body<N, MODE, THREADS>(a, t, smem4, s_max, gs);
 }
 
 }  // namespace sbw
