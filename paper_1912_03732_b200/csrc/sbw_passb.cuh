@@ -188,10 +188,11 @@ __device__ __forceinline__ void wait_counter(const unsigned* p, unsigned target)
   __syncthreads();
 }
 
+// bar.sync orders every thread's writes before thread 0's release-add (PTX
+// release is cumulative), so one fence-carrying atomic publishes the CTA's work.
 __device__ __forceinline__ void release_counter(unsigned* p) {
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) atomicAdd(p, 1u);
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
 }
 
 template <int H, int MODE>
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(512, 1) k3_persistent(K3Args a) {
   extern __shared__ uint4 smem4[];
   __shared__ int s_max[2];
   __shared__ int s_red[THREADS / 32];
-  __shared__ long long s_item;
+  __shared__ long long s_item[2];  // current / next queue item (prefetched by thread 0)
   const int64_t total = a.ncomp * (NA + NB);
   unsigned* head = a.counters;
   unsigned* done_a = a.counters + 1;
@@ -210,12 +211,14 @@ __global__ void __launch_bounds__(512, 1) k3_persistent(K3Args a) {
   const int64_t slot_words = int64_t(1) << (a.pb.n - 1);
   GenState<1024 / THREADS> gs;
   gs.reset();
-  for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(head, 1u);
-    __syncthreads();
-    const int64_t item = s_item;
-    __syncthreads();
+  if (threadIdx.x == 0) s_item[0] = atomicAdd(head, 1u);
+  __syncthreads();
+  for (int it = 0;; it ^= 1) {
+    const int64_t item = s_item[it];
     if (item >= total) break;
+    // fetch the next item now; every item body ends with a barrier, which
+    // publishes s_item[it ^ 1] before the next iteration reads it
+    if (threadIdx.x == 0) s_item[it ^ 1] = atomicAdd(head, 1u);
     // decode the item (see the sequence above)
     const int64_t D = a.lookahead, C = a.ncomp;
     int64_t c, k;
