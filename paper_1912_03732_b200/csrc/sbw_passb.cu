@@ -2,6 +2,9 @@
 // that interleaves pass A (generation + 15 on-chip stages, biased u16 to an
 // L2-resident ring of scratch slots) and pass B (stages 15..n-1 + fused
 // max|W|) through an ordered work queue.  See sbw_passb.cuh.
+#include <cstdio>
+#include <cstdlib>
+
 #include "sbw_launch.h"
 #include "sbw_passb.cuh"
 
@@ -27,7 +30,7 @@ int64_t lookahead(int n, int64_t ncomp) {
 int ring_slots(int n, int64_t ncomp) {
   const size_t per = size_t(2) << n;  // u16 bytes per component
   int64_t r = int64_t(kRingBudget / per);
-  const int64_t need = lookahead(n, ncomp) + 2;  // R > D, with one slot of slack
+  const int64_t need = lookahead(n, ncomp) + 2;  // R > D, plus one slot of slack (R = D + 1 measured slower)
   if (r < need) r = need;
   return int(r);
 }
@@ -39,7 +42,7 @@ int run_persistent(const K3Args& a, cudaStream_t st) {
   DeviceProps dp;
   if (int rc = device_props(&dp)) return rc;
   auto kern = k3_persistent<H, MODE>;
-  constexpr size_t kSmem = size_t(kTileWords) * sizeof(uint32_t);  // 128 KiB: tile or pass-B rows
+  constexpr size_t kSmem = kK3Smem;  // 128 KiB tile / pass-B rows + 64 KiB staging
   static unsigned long long attr_done = 0;
   if (!(attr_done >> (dp.device & 63) & 1ull)) {
     SBW_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -111,7 +114,28 @@ int launch_k3(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32
   a.ring_slots = R;
   a.lookahead = lookahead(n, ncomp);
   a.counters = counters;
-  return out ? dispatch_h<MODE_SPEC>(n - 15, a, st) : dispatch_h<MODE_NL>(n - 15, a, st);
+  // SBW_K3_PROF=1 (debugging aid): per-item cycle accounting printed to stderr
+  static const bool prof = getenv("SBW_K3_PROF") != nullptr;
+  unsigned long long* dprof = nullptr;
+  if (prof) {
+    SBW_CUDA_CHECK(cudaMallocAsync(&dprof, 8 * sizeof(unsigned long long), st));
+    SBW_CUDA_CHECK(cudaMemsetAsync(dprof, 0, 8 * sizeof(unsigned long long), st));
+    a.prof = dprof;
+  }
+  const int rc = out ? dispatch_h<MODE_SPEC>(n - 15, a, st) : dispatch_h<MODE_NL>(n - 15, a, st);
+  if (prof) {
+    unsigned long long h[8];
+    SBW_CUDA_CHECK(cudaMemcpyAsync(h, dprof, sizeof(h), cudaMemcpyDeviceToHost, st));
+    SBW_CUDA_CHECK(cudaStreamSynchronize(st));
+    cudaFreeAsync(dprof, st);
+    fprintf(stderr,
+            "[k3 prof] n=%d comps=%lld R=%d D=%lld | A items %llu avg %.0f cyc (wait %.0f) | "
+            "B items %llu avg %.0f cyc (counter wait %.0f, stage wait %.0f, prefetched %llu)\n",
+            n, (long long)ncomp, R, (long long)a.lookahead, h[5], h[5] ? double(h[0]) / h[5] : 0.0,
+            h[5] ? double(h[1]) / h[5] : 0.0, h[6], h[6] ? double(h[2]) / h[6] : 0.0,
+            h[6] ? double(h[3]) / h[6] : 0.0, h[6] ? double(h[4]) / h[6] : 0.0, h[7]);
+  }
+  return rc;
 }
 
 }  // namespace sbw

@@ -53,19 +53,53 @@ __device__ __forceinline__ void cta_publish_max(int mx, int* s_red, int32_t* slo
 }
 
 // ---- pass-B chunk bodies (called by every thread of the CTA) --------------
-// Scratch reads use ld.global.cg: the persistent kernel reuses ring slots, so
-// an SM's L1 may hold lines of an older component.
+// A chunk's u16-pair words are first staged in shared memory by cp.async.cg
+// (16-byte pieces, L2 only: the persistent kernel reuses ring slots, so an
+// SM's L1 may hold lines of an older component).  Staging is asynchronous, so
+// the copy of chunk i+1 overlaps the arithmetic of chunk i.
 
-// H <= 5: THREADS pair-columns of one component, 2^H rows each, in registers.
-template <int H, int MODE, int THREADS>
+template <int H, int THREADS>
+struct ChunkShape {
+  static constexpr int R = 1 << H;                 // rows (x bits 15..n-1)
+  static constexpr int CW = H <= 5 ? THREADS : 32; // pair-columns (words) per chunk
+  static constexpr int64_t PER_COMP = (int64_t(1) << 14) / CW;
+  static constexpr int PIECES = R * CW / 4;        // 16-byte pieces
+};
+
+// Issue (not wait for) the copies of chunk `chunk` of a component whose
+// scratch starts at `comp_base` into `stg` ([R][CW] words).
+template <int H, int THREADS>
+__device__ __forceinline__ void stage_chunk(const uint32_t* comp_base, int64_t chunk, uint32_t* stg) {
+  using S = ChunkShape<H, THREADS>;
+  constexpr int PR = S::CW / 4;  // pieces per row
+  const int64_t col0 = chunk * S::CW;
+  for (int p = threadIdx.x; p < S::PIECES; p += THREADS) {
+    const int r = p / PR, q = p - (p / PR) * PR;
+    const uint32_t* g = comp_base + (int64_t(r) << 14) + col0 + 4 * q;
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(stg + r * S::CW + 4 * q));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void stage_wait() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+}
+
+// H <= 5: THREADS pair-columns, 2^H rows each, in registers.  `after_read`
+// runs (by every thread) once the staging buffer is no longer needed.
+template <int H, int MODE, int THREADS, typename AfterRead>
 __device__ __forceinline__ void passb_regs_chunk(const PassBArgs& a, int64_t comp, int64_t chunk,
-                                                 int* s_red) {
+                                                 const uint32_t* stg, int* s_red,
+                                                 AfterRead after_read) {
   constexpr int NI = 1 << H;
   const int64_t col = chunk * THREADS + threadIdx.x;
-  const uint32_t* src = a.scratch + (comp << (a.n - 1)) + col;
   uint32_t u[NI];
 #pragma unroll
-  for (int i = 0; i < NI; ++i) u[i] = __ldcg(src + (int64_t(i) << 14));
+  for (int i = 0; i < NI; ++i) u[i] = stg[i * THREADS + threadIdx.x];
+  __syncthreads();
+  after_read();
   int e[2 * NI];
 #pragma unroll
   for (int i = 0; i < NI; ++i) {
@@ -94,32 +128,31 @@ __device__ __forceinline__ void passb_regs_chunk(const PassBArgs& a, int64_t com
   cta_publish_max(mx, s_red, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
 }
 
-// H = 6..9: 32 pair-columns x 2^H rows.  B1 reads row bits 0..4 straight from
-// the scratch (32 independent loads in flight per task) and parks int32 pairs
-// in shared memory; B2 runs row bits 5..H-1 with the fused top stage.
-template <int H, int MODE>
+// H = 6..9: 32 pair-columns x 2^H rows.  B1 runs row bits 0..4 from the
+// staging buffer and parks int32 pairs in `tile`; B2 runs row bits 5..H-1
+// with the fused top stage.
+template <int H, int MODE, typename AfterRead>
 __device__ __forceinline__ void passb_smem_chunk(const PassBArgs& a, int64_t comp, int64_t chunk,
-                                                 int2* tile, int* s_red) {
+                                                 const uint32_t* stg, int2* tile, int* s_red,
+                                                 AfterRead after_read) {
   constexpr int H2 = H - 5;
   constexpr int N2 = 1 << H2;
   const int64_t col0 = chunk * 32;
-  const uint32_t* src = a.scratch + (comp << (a.n - 1)) + col0;
   for (int task = threadIdx.x; task < 32 * N2; task += blockDim.x) {
     const int c = task & 31, rh = task >> 5;
-    uint32_t u[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) u[i] = __ldcg(src + (int64_t((rh << 5) | i) << 14) + c);
     int e[64];
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      e[2 * i] = lo_half(u[i]);
-      e[2 * i + 1] = hi_half(u[i]);
+      const uint32_t u = stg[((rh << 5) | i) * 32 + c];
+      e[2 * i] = lo_half(u);
+      e[2 * i + 1] = hi_half(u);
     }
     fwht_regs<64, 2>(e);
 #pragma unroll
     for (int i = 0; i < 32; ++i) tile[((rh << 5) | i) * 32 + c] = make_int2(e[2 * i], e[2 * i + 1]);
   }
   __syncthreads();
+  after_read();
   int mx = 0;
   for (int task = threadIdx.x; task < 32 * 32; task += blockDim.x) {
     const int c = task & 31, rl = task >> 5;
@@ -173,12 +206,22 @@ struct K3Args {
   int ring_slots;
   int64_t lookahead;        // D: B(c) is queued after A(c + D); 1 <= D < R, D <= ncomp
   unsigned int* counters;   // [0] = queue head, [1 + c] = A done, [1 + ncomp + c] = B done
+  unsigned long long* prof; // optional (debug): cycle accounting, see k3_persistent
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+// Non-blocking, CTA-uniform check (one barrier).
+__device__ __forceinline__ bool counter_reached(const unsigned* p, unsigned target, int* flag) {
+  if (threadIdx.x == 0) *flag = ld_acquire(p) >= target;
+  __syncthreads();
+  const bool r = *flag != 0;
+  __syncthreads();
+  return r;
 }
 
 __device__ __forceinline__ void wait_counter(const unsigned* p, unsigned target) {
@@ -195,15 +238,44 @@ __device__ __forceinline__ void release_counter(unsigned* p) {
   if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
 }
 
+struct K3Item {
+  int64_t c, k;
+  bool is_a;
+};
+
+// Decode a queue index (see the sequence above).
+template <int64_t NA, int64_t NB>
+__device__ __forceinline__ K3Item k3_decode(int64_t item, int64_t D, int64_t C) {
+  K3Item r;
+  if (item < D * NA) {
+    r.c = item / NA, r.k = item - r.c * NA, r.is_a = true;
+  } else if (item - D * NA < (C - D) * (NA + NB)) {
+    const int64_t q = item - D * NA;
+    const int64_t j = D + q / (NA + NB), off = q - (j - D) * (NA + NB);
+    r.is_a = off < NA;
+    r.c = r.is_a ? j : j - D;
+    r.k = r.is_a ? off : off - NA;
+  } else {
+    const int64_t q = item - D * NA - (C - D) * (NA + NB);
+    r.c = C - D + q / NB, r.k = q - (r.c - (C - D)) * NB, r.is_a = false;
+  }
+  return r;
+}
+
+constexpr size_t kK3Smem = size_t(kTileWords) * sizeof(uint32_t) + (size_t(64) << 10);
+
 template <int H, int MODE>
 __global__ void __launch_bounds__(512, 1) k3_persistent(K3Args a) {
   constexpr int THREADS = 512;
-  constexpr int64_t NA = int64_t(1) << (H - 1);        // pass-A tiles per component
-  constexpr int64_t NB = H <= 5 ? (int64_t(1) << 14) / THREADS : (int64_t(1) << 14) / 32;
-  extern __shared__ uint4 smem4[];
+  using S = ChunkShape<H, THREADS>;
+  constexpr int64_t NA = int64_t(1) << (H - 1);  // pass-A tiles per component
+  constexpr int64_t NB = S::PER_COMP;            // pass-B chunks per component
+  extern __shared__ uint4 smem4[];               // [128 KiB tile / int32 rows][64 KiB staging]
+  uint32_t* stg = reinterpret_cast<uint32_t*>(smem4) + kTileWords;
   __shared__ int s_max[2];
   __shared__ int s_red[THREADS / 32];
   __shared__ long long s_item[2];  // current / next queue item (prefetched by thread 0)
+  __shared__ int s_flag;
   const int64_t total = a.ncomp * (NA + NB);
   unsigned* head = a.counters;
   unsigned* done_a = a.counters + 1;
@@ -211,6 +283,11 @@ __global__ void __launch_bounds__(512, 1) k3_persistent(K3Args a) {
   const int64_t slot_words = int64_t(1) << (a.pb.n - 1);
   GenState<1024 / THREADS> gs;
   gs.reset();
+  int64_t staged = -1;  // queue item whose chunk is in (or in flight to) `stg`
+  // Counters only grow, so a condition this CTA has seen satisfied stays
+  // satisfied: skip the acquire round trip (and its barrier) when possible.
+  int64_t seen_a = -1;  // largest c with done_a[c] == NA observed
+  int64_t seen_b = -1;  // component c whose done_b[c] == NB was observed
   if (threadIdx.x == 0) s_item[0] = atomicAdd(head, 1u);
   __syncthreads();
   for (int it = 0;; it ^= 1) {
@@ -219,46 +296,75 @@ __global__ void __launch_bounds__(512, 1) k3_persistent(K3Args a) {
     // fetch the next item now; every item body ends with a barrier, which
     // publishes s_item[it ^ 1] before the next iteration reads it
     if (threadIdx.x == 0) s_item[it ^ 1] = atomicAdd(head, 1u);
-    // decode the item (see the sequence above)
-    const int64_t D = a.lookahead, C = a.ncomp;
-    int64_t c, k;
-    bool is_a;
-    if (item < D * NA) {
-      c = item / NA, k = item - c * NA, is_a = true;
-    } else if (item - D * NA < (C - D) * (NA + NB)) {
-      const int64_t r = item - D * NA;
-      const int64_t j = D + r / (NA + NB), off = r - (j - D) * (NA + NB);
-      is_a = off < NA;
-      c = is_a ? j : j - D;
-      k = is_a ? off : off - NA;
-    } else {
-      const int64_t r = item - D * NA - (C - D) * (NA + NB);
-      c = C - D + r / NB, k = r - (c - (C - D)) * NB, is_a = false;
-    }
-    uint32_t* slot = a.ring + (c % a.ring_slots) * slot_words;
-    if (is_a) {
-      if (c >= a.ring_slots) wait_counter(done_b + (c - a.ring_slots), unsigned(NB));
+    const K3Item cur = k3_decode<NA, NB>(item, a.lookahead, a.ncomp);
+    uint32_t* slot = a.ring + (cur.c % a.ring_slots) * slot_words;
+    const long long t0 = clock64();
+    if (cur.is_a) {
+      if (cur.c >= a.ring_slots && seen_b != cur.c - a.ring_slots) {
+        wait_counter(done_b + (cur.c - a.ring_slots), unsigned(NB));
+        seen_b = cur.c - a.ring_slots;
+      }
+      const long long t1 = clock64();
       TileArgs ta = a.ta;
-      ta.v_first = a.v_lo + uint32_t(c);
+      ta.v_first = a.v_lo + uint32_t(cur.c);
       ta.n_comp = 1;
       ta.emit = slot;
-      tile_body<15, MODE_EMIT, THREADS>(ta, k, smem4, s_max, gs);
-      release_counter(done_a + c);
+      tile_body<15, MODE_EMIT, THREADS>(ta, cur.k, smem4, s_max, gs);
+      release_counter(done_a + cur.c);
+      if (a.prof && threadIdx.x == 0) {
+        atomicAdd(a.prof + 0, (unsigned long long)(clock64() - t0));
+        atomicAdd(a.prof + 1, (unsigned long long)(t1 - t0));
+        atomicAdd(a.prof + 5, 1ull);
+      }
     } else {
-      wait_counter(done_a + c, unsigned(NA));
+      if (staged != item) {
+        if (seen_a != cur.c) {
+          wait_counter(done_a + cur.c, unsigned(NA));
+          seen_a = cur.c;
+        }
+        stage_chunk<H, THREADS>(slot, cur.k, stg);
+      }
+      const long long t1 = clock64();
+      stage_wait();
+      const long long t2 = clock64();
+      // once this chunk's staging is consumed, start copying the next chunk
+      auto prefetch_next = [&]() {
+        staged = -1;
+        const int64_t nxt = s_item[it ^ 1];
+        if (nxt >= total) return;
+        const K3Item n = k3_decode<NA, NB>(nxt, a.lookahead, a.ncomp);
+        if (n.is_a) return;
+        // never block here: this CTA still holds `item`, which A(n.c) may be
+        // waiting on (ring reuse), so only prefetch a chunk that is ready
+        if (seen_a != n.c) {
+          if (!counter_reached(done_a + n.c, unsigned(NA), &s_flag)) return;
+          seen_a = n.c;
+        }
+        stage_chunk<H, THREADS>(a.ring + (n.c % a.ring_slots) * slot_words, n.k, stg);
+        staged = nxt;
+      };
       PassBArgs pb = a.pb;
       pb.scratch = slot;
       pb.n_comp = 1;
-      pb.out_row0 = c;
-      pb.v_first = a.v_lo + uint32_t(c);
+      pb.out_row0 = cur.c;
+      pb.v_first = a.v_lo + uint32_t(cur.c);
       if constexpr (H <= 5) {
-        passb_regs_chunk<H, MODE, THREADS>(pb, 0, k, s_red);
+        passb_regs_chunk<H, MODE, THREADS>(pb, 0, cur.k, stg, s_red, prefetch_next);
       } else {
-        passb_smem_chunk<H, MODE>(pb, 0, k, reinterpret_cast<int2*>(smem4), s_red);
+        passb_smem_chunk<H, MODE>(pb, 0, cur.k, stg, reinterpret_cast<int2*>(smem4), s_red,
+                                  prefetch_next);
       }
-      release_counter(done_b + c);
+      release_counter(done_b + cur.c);
+      if (a.prof && threadIdx.x == 0) {
+        atomicAdd(a.prof + 2, (unsigned long long)(clock64() - t0));
+        atomicAdd(a.prof + 3, (unsigned long long)(t1 - t0));
+        atomicAdd(a.prof + 4, (unsigned long long)(t2 - t1));
+        atomicAdd(a.prof + 6, 1ull);
+        atomicAdd(a.prof + 7, staged >= 0 ? 1ull : 0ull);
+      }
     }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 }  // namespace sbw

@@ -154,6 +154,27 @@ __device__ __forceinline__ void apply_planes(const uint32_t* __restrict__ planes
   }
 }
 
+// Full recompute (the task moved to a new input range): XOR the planes of
+// every set bit of v.  Unrolled and predicated so all loads are in flight at
+// once -- a data-dependent loop would serialise up to 24 memory latencies.
+__device__ __forceinline__ void planes_full(const uint32_t* __restrict__ planes, int64_t pw,
+                                            uint32_t v, int64_t cw, uint32_t& w0, uint32_t& w1) {
+  uint2 p[24];
+#pragma unroll
+  for (int i = 0; i < 24; ++i) {
+    p[i] = make_uint2(0u, 0u);
+    if ((v >> i) & 1u) p[i] = __ldg(reinterpret_cast<const uint2*>(planes + int64_t(i) * pw + cw));
+  }
+  uint32_t a = 0, b = 0;
+#pragma unroll
+  for (int i = 0; i < 24; ++i) {
+    a ^= p[i].x;
+    b ^= p[i].y;
+  }
+  w0 = a;
+  w1 = b;
+}
+
 // max|W| of a task from its packed max/min trackers (top stage index N)
 template <int N>
 __device__ __forceinline__ int lanes_maxabs(uint32_t mx, uint32_t mn) {
@@ -189,14 +210,13 @@ __device__ __forceinline__ void tile_last_pass(const TileArgs& a, uint32_t (&E)[
 #pragma unroll
     for (int k = 0; k < HALF; ++k) {
       const uint32_t x = E[k], y = E[k + HALF];
-      uint32_t S, D;
-      if constexpr (N == 16) {
-        S = __vadd2(x, y);                       // per-lane mod 2^16
-        D = __vadd2(x, 0x80008000u - y);         // (x - y + 2^15) mod 2^16
-      } else {
-        S = x + y;
-        D = x - y + ((1u << (N - 1)) * 0x00010001u);
-      }
+      // Plain 32-bit adds.  For N < 16 every lane stays in [0, 2^N] (no carry).
+      // For N = 16 a low lane reaches 2^16 only when |W| = 2^16, the largest
+      // value possible: it wraps to 0 (same |W|) and carries +1 into the high
+      // lane, which then reads some |W'| <= 2^16 -- the component max is 2^16
+      // either way, so max|W| stays exact without per-lane modular adds.
+      const uint32_t S = x + y;
+      const uint32_t D = x - y + ((1u << (N - 1)) * 0x00010001u);
       mx = __vimax3_u16x2(mx, S, D);
       mn = __vimin3_u16x2(mn, S, D);
     }
@@ -297,13 +317,13 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
     }
     uint32_t w0 = 0, w1 = 0;
     if (valid) {
-      uint32_t delta = v;
       if (cw == g_cw[r]) {
-        delta = v ^ g_v[r];
         w0 = g_w0[r];
         w1 = g_w1[r];
+        apply_planes(a.planes, a.plane_words, v ^ g_v[r], cw, w0, w1);
+      } else {
+        planes_full(a.planes, a.plane_words, v, cw, w0, w1);
       }
-      apply_planes(a.planes, a.plane_words, delta, cw, w0, w1);
       g_v[r] = v;
       g_w0[r] = w0;
       g_w1[r] = w1;
@@ -314,8 +334,9 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
     const uint32_t n0 = ~w0, n1 = ~w1;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      R[q] = (n0 >> q) & 0x01010101u;
-      R[8 + q] = (n1 >> q) & 0x01010101u;
+      // w >> q as a high multiply (FMA pipe) instead of SHF (ALU pipe)
+      R[q] = (q ? __umulhi(n0, 1u << (32 - q)) : n0) & 0x01010101u;
+      R[8 + q] = (q ? __umulhi(n1, 1u << (32 - q)) : n1) & 0x01010101u;
     }
     // byte stages on register bits (x bits 0,1,2,5), k = 0..3
 #pragma unroll

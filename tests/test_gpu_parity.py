@@ -190,6 +190,21 @@ def test_identity_16_full_range_stress():
     assert np.array_equal(rows.cpu().numpy(), orc.spectrum(s.table, 16, 1, 64))
 
 
+def test_partially_affine_16():
+    """Components that are affine (|W| = 2^16, the packed-lane wrap case) next
+    to random ones in the same box."""
+    rng = np.random.default_rng(11)
+    t = (np.arange(1 << 16, dtype=np.uint32) & 0xFF) | (rng.integers(0, 256, 1 << 16,
+                                                                    dtype=np.uint32) << 8)
+    s = sw.SBox(16, 16, t)
+    for lo, hi in [(1, 300), (250, 262), (65400, 65536)]:
+        mx, _ = sw.component_max_abs_device(s, lo, hi)
+        assert np.array_equal(mx.cpu().numpy(), orc.component_max_abs(s.table, 16, lo, hi))
+    mx, key = sw.component_max_abs_device(s)
+    assert np.all(mx.cpu().numpy()[:255] == 1 << 16)
+    assert sw.transforms.decode_key(key, 16)[:2] == (0, 1)
+
+
 def test_identity_and_constant_24_bit():
     s = sw.SBox(17, 3, np.zeros(1 << 17, dtype=np.uint32))
     mx, key = sw.component_max_abs_device(s)
