@@ -443,3 +443,62 @@ def test_distributed_single_rank_nccl():
     finally:
         dist.destroy_process_group()
     del torch
+
+
+# ---------------------------------------------- CLI + bench harness (GPU) ----
+def _boxfile(tmp_path, name, s):
+    p = tmp_path / name
+    p.write_text(sw.render_sbox(s))
+    return str(p)
+
+
+def test_cli_nl_walsh_verify(tmp_path, capsys):
+    from paper_1912_03732_b200.cli import main
+
+    aes = _boxfile(tmp_path, "aes.sbox", sw.aes_sbox())
+    assert main(["nl", aes]) == 0
+    out = capsys.readouterr().out
+    assert out.startswith("nl = 112") and "argmin v = 1" in out
+    for method in ("fused", "bruteforce", "transposed"):
+        assert main(["nl", aes, "--method", method]) == 0
+        assert capsys.readouterr().out.startswith("nl = 112")
+    r8 = _boxfile(tmp_path, "r8.sbox", sw.generate_sbox(8, 8, 1))
+    assert main(["nl", r8, "--max-mem", str(8 * 256 * 4), "--mode", "stream",
+                 "--workers", "2"]) == 0
+    idf = _boxfile(tmp_path, "id2.sbox", sw.identity_sbox(2))
+    wout = tmp_path / "id2.wspec"
+    assert main(["walsh", idf, "--out", str(wout)]) == 0
+    lines = wout.read_text().splitlines()
+    assert lines[0] == "2 2" and len(lines) == 4
+    for line in lines[1:]:
+        assert sorted(map(abs, map(int, line.split()))) == [0, 0, 0, 4]
+    r6 = _boxfile(tmp_path, "r6.sbox", sw.generate_sbox(6, 5, 3))
+    assert main(["verify", r6, "--max-workers", "4"]) == 0
+    assert capsys.readouterr().out.count("PASS") == 4
+    assert main(["verify", r6, "--max-workers", "2", "--inject-corruption"]) == 5
+    out = capsys.readouterr().out
+    assert "FAIL direct-oracle equivalence" in out and "FAIL parseval" in out
+
+
+def test_cli_bench_csv_and_harness(tmp_path, monkeypatch):
+    import paper_1912_03732_b200.harness as h
+    from paper_1912_03732_b200.cli import main
+
+    path = _boxfile(tmp_path, "r7.sbox", sw.generate_sbox(7, 7, 2))
+    out = tmp_path / "rep.csv"
+    assert main(["bench", path, "--methods", "fused,transposed,parallel", "--workers", "1,3",
+                 "--reps", "2", "--out", str(out)]) == 0
+    rows = sw.read_csv(out.read_text())
+    assert [(r["method"], r["workers"]) for r in rows] == [
+        ("fused", 1), ("parallel", 1), ("parallel", 3), ("transposed", 1)]
+    assert all(r["mean_ms"] > 0 and r["transform_only_mean_ms"] > 0 for r in rows)
+    # verify-before-time: a wrong answer raises instead of being timed
+    real = h._PIPELINES["fused"]
+
+    def wrong(*a, **k):
+        res, spec = real(*a, **k)
+        return sw.NonlinearityResult(res.value + 1, res.argmin_v, res.method), spec
+
+    monkeypatch.setitem(h._PIPELINES, "fused", wrong)
+    with pytest.raises(sw.BenchVerificationError):
+        sw.run_benchmark(sw.generate_sbox(6, 6, 1), ["fused"], repetitions=1)
