@@ -95,6 +95,82 @@ def spectrum_device(s: SBox, v_lo: int = 1, v_hi: int | None = None, layout: str
     return out, mx[:rows]
 
 
+# Materialised spectra above this size stream to the host in chunks.
+STREAM_THRESHOLD_BYTES = 1 << 30
+
+
+def spectrum_to_host(s: SBox, v_lo: int = 1, v_hi: int | None = None, layout: str = "mask",
+                     out: np.ndarray | None = None, chunk_bytes: int = 512 << 20,
+                     device=None) -> tuple[np.ndarray, np.ndarray]:
+    """Materialise W for masks [v_lo, v_hi) into a host array, chunk by chunk.
+
+    Device memory stays at two chunk buffers regardless of the spectrum size
+    (16 GiB at 16x16): chunk i+1 is computed on one stream while chunk i is
+    copied device->host (pinned staging) on the other.  layout "mask" fills
+    out[v - v_lo][u]; layout "x" fills out[u][v - v_lo] (the reference's
+    x-major store, walsh.py:117-131).  Returns (out, max_abs int32 per mask).
+    """
+    torch = _dev.torch_mod()
+    dev = _dev.require_device(device)
+    if v_hi is None:
+        v_hi = 1 << s.m
+    nv, nx = v_hi - v_lo, 1 << s.n
+    if layout not in ("mask", "x"):
+        raise ValueError(f"layout must be 'mask' or 'x', got {layout!r}")
+    shape = (nv, nx) if layout == "mask" else (nx, nv)
+    if out is None:
+        out = np.empty(shape, dtype=np.int32)
+    elif out.shape != shape or out.dtype != np.int32:
+        raise ValueError(f"out must be an int32 array of shape {shape}")
+    maxima = np.empty(nv, dtype=np.int32)
+    rows = max(1, min(nv, chunk_bytes // (nx * 4)))
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    bufs, pins, done = [], [], []
+    for _ in range(2):
+        bshape = (rows, nx) if layout == "mask" else (nx, rows)
+        bufs.append(torch.empty(bshape, dtype=torch.int32, device=dev))
+        pins.append(torch.empty(bshape, dtype=torch.int32, pin_memory=True))
+        done.append(None)
+    mx_dev = torch.empty(nv, dtype=torch.int32, device=dev)
+    lib = _dev.load_library()
+    tab = _dev.device_table(s, dev)
+    lay = _dev.LAYOUT_MASK_MAJOR if layout == "mask" else _dev.LAYOUT_X_MAJOR
+    sbytes = lib.sbw_spectrum_scratch_bytes(s.n, s.m, v_lo, v_lo + rows, lay)
+    scratch = [_scratch(sbytes, dev), _scratch(sbytes, dev)]
+    torch.cuda.current_stream(dev).synchronize()  # table upload visible to both streams
+    pending = []  # (slot, a, b) chunks whose D2H is in flight
+
+    def drain(slot, a, b):
+        done[slot].synchronize()
+        if layout == "mask":
+            out[a - v_lo:b - v_lo] = pins[slot][: b - a].numpy()
+        else:
+            out[:, a - v_lo:b - v_lo] = pins[slot][:, : b - a].numpy()
+
+    for i, a in enumerate(range(v_lo, v_hi, rows)):
+        b = min(v_hi, a + rows)
+        slot = i & 1
+        if len(pending) == 2:  # the slot we are about to reuse
+            drain(*pending.pop(0))
+        st = streams[slot]
+        with torch.cuda.stream(st):
+            ld = nx if layout == "mask" else rows
+            _dev.check(lib.sbw_spectrum(
+                _dev.ptr(tab), _dev.table_bytes(s.m), s.n, s.m, a, b, lay, _dev.ptr(bufs[slot]),
+                ld, _dev.ptr(mx_dev) + 4 * (a - v_lo), _dev.ptr(scratch[slot]), sbytes,
+                st.cuda_stream))
+            pins[slot].copy_(bufs[slot], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            done[slot] = ev
+        pending.append((slot, a, b))
+    for p in pending:
+        drain(*p)
+    torch.cuda.synchronize(dev)
+    maxima[:] = mx_dev.cpu().numpy()
+    return out, maxima
+
+
 def maxabs_to_nl(max_abs, n: int) -> np.ndarray:
     """Device max|W| -> host int64 NL per component (walsh.py:107-114)."""
     torch = _dev.torch_mod()
@@ -219,18 +295,20 @@ def fwht_rowmajor(s: SBox, max_bytes: int | None = None,
     check_budget(memory_estimate(s.n, s.m, mode="retain"), max_bytes)
     t0 = time.perf_counter()
     dev = _dev.require_device()
-    torch = _dev.torch_mod()
     nbytes = ((1 << s.m) - 1) * (1 << s.n) * 4
     with charged(nbytes):
         t1 = time.perf_counter()
-        wt, _ = spectrum_device(s, layout="x", device=dev)
-        rows_t = wt.t().contiguous()
-        del wt
-        _sync(dev)
-        t2 = time.perf_counter()
-        rows = _host_rows(rows_t)
-    del rows_t
-    torch.cuda.empty_cache() if nbytes > (1 << 30) else None
+        if nbytes > STREAM_THRESHOLD_BYTES:
+            rows, _ = spectrum_to_host(s, layout="mask", device=dev)
+            t2 = time.perf_counter()
+        else:
+            wt, _ = spectrum_device(s, layout="x", device=dev)
+            rows_t = wt.t().contiguous()
+            del wt
+            _sync(dev)
+            t2 = time.perf_counter()
+            rows = _host_rows(rows_t)
+            del rows_t
     if timings is not None:
         timings["build_s"] = t1 - t0
         timings["transform_s"] = t2 - t1
@@ -246,10 +324,14 @@ def fwht_transposed(s: SBox, max_bytes: int | None = None,
     nbytes = ((1 << s.m) - 1) * (1 << s.n) * 4
     with charged(nbytes):
         t1 = time.perf_counter()
-        spec, _ = spectrum_device(s, layout="mask", device=dev)
-        _sync(dev)
-        t2 = time.perf_counter()
-        rows = _host_rows(spec)
+        if nbytes > STREAM_THRESHOLD_BYTES:
+            rows, _ = spectrum_to_host(s, layout="mask", device=dev)
+            t2 = time.perf_counter()
+        else:
+            spec, _ = spectrum_device(s, layout="mask", device=dev)
+            _sync(dev)
+            t2 = time.perf_counter()
+            rows = _host_rows(spec)
     if timings is not None:
         timings["build_s"] = t1 - t0
         timings["transform_s"] = t2 - t1
@@ -272,11 +354,16 @@ def fwht_fused(s: SBox, mode: str = "retain", max_bytes: int | None = None,
         nbytes = ((1 << s.m) - 1) * (1 << s.n) * 4
         with charged(nbytes):
             t1 = time.perf_counter()
-            spec, mx = spectrum_device(s, layout="mask", device=dev)
-            _sync(dev)
-            t2 = time.perf_counter()
-            rows = _host_rows(spec)
-        del spec
+            if nbytes > STREAM_THRESHOLD_BYTES:
+                rows, mx_host = spectrum_to_host(s, layout="mask", device=dev)
+                mx = _dev.torch_mod().from_numpy(mx_host).to(dev)
+                t2 = time.perf_counter()
+            else:
+                spec, mx = spectrum_device(s, layout="mask", device=dev)
+                _sync(dev)
+                t2 = time.perf_counter()
+                rows = _host_rows(spec)
+                del spec
         values = maxabs_to_nl(mx, s.n)
         spectrum = WalshSpectrum(s.n, s.m, rows)
     else:

@@ -502,3 +502,31 @@ def test_cli_bench_csv_and_harness(tmp_path, monkeypatch):
     monkeypatch.setitem(h._PIPELINES, "fused", wrong)
     with pytest.raises(sw.BenchVerificationError):
         sw.run_benchmark(sw.generate_sbox(6, 6, 1), ["fused"], repetitions=1)
+
+
+def test_streamed_spectrum_chunks_match(golden):
+    """Chunked, double-buffered export (bounded device memory) equals the
+    one-shot spectrum in both layouts, including ragged last chunks."""
+    s = box("12x12")
+    g = golden["configs"]["12x12"]
+    rows, mx = sw.spectrum_to_host(s, chunk_bytes=3 * 4096 * 4 + 7)   # 3 rows per chunk
+    assert sha(rows) == g["sha_mask_major"]
+    xm, mx2 = sw.spectrum_to_host(s, layout="x", chunk_bytes=1000 * 4096 * 4)
+    assert sha(xm) == g["sha_x_major"]
+    assert np.array_equal(mx, mx2)
+    want, _ = sw.spectrum_device(s, 100, 1100)
+    part, _ = sw.spectrum_to_host(s, 100, 1100, chunk_bytes=64 * 4096 * 4)
+    assert np.array_equal(part, want.cpu().numpy())
+
+
+@pytest.mark.slow
+def test_16x16_retain_streams_to_host(golden, golden_arrays):
+    """fwht_fused(retain) at 16x16: 16 GiB spectrum exported in chunks."""
+    s = box("16x16")
+    spec, cm = sw.fwht_fused(s, mode="retain")
+    assert np.array_equal(cm.values, golden_arrays["maxima_16x16"])
+    assert spec.rows.shape == (65535, 65536)
+    assert spec.rows[0, :8].tolist() == [0, -368, 440, 104, 52, 348, 260, -196]
+    assert spec.rows[-1, :8].tolist() == [0, -296, -56, -104, 272, -128, 288, -40]
+    r = sw.nonlinearity_from_spectrum(spec)
+    assert (r.value, r.argmin_v) == (31942, 44828)
