@@ -262,7 +262,25 @@ __device__ __forceinline__ K3Item k3_decode(int64_t item, int64_t D, int64_t C) 
   return r;
 }
 
-constexpr size_t kK3Smem = size_t(kTileWords) * sizeof(uint32_t) + (size_t(64) << 10);
+constexpr int kStageWords = 24 * 1024;     // 96 KiB staging: a pass-B chunk or A-tile planes
+constexpr int kStagedPlanesMax = kStageWords / 2048;  // 12 plane segments of 8 KiB
+constexpr size_t kK3Smem = size_t(kTileWords) * sizeof(uint32_t) + size_t(kStageWords) * 4;
+
+// Issue (not wait for) the copies of the plane segments an A tile needs: the
+// first `count` set bits of v, each 2048 words starting at `base_word`.
+template <int THREADS>
+__device__ __forceinline__ void stage_planes(const uint32_t* planes, int64_t pw, uint32_t v,
+                                             int64_t base_word, int count, uint32_t* stg) {
+  int j = 0;
+  for (uint32_t d = v; d && j < count; d &= d - 1, ++j) {
+    const uint32_t* g = planes + int64_t(__ffs(d) - 1) * pw + base_word;
+    for (int p = threadIdx.x; p < 512; p += THREADS) {
+      const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(stg + j * 2048 + 4 * p));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g + 4 * p) : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
 
 template <int H, int MODE>
 __global__ void __launch_bounds__(512, 1) k3_persistent(K3Args a) {
@@ -270,7 +288,7 @@ __global__ void __launch_bounds__(512, 1) k3_persistent(K3Args a) {
   using S = ChunkShape<H, THREADS>;
   constexpr int64_t NA = int64_t(1) << (H - 1);  // pass-A tiles per component
   constexpr int64_t NB = S::PER_COMP;            // pass-B chunks per component
-  extern __shared__ uint4 smem4[];               // [128 KiB tile / int32 rows][64 KiB staging]
+  extern __shared__ uint4 smem4[];               // [128 KiB tile / int32 rows][96 KiB staging]
   uint32_t* stg = reinterpret_cast<uint32_t*>(smem4) + kTileWords;
   __shared__ int s_max[2];
   __shared__ int s_red[THREADS / 32];
@@ -283,7 +301,7 @@ __global__ void __launch_bounds__(512, 1) k3_persistent(K3Args a) {
   const int64_t slot_words = int64_t(1) << (a.pb.n - 1);
   GenState<1024 / THREADS> gs;
   gs.reset();
-  int64_t staged = -1;  // queue item whose chunk is in (or in flight to) `stg`
+  int64_t staged = -1;  // queue item whose chunk / planes are in (or in flight to) `stg`
   // Counters only grow, so a condition this CTA has seen satisfied stays
   // satisfied: skip the acquire round trip (and its barrier) when possible.
   int64_t seen_a = -1;  // largest c with done_a[c] == NA observed
@@ -298,6 +316,29 @@ __global__ void __launch_bounds__(512, 1) k3_persistent(K3Args a) {
     if (threadIdx.x == 0) s_item[it ^ 1] = atomicAdd(head, 1u);
     const K3Item cur = k3_decode<NA, NB>(item, a.lookahead, a.ncomp);
     uint32_t* slot = a.ring + (cur.c % a.ring_slots) * slot_words;
+    // Start copying the next item's inputs into `stg` once this item no
+    // longer reads it: the plane segments of an A tile (always ready) or a
+    // pass-B chunk whose tiles are all published (never blocks: this CTA
+    // still holds `item`, which A tiles may be waiting on via ring reuse).
+    auto prefetch_next = [&]() {
+      staged = -1;
+      const int64_t nxt = s_item[it ^ 1];
+      if (nxt >= total) return;
+      const K3Item n = k3_decode<NA, NB>(nxt, a.lookahead, a.ncomp);
+      if (n.is_a) {
+        const uint32_t vn = a.v_lo + uint32_t(n.c);
+        stage_planes<THREADS>(a.ta.planes, a.ta.plane_words, vn, n.k * 2048,
+                              min(__popc(vn), kStagedPlanesMax), stg);
+        staged = nxt;
+        return;
+      }
+      if (seen_a != n.c) {
+        if (!counter_reached(done_a + n.c, unsigned(NA), &s_flag)) return;
+        seen_a = n.c;
+      }
+      stage_chunk<H, THREADS>(a.ring + (n.c % a.ring_slots) * slot_words, n.k, stg);
+      staged = nxt;
+    };
     const long long t0 = clock64();
     if (cur.is_a) {
       if (cur.c >= a.ring_slots && seen_b != cur.c - a.ring_slots) {
@@ -309,7 +350,14 @@ __global__ void __launch_bounds__(512, 1) k3_persistent(K3Args a) {
       ta.v_first = a.v_lo + uint32_t(cur.c);
       ta.n_comp = 1;
       ta.emit = slot;
-      tile_body<15, MODE_EMIT, THREADS>(ta, cur.k, smem4, s_max, gs);
+      StagedPlanes sp;
+      if (staged == item) {
+        stage_wait();
+        sp.words = stg;
+        sp.count = min(__popc(ta.v_first), kStagedPlanesMax);
+        sp.base_word = cur.k * 2048;
+      }
+      tile_body<15, MODE_EMIT, THREADS>(ta, cur.k, smem4, s_max, gs, sp, prefetch_next);
       release_counter(done_a + cur.c);
       if (a.prof && threadIdx.x == 0) {
         atomicAdd(a.prof + 0, (unsigned long long)(clock64() - t0));
@@ -327,22 +375,6 @@ __global__ void __launch_bounds__(512, 1) k3_persistent(K3Args a) {
       const long long t1 = clock64();
       stage_wait();
       const long long t2 = clock64();
-      // once this chunk's staging is consumed, start copying the next chunk
-      auto prefetch_next = [&]() {
-        staged = -1;
-        const int64_t nxt = s_item[it ^ 1];
-        if (nxt >= total) return;
-        const K3Item n = k3_decode<NA, NB>(nxt, a.lookahead, a.ncomp);
-        if (n.is_a) return;
-        // never block here: this CTA still holds `item`, which A(n.c) may be
-        // waiting on (ring reuse), so only prefetch a chunk that is ready
-        if (seen_a != n.c) {
-          if (!counter_reached(done_a + n.c, unsigned(NA), &s_flag)) return;
-          seen_a = n.c;
-        }
-        stage_chunk<H, THREADS>(a.ring + (n.c % a.ring_slots) * slot_words, n.k, stg);
-        staged = nxt;
-      };
       PassBArgs pb = a.pb;
       pb.scratch = slot;
       pb.n_comp = 1;

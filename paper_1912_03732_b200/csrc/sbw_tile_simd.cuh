@@ -275,9 +275,47 @@ struct GenState {
 // One tile t (see the file comment): three passes over the shared-memory
 // tile, result published per component (NL / SPEC) or emitted (EMIT).  Must be
 // called by all THREADS threads of the CTA.
-template <int N, int MODE, int THREADS>
+// Plane segments of one tile staged in shared memory by the caller (the
+// multi-pass kernel prefetches them during the previous work item): the j-th
+// set bit of v has its 2048-word segment at words[j * 2048 ...], j < count.
+struct StagedPlanes {
+  const uint32_t* words = nullptr;
+  int count = 0;
+  int64_t base_word = 0;  // first plane word of the tile
+};
+
+// Component bits of one task from staged plane segments (shared memory),
+// falling back to global memory for set bits beyond the staged count.
+__device__ __forceinline__ void planes_staged(const StagedPlanes& sp, const uint32_t* planes,
+                                              int64_t pw, uint32_t v, int64_t cw, uint32_t& w0,
+                                              uint32_t& w1) {
+  const int lw = int(cw - sp.base_word);
+  uint32_t a = 0, b = 0;
+  int j = 0;
+  for (uint32_t d = v; d; d &= d - 1, ++j) {
+    uint2 p;
+    if (j < sp.count) {
+      p = *reinterpret_cast<const uint2*>(sp.words + j * 2048 + lw);
+    } else {
+      const int i = __ffs(d) - 1;
+      p = __ldg(reinterpret_cast<const uint2*>(planes + int64_t(i) * pw + cw));
+    }
+    a ^= p.x;
+    b ^= p.y;
+  }
+  w0 = a;
+  w1 = b;
+}
+
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+template <int N, int MODE, int THREADS, typename Hook = NoHook>
 __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* smem4, int* s_max,
-                                          GenState<1024 / THREADS>& gs) {
+                                          GenState<1024 / THREADS>& gs,
+                                          const StagedPlanes& sp = StagedPlanes(),
+                                          Hook after_pass1 = Hook()) {
   constexpr int ROUNDS = 1024 / THREADS;         // pass-1 tasks per thread
   static_assert(N >= 7 && N <= 16, "tile kernel covers n = 7..16");
   static_assert(MODE != MODE_EMIT || N == 15, "EMIT works on 2^15 blocks");
@@ -292,7 +330,6 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
   uint32_t* g_w0 = gs.w0;
   uint32_t* g_w1 = gs.w1;
   int64_t* g_cw = gs.cw;
-  if (tid < C) s_max[tid] = 0;
 
   // ---------------- pass 1: generation + x bits 0..5 ---------------------
 #pragma unroll
@@ -322,7 +359,10 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
         w1 = g_w1[r];
         apply_planes(a.planes, a.plane_words, v ^ g_v[r], cw, w0, w1);
       } else {
-        planes_full(a.planes, a.plane_words, v, cw, w0, w1);
+        if (sp.words)
+          planes_staged(sp, a.planes, a.plane_words, v, cw, w0, w1);
+        else
+          planes_full(a.planes, a.plane_words, v, cw, w0, w1);
       }
       g_v[r] = v;
       g_w0[r] = w0;
@@ -368,6 +408,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
       dst[c4 ^ (task & 7)] = make_uint4(H[4 * c4], H[4 * c4 + 1], H[4 * c4 + 2], H[4 * c4 + 3]);
   }
   __syncthreads();
+  after_pass1();
 
   // ---------------- pass 2: x bits 6 .. 6+B2-1 ---------------------------
   {
@@ -420,16 +461,22 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
     __syncthreads();
   }
 
-  if constexpr (MODE != MODE_EMIT) {
-    if (tid < C) {
-      const int64_t vv = t * C + tid;
-      if (vv >= a.v_lo && vv < a.v_hi) {
-        const int mx = s_max[tid];
-        a.max_abs[vv - a.v_lo] = mx;
-        if (a.key) atomicMax(a.key, nl_key(mx, uint32_t(vv)));
-      }
+}
+
+// Publish tile t's per-component maxima and clear its slots.  Called right
+// after tile_body (whose last barrier orders every atomicMax before this);
+// the caller alternates two s_max buffers so no extra barrier is needed.
+template <int N>
+__device__ __forceinline__ void tile_publish(const TileArgs& a, int64_t t, int* s_max) {
+  constexpr int C = 1 << (16 - N);
+  if (threadIdx.x < C) {
+    const int64_t vv = t * C + threadIdx.x;
+    if (vv >= a.v_lo && vv < a.v_hi) {
+      const int mx = s_max[threadIdx.x];
+      a.max_abs[vv - a.v_lo] = mx;
+      if (a.key) atomicMax(a.key, nl_key(mx, uint32_t(vv)));
     }
-    __syncthreads();
+    s_max[threadIdx.x] = 0;
   }
 }
 
@@ -437,12 +484,18 @@ template <int N, int MODE, int THREADS = kTileThreads>
 __global__ void __launch_bounds__(THREADS, 1) k_tile_simd(TileArgs a) {
   constexpr int C = 1 << (16 - N);
   extern __shared__ uint4 smem4[];
-  __shared__ int s_max[C];
+  __shared__ int s_max[2][C];  // per-component max, double-buffered by tile parity
   const int64_t t_lo = a.t_begin + (a.t_count * blockIdx.x) / gridDim.x;
   const int64_t t_hi = a.t_begin + (a.t_count * (blockIdx.x + 1)) / gridDim.x;
+  if (threadIdx.x < C) s_max[0][threadIdx.x] = s_max[1][threadIdx.x] = 0;
+  __syncthreads();
   GenState<1024 / THREADS> gs;
   gs.reset();
-  for (int64_t t = t_lo; t < t_hi; ++t) tile_body<N, MODE, THREADS>(a, t, smem4, s_max, gs);
+  int par = 0;
+  for (int64_t t = t_lo; t < t_hi; ++t, par ^= 1) {
+    tile_body<N, MODE, THREADS>(a, t, smem4, s_max[par], gs);
+    if constexpr (MODE != MODE_EMIT) tile_publish<N>(a, t, s_max[par]);
+  }
 }
 
 }  // namespace sbw
