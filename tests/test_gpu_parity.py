@@ -530,3 +530,21 @@ def test_16x16_retain_streams_to_host(golden, golden_arrays):
     assert spec.rows[-1, :8].tolist() == [0, -296, -56, -104, 272, -128, 288, -40]
     r = sw.nonlinearity_from_spectrum(spec)
     assert (r.value, r.argmin_v) == (31942, 44828)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,want", [("20x20", (520495, 334146, 7586)),
+                                       ("24x16", (8374359, 27804, 28498))])
+def test_full_large_config_nl(name, want):
+    """Full 20x20 / 24x16 NL on one GPU.  The reference needs hours here, so
+    the result is checked where it matters: the argmin component and random
+    masks against the oracle, plus the smallest-v tie-break on the maxima."""
+    s = box(name)
+    mx, key = sw.component_max_abs_device(s)
+    res = sw.transforms.decode_key(key, s.n)
+    assert res == want
+    full = mx.cpu().numpy()
+    assert int(full.max()) == res[2] and int(np.argmax(full)) + 1 == res[1]
+    checks = [res[1]] + [int(v) for v in np.random.default_rng(9).integers(1, 1 << s.m, 2)]
+    for v in checks:
+        assert full[v - 1] == orc.component_max_abs(s.table, s.n, v, v + 1)[0], v
