@@ -118,13 +118,14 @@ int launch_k3(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32
   static const bool prof = getenv("SBW_K3_PROF") != nullptr;
   unsigned long long* dprof = nullptr;
   if (prof) {
-    SBW_CUDA_CHECK(cudaMallocAsync(&dprof, 8 * sizeof(unsigned long long), st));
-    SBW_CUDA_CHECK(cudaMemsetAsync(dprof, 0, 8 * sizeof(unsigned long long), st));
+    SBW_CUDA_CHECK(cudaMallocAsync(&dprof, 16 * sizeof(unsigned long long), st));
+    SBW_CUDA_CHECK(cudaMemsetAsync(dprof, 0, 16 * sizeof(unsigned long long), st));
     a.prof = dprof;
+    a.ta.phase_prof = dprof + 8;
   }
   const int rc = out ? dispatch_h<MODE_SPEC>(n - 15, a, st) : dispatch_h<MODE_NL>(n - 15, a, st);
   if (prof) {
-    unsigned long long h[8];
+    unsigned long long h[16];
     SBW_CUDA_CHECK(cudaMemcpyAsync(h, dprof, sizeof(h), cudaMemcpyDeviceToHost, st));
     SBW_CUDA_CHECK(cudaStreamSynchronize(st));
     cudaFreeAsync(dprof, st);
@@ -134,6 +135,9 @@ int launch_k3(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32
             n, (long long)ncomp, R, (long long)a.lookahead, h[5], h[5] ? double(h[0]) / h[5] : 0.0,
             h[5] ? double(h[1]) / h[5] : 0.0, h[6], h[6] ? double(h[2]) / h[6] : 0.0,
             h[6] ? double(h[3]) / h[6] : 0.0, h[6] ? double(h[4]) / h[6] : 0.0, h[7]);
+    if (h[5])
+      fprintf(stderr, "[k3 prof]   A tile phases: pass1 %.0f  pass2 %.0f  pass3+emit %.0f cyc\n",
+              double(h[8]) / h[5], double(h[9]) / h[5], double(h[10]) / h[5]);
   }
   return rc;
 }

@@ -55,6 +55,7 @@ struct TileArgs {
   int64_t n_comp;
   int n_full;              // n of the S-box (EMIT: 17..24)
   uint32_t* emit;          // u16 pairs, [comp][2^n_full]
+  unsigned long long* phase_prof;  // optional (debug): cycles in pass 1 / 2 / 3 (thread 0)
 };
 
 // packed stage helpers -------------------------------------------------------
@@ -326,6 +327,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
   constexpr int XMASK = (1 << N) - 1;
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
   const int tid = threadIdx.x;
+  const long long ph0 = clock64();
   uint32_t* g_v = gs.v;
   uint32_t* g_w0 = gs.w0;
   uint32_t* g_w1 = gs.w1;
@@ -408,6 +410,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
       dst[c4 ^ (task & 7)] = make_uint4(H[4 * c4], H[4 * c4 + 1], H[4 * c4 + 2], H[4 * c4 + 3]);
   }
   __syncthreads();
+  const long long ph1 = clock64();
   after_pass1();
 
   // ---------------- pass 2: x bits 6 .. 6+B2-1 ---------------------------
@@ -415,7 +418,28 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
     constexpr int NI = 1 << B2;
     constexpr int NT = kTileWords >> B2;
     constexpr bool LAST = (B3 == 0);
-    for (int task = tid; task < NT; task += THREADS) {
+    // two tasks per thread in flight when there are enough of them: all loads
+    // of both issue before either's arithmetic (hides the LDS latency with
+    // few warps, e.g. the 512-thread multi-pass kernel)
+    constexpr int IL = (!LAST && NT >= 2 * THREADS) ? 2 : 1;
+    for (int task0 = tid; IL == 2 && task0 < NT; task0 += 2 * THREADS) {
+      uint32_t E[2][NI];
+      int P[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int task = task0 + q * THREADS;
+        P[q] = phys_word(((task >> 5) << (5 + B2)) | (task & 31));
+#pragma unroll
+        for (int i = 0; i < NI; ++i) E[q][i] = sm[(P[q] ^ ((i & 7) << 2)) + (i << 5)];
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) stages16<NI, 0, B2, 6>(E[q]);
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int i = 0; i < NI; ++i) sm[(P[q] ^ ((i & 7) << 2)) + (i << 5)] = E[q][i];
+    }
+    for (int task = tid; IL == 1 && task < NT; task += THREADS) {
       const int lo = task & 31, hi = task >> 5;
       const int wb = (hi << (5 + B2)) | lo;
       // phys(wb | i << 5) = (P ^ ((i & 7) << 2)) + (i << 5), P = phys(wb):
@@ -443,24 +467,37 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
     }
   }
   __syncthreads();
+  const long long ph2 = clock64();
 
   // ---------------- pass 3: x bits 11 .. N-1 ------------------------------
   if constexpr (B3 > 0) {
     constexpr int NI = 1 << B3;
     constexpr int NT = kTileWords >> B3;
-    for (int task = tid; task < NT; task += THREADS) {
-      const int lo = task & 1023, hi = task >> 10;
-      const int wb = (hi << (10 + B3)) | lo;
-      // the swizzle depends on word bits 5..7 only, so phys(wb | i << 10) = phys(wb) + (i << 10)
-      const uint32_t* base = sm + phys_word(wb);
-      uint32_t E[NI];
+    // the swizzle depends on word bits 5..7 only, so phys(wb | i << 10) = phys(wb) + (i << 10)
+    constexpr int IL = (NT >= 2 * THREADS && NI <= 16) ? 2 : 1;
+    for (int task0 = tid; task0 < NT; task0 += IL * THREADS) {
+      uint32_t E[IL][NI];
+      int wb[IL];
 #pragma unroll
-      for (int i = 0; i < NI; ++i) E[i] = base[i << 10];
-      tile_last_pass<N, MODE, NI, 10, 11>(a, E, wb, t, s_max);
+      for (int q = 0; q < IL; ++q) {
+        const int task = task0 + q * THREADS;
+        wb[q] = ((task >> 10) << (10 + B3)) | (task & 1023);
+        const uint32_t* base = sm + phys_word(wb[q]);
+#pragma unroll
+        for (int i = 0; i < NI; ++i) E[q][i] = base[i << 10];
+      }
+#pragma unroll
+      for (int q = 0; q < IL; ++q) tile_last_pass<N, MODE, NI, 10, 11>(a, E[q], wb[q], t, s_max);
     }
     __syncthreads();
   }
 
+  if (a.phase_prof && threadIdx.x == 0) {
+    const long long ph3 = clock64();
+    atomicAdd(a.phase_prof + 0, (unsigned long long)(ph1 - ph0));
+    atomicAdd(a.phase_prof + 1, (unsigned long long)(ph2 - ph1));
+    atomicAdd(a.phase_prof + 2, (unsigned long long)(ph3 - ph2));
+  }
 }
 
 // Publish tile t's per-component maxima and clear its slots.  Called right
