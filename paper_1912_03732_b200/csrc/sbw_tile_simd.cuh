@@ -33,6 +33,11 @@
 
 #include "sbw_fused.cuh"
 
+// Per-phase cycle stamps of tile_body (debug builds: make EXTRA=-DSBW_PHASE_PROF=1).
+#ifndef SBW_PHASE_PROF
+#define SBW_PHASE_PROF 0
+#endif
+
 #ifndef SBW_PASS2_FP16
 #define SBW_PASS2_FP16 0  // exact but measured slower (2.70 vs 2.18 ms at 16x16): HFMA2 conversions cost more than the ALU they free
 #endif
@@ -327,7 +332,9 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
   constexpr int XMASK = (1 << N) - 1;
   uint32_t* sm = reinterpret_cast<uint32_t*>(smem4);
   const int tid = threadIdx.x;
+#if SBW_PHASE_PROF
   const long long ph0 = clock64();
+#endif
   uint32_t* g_v = gs.v;
   uint32_t* g_w0 = gs.w0;
   uint32_t* g_w1 = gs.w1;
@@ -410,7 +417,9 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
       dst[c4 ^ (task & 7)] = make_uint4(H[4 * c4], H[4 * c4 + 1], H[4 * c4 + 2], H[4 * c4 + 3]);
   }
   __syncthreads();
+#if SBW_PHASE_PROF
   const long long ph1 = clock64();
+#endif
   after_pass1();
 
   // ---------------- pass 2: x bits 6 .. 6+B2-1 ---------------------------
@@ -421,7 +430,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
     // two tasks per thread in flight when there are enough of them: all loads
     // of both issue before either's arithmetic (hides the LDS latency with
     // few warps, e.g. the 512-thread multi-pass kernel)
-    constexpr int IL = (!LAST && NT >= 2 * THREADS) ? 2 : 1;
+    constexpr int IL = (!LAST && THREADS <= 512 && NT >= 2 * THREADS) ? 2 : 1;
     for (int task0 = tid; IL == 2 && task0 < NT; task0 += 2 * THREADS) {
       uint32_t E[2][NI];
       int P[2];
@@ -467,37 +476,35 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
     }
   }
   __syncthreads();
+#if SBW_PHASE_PROF
   const long long ph2 = clock64();
+#endif
 
   // ---------------- pass 3: x bits 11 .. N-1 ------------------------------
   if constexpr (B3 > 0) {
     constexpr int NI = 1 << B3;
     constexpr int NT = kTileWords >> B3;
-    // the swizzle depends on word bits 5..7 only, so phys(wb | i << 10) = phys(wb) + (i << 10)
-    constexpr int IL = (NT >= 2 * THREADS && NI <= 16) ? 2 : 1;
-    for (int task0 = tid; task0 < NT; task0 += IL * THREADS) {
-      uint32_t E[IL][NI];
-      int wb[IL];
+    for (int task = tid; task < NT; task += THREADS) {
+      const int lo = task & 1023, hi = task >> 10;
+      const int wb = (hi << (10 + B3)) | lo;
+      // the swizzle depends on word bits 5..7 only, so phys(wb | i << 10) = phys(wb) + (i << 10)
+      const uint32_t* base = sm + phys_word(wb);
+      uint32_t E[NI];
 #pragma unroll
-      for (int q = 0; q < IL; ++q) {
-        const int task = task0 + q * THREADS;
-        wb[q] = ((task >> 10) << (10 + B3)) | (task & 1023);
-        const uint32_t* base = sm + phys_word(wb[q]);
-#pragma unroll
-        for (int i = 0; i < NI; ++i) E[q][i] = base[i << 10];
-      }
-#pragma unroll
-      for (int q = 0; q < IL; ++q) tile_last_pass<N, MODE, NI, 10, 11>(a, E[q], wb[q], t, s_max);
+      for (int i = 0; i < NI; ++i) E[i] = base[i << 10];
+      tile_last_pass<N, MODE, NI, 10, 11>(a, E, wb, t, s_max);
     }
     __syncthreads();
   }
 
+#if SBW_PHASE_PROF
   if (a.phase_prof && threadIdx.x == 0) {
     const long long ph3 = clock64();
     atomicAdd(a.phase_prof + 0, (unsigned long long)(ph1 - ph0));
     atomicAdd(a.phase_prof + 1, (unsigned long long)(ph2 - ph1));
     atomicAdd(a.phase_prof + 2, (unsigned long long)(ph3 - ph2));
   }
+#endif
 }
 
 // Publish tile t's per-component maxima and clear its slots.  Called right
