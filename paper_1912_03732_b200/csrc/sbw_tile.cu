@@ -1,5 +1,8 @@
 // Dispatch of the fused on-chip kernels (n = 1..16) and of pass A of the
 // multi-pass path; bit-plane construction.  See sbw_tile_simd.cuh.
+#include <cstdio>
+#include <cstdlib>
+
 #include "sbw_launch.h"
 #include "sbw_tile_simd.cuh"
 
@@ -27,7 +30,10 @@ __global__ void __launch_bounds__(256) k_build_planes(const TT* __restrict__ tab
 
 template <int N, int MODE>
 int run_tile(const TileArgs& a, int64_t ntiles, cudaStream_t st) {
-  auto kern = k_tile_simd<N, MODE>;
+  // materialising (SPEC) tiles are store-bound and need more registers for
+  // the int32 epilogue: 512 threads; fused NL tiles: 1024 threads
+  constexpr int THREADS = MODE == MODE_SPEC ? 512 : kTileThreads;
+  auto kern = k_tile_simd<N, MODE, THREADS>;
   DeviceProps dp;
   if (int rc = device_props(&dp)) return rc;
   // per (instantiation, device); the attribute call is idempotent, so a race is benign
@@ -39,7 +45,7 @@ int run_tile(const TileArgs& a, int64_t ntiles, cudaStream_t st) {
   }
   const int grid = int(ntiles < dp.sm_count ? ntiles : dp.sm_count);
   if (grid <= 0) return SBW_OK;
-  kern<<<grid, kTileThreads, kTileSmem, st>>>(a);
+  kern<<<grid, THREADS, kTileSmem, st>>>(a);
   SBW_LAUNCH_CHECK("k_tile_simd");
   return SBW_OK;
 }
@@ -146,8 +152,29 @@ int launch_fused_onchip(const void* table, int tbytes, int n, int m, uint32_t v_
   a.key = key;
   a.out = out;
   a.ld = ld;
-  return out ? dispatch_tile<MODE_SPEC>(n, a, a.t_count, st)
-             : dispatch_tile<MODE_NL>(n, a, a.t_count, st);
+#if SBW_PHASE_PROF
+  // debug builds: per-phase cycle accounting of the on-chip tiles (SBW_K3_PROF=1)
+  unsigned long long* dprof = nullptr;
+  if (getenv("SBW_K3_PROF")) {
+    SBW_CUDA_CHECK(cudaMallocAsync(&dprof, 4 * sizeof(unsigned long long), st));
+    SBW_CUDA_CHECK(cudaMemsetAsync(dprof, 0, 4 * sizeof(unsigned long long), st));
+    a.phase_prof = dprof;
+  }
+#endif
+  const int rc = out ? dispatch_tile<MODE_SPEC>(n, a, a.t_count, st)
+                     : dispatch_tile<MODE_NL>(n, a, a.t_count, st);
+#if SBW_PHASE_PROF
+  if (dprof) {
+    unsigned long long h[4];
+    SBW_CUDA_CHECK(cudaMemcpyAsync(h, dprof, sizeof(h), cudaMemcpyDeviceToHost, st));
+    SBW_CUDA_CHECK(cudaStreamSynchronize(st));
+    cudaFreeAsync(dprof, st);
+    const double nt = double(a.t_count);
+    fprintf(stderr, "[tile prof] n=%d tiles=%lld pass1 %.0f pass2 %.0f pass3 %.0f cyc/tile\n", n,
+            (long long)a.t_count, h[0] / nt, h[1] / nt, h[2] / nt);
+  }
+#endif
+  return rc;
 }
 
 }  // namespace sbw
