@@ -25,6 +25,11 @@ int launch_k3(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32
               size_t scratch_bytes, cudaStream_t st);
 
 
+// Pass-A tiles (generation + 15 stages, biased u16 out) for components
+// [v_first, v_first + n_comp), used by the batched multi-pass path.
+int launch_emit_tiles(const uint32_t* planes, int n, int m, uint32_t v_first, int64_t n_comp,
+                      uint32_t* emit, cudaStream_t st);
+
 // Total workspace of sbw_nl (planes + multi-pass scratch).
 inline size_t nl_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi) {
   return n >= 17 ? k3_scratch_bytes(n, m, v_lo, v_hi) : planes_bytes(n, m);

@@ -1,72 +1,147 @@
-// Multi-pass driver for n = 17..24: bit planes, then one persistent kernel
-// that interleaves pass A (generation + 15 on-chip stages, biased u16 to an
-// L2-resident ring of scratch slots) and pass B (stages 15..n-1 + fused
-// max|W|) through an ordered work queue.  See sbw_passb.cuh.
+// Multi-pass driver for n = 17..24: bit planes, then per batch of components
+// one pass-A launch (generation + 15 on-chip stages, biased u16 out) and one
+// pass-B launch (stages 15..n-1 + fused max|W|).  Batch b+1's pass A runs on
+// one stream beside batch b's pass B on another (double-buffered scratch).
+// Measured: ~1 GiB batches beat L2-sized ones and a persistent
+// work-queue kernel, because launches are few and both passes run at full
+// occupancy; the scratch traffic (4 B / element) streams through HBM.
 #include <cstdio>
 #include <cstdlib>
 
 #include "sbw_launch.h"
 #include "sbw_passb.cuh"
 
+#include <mutex>
+
 namespace sbw {
 
 namespace {
 
-// Ring of component scratch slots kept within this budget so that pass B
-// reads what pass A just wrote from the 126 MB L2.
-constexpr size_t kRingBudget = size_t(64) << 20;
-
-// Lookahead D (components) so that >= ~3 waves of queue items separate A(c)
-// from B(c): B(c) then rarely waits for its tiles.
-int64_t lookahead(int n, int64_t ncomp) {
-  const int64_t na = int64_t(1) << (n - 16);
-  const int64_t nb = (n - 15) <= 5 ? (int64_t(1) << 14) / 512 : (int64_t(1) << 14) / 32;
-  int64_t d = (3 * 148 + na + nb - 1) / (na + nb);
-  if (d < 1) d = 1;
-  if (d > ncomp) d = ncomp;
-  return d;
-}
-
-int ring_slots(int n, int64_t ncomp) {
-  const size_t per = size_t(2) << n;  // u16 bytes per component
-  int64_t r = int64_t(kRingBudget / per);
-  const int64_t need = lookahead(n, ncomp) + 2;  // R > D, plus one slot of slack (R = D + 1 measured slower)
-  if (r < need) r = need;
-  return int(r);
-}
-
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// ---- batched two-kernel path for n = 17..20 ---------------------------------
+// Two scratch buffers of `bb` components (~1 GiB each): pass A of batch b+1
+// runs on one stream beside pass B of batch b on another.
+constexpr size_t kBatchBytes = size_t(1) << 30;  // per buffer (measured: bigger batches win)
+
+int64_t batch_components(int n, int64_t total) {
+  static const char* env = getenv("SBW_K3_BATCH");  // tuning aid: components per batch
+  int64_t bb = env ? atoll(env) : int64_t(kBatchBytes / (size_t(2) << n));
+  if (bb < 1) bb = 1;
+  return bb < total ? bb : total;
+}
+
+struct K3Streams {
+  cudaStream_t a = nullptr, b = nullptr;
+  cudaEvent_t fork = nullptr, done_a[2] = {nullptr, nullptr}, done_b[2] = {nullptr, nullptr};
+};
+K3Streams g_k3[64];
+std::mutex g_k3_mu;
+std::mutex g_k3_launch_mu[64];  // one enqueue at a time per device (shared events)
+
+int k3_streams(int dev, K3Streams** out) {
+  std::lock_guard<std::mutex> lk(g_k3_mu);
+  K3Streams& s = g_k3[dev & 63];
+  if (!s.a) {
+    SBW_CUDA_CHECK(cudaStreamCreateWithFlags(&s.a, cudaStreamNonBlocking));
+    SBW_CUDA_CHECK(cudaStreamCreateWithFlags(&s.b, cudaStreamNonBlocking));
+    SBW_CUDA_CHECK(cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      SBW_CUDA_CHECK(cudaEventCreateWithFlags(&s.done_a[i], cudaEventDisableTiming));
+      SBW_CUDA_CHECK(cudaEventCreateWithFlags(&s.done_b[i], cudaEventDisableTiming));
+    }
+  }
+  *out = &s;
+  return SBW_OK;
+}
+
 template <int H, int MODE>
-int run_persistent(const K3Args& a, cudaStream_t st) {
+int run_passb_regs(const PassBArgs& a, cudaStream_t st) {
   DeviceProps dp;
   if (int rc = device_props(&dp)) return rc;
-  auto kern = k3_persistent<H, MODE>;
-  constexpr size_t kSmem = kK3Smem;  // 128 KiB tile / pass-B rows + 64 KiB staging
+  const int64_t ctas = a.n_comp * ((int64_t(1) << 14) / kPassBThreads);
+  const int64_t cap = int64_t(dp.sm_count) * 8;
+  k_passb_regs<H, MODE><<<int(ctas < cap ? ctas : cap), kPassBThreads, 0, st>>>(a);
+  SBW_LAUNCH_CHECK("k_passb_regs");
+  return SBW_OK;
+}
+
+template <int H, int MODE>
+int run_passb_staged(const PassBArgs& a, cudaStream_t st) {
+  DeviceProps dp;
+  if (int rc = device_props(&dp)) return rc;
+  auto kern = k_passb_staged<H, MODE>;
   static unsigned long long attr_done = 0;
   if (!(attr_done >> (dp.device & 63) & 1ull)) {
     SBW_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(kSmem)));
+                                        int(kPassBSmem)));
     attr_done |= 1ull << (dp.device & 63);
   }
-  kern<<<dp.sm_count, 512, kSmem, st>>>(a);
-  SBW_LAUNCH_CHECK("k3_persistent");
+  const int64_t items = a.n_comp * ChunkShape<H, 512>::PER_COMP;
+  const int grid = int(items < dp.sm_count ? items : dp.sm_count);
+  kern<<<grid, 512, kPassBSmem, st>>>(a);
+  SBW_LAUNCH_CHECK("k_passb_staged");
   return SBW_OK;
 }
 
 template <int MODE>
-int dispatch_h(int h, const K3Args& a, cudaStream_t st) {
+int dispatch_passb_regs(int h, const PassBArgs& a, cudaStream_t st) {
   switch (h) {
-    case 2: return run_persistent<2, MODE>(a, st);
-    case 3: return run_persistent<3, MODE>(a, st);
-    case 4: return run_persistent<4, MODE>(a, st);
-    case 5: return run_persistent<5, MODE>(a, st);
-    case 6: return run_persistent<6, MODE>(a, st);
-    case 7: return run_persistent<7, MODE>(a, st);
-    case 8: return run_persistent<8, MODE>(a, st);
-    case 9: return run_persistent<9, MODE>(a, st);
-    default: return set_error(SBW_EINVAL, "multi-pass path needs n in 17..24");
+    case 2: return run_passb_regs<2, MODE>(a, st);
+    case 3: return run_passb_regs<3, MODE>(a, st);
+    case 4: return run_passb_regs<4, MODE>(a, st);
+    case 5: return run_passb_regs<5, MODE>(a, st);
+    case 6: return run_passb_staged<6, MODE>(a, st);
+    case 7: return run_passb_staged<7, MODE>(a, st);
+    case 8: return run_passb_staged<8, MODE>(a, st);
+    case 9: return run_passb_staged<9, MODE>(a, st);
+    default: return set_error(SBW_EINVAL, "batched path needs n in 17..24");
   }
+}
+
+int launch_k3_batched(const uint32_t* planes, int n, int m, uint32_t v_lo, uint32_t v_hi,
+                      int32_t* max_abs, unsigned long long* key, int32_t* out, int64_t ld,
+                      uint32_t* bufs, cudaStream_t st) {
+  const int64_t total = int64_t(v_hi) - int64_t(v_lo);
+  const int64_t bb = batch_components(n, total);
+  uint32_t* emit[2] = {bufs, bufs + size_t(bb) * (size_t(1) << (n - 1))};
+  DeviceProps dp;
+  if (int rc = device_props(&dp)) return rc;
+  K3Streams* ks = nullptr;
+  if (int rc = k3_streams(dp.device, &ks)) return rc;
+  std::lock_guard<std::mutex> launch_lock(g_k3_launch_mu[dp.device & 63]);
+  // fork: both aux streams start after everything already queued on `st`
+  SBW_CUDA_CHECK(cudaEventRecord(ks->fork, st));
+  SBW_CUDA_CHECK(cudaStreamWaitEvent(ks->a, ks->fork, 0));
+  SBW_CUDA_CHECK(cudaStreamWaitEvent(ks->b, ks->fork, 0));
+  int64_t nb = 0;
+  for (int64_t c0 = 0; c0 < total; c0 += bb, ++nb) {
+    const int64_t nc = (total - c0) < bb ? (total - c0) : bb;
+    const uint32_t vf = v_lo + uint32_t(c0);
+    const int buf = int(nb & 1);
+    if (nb >= 2) SBW_CUDA_CHECK(cudaStreamWaitEvent(ks->a, ks->done_b[buf], 0));  // buffer free
+    if (int rc = launch_emit_tiles(planes, n, m, vf, nc, emit[buf], ks->a)) return rc;
+    SBW_CUDA_CHECK(cudaEventRecord(ks->done_a[buf], ks->a));
+    SBW_CUDA_CHECK(cudaStreamWaitEvent(ks->b, ks->done_a[buf], 0));
+    PassBArgs a{};
+    a.scratch = emit[buf];
+    a.n = n;
+    a.n_comp = nc;
+    a.out_row0 = c0;
+    a.v_first = vf;
+    a.max_abs = max_abs;
+    a.key = key;
+    a.out = out;
+    a.ld = ld;
+    const int rc = out ? dispatch_passb_regs<MODE_SPEC>(n - 15, a, ks->b)
+                       : dispatch_passb_regs<MODE_NL>(n - 15, a, ks->b);
+    if (rc) return rc;
+    SBW_CUDA_CHECK(cudaEventRecord(ks->done_b[buf], ks->b));
+  }
+  // join: `st` continues after the last pass B (which follows every pass A)
+  SBW_CUDA_CHECK(cudaEventRecord(ks->fork, ks->b));
+  SBW_CUDA_CHECK(cudaStreamWaitEvent(st, ks->fork, 0));
+  return SBW_OK;
 }
 
 }  // namespace
@@ -74,9 +149,9 @@ int dispatch_h(int h, const K3Args& a, cudaStream_t st) {
 size_t k3_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi) {
   if (n < 17) return 0;
   const int64_t ncomp = int64_t(v_hi) - int64_t(v_lo);
-  const size_t ring = size_t(ring_slots(n, ncomp)) * (size_t(2) << n);
-  const size_t counters = sizeof(unsigned) * (1 + 2 * size_t(ncomp > 0 ? ncomp : 0));
-  return planes_bytes(n, m) + align256(ring) + align256(counters);
+  // bit planes + two batch buffers of biased u16 partial transforms
+  return planes_bytes(n, m) +
+         align256(2 * size_t(batch_components(n, ncomp > 0 ? ncomp : 1)) * (size_t(2) << n));
 }
 
 int launch_k3(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32_t v_hi,
@@ -84,62 +159,16 @@ int launch_k3(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32
               size_t scratch_bytes, cudaStream_t st) {
   if (n < 17 || n > 24) return set_error(SBW_EINVAL, "multi-pass path needs n in 17..24");
   if (v_hi <= v_lo) return SBW_OK;
-  const int64_t ncomp = int64_t(v_hi) - int64_t(v_lo);
   const size_t need = k3_scratch_bytes(n, m, v_lo, v_hi);
   if (scratch == nullptr || scratch_bytes < need)
     return set_error(SBW_EINVAL, "n=%d needs a scratch workspace of %zu bytes, got %zu", n, need,
                      scratch_bytes);
-  const int R = ring_slots(n, ncomp);
   char* base = static_cast<char*>(scratch);
   uint32_t* planes = reinterpret_cast<uint32_t*>(base);
-  uint32_t* ring = reinterpret_cast<uint32_t*>(base + planes_bytes(n, m));
-  unsigned* counters = reinterpret_cast<unsigned*>(base + planes_bytes(n, m) +
-                                                   align256(size_t(R) * (size_t(2) << n)));
+  uint32_t* bufs = reinterpret_cast<uint32_t*>(base + planes_bytes(n, m));
   if (int rc = build_planes(table, tbytes, n, m, planes, st)) return rc;
-  SBW_CUDA_CHECK(cudaMemsetAsync(max_abs, 0, sizeof(int32_t) * size_t(ncomp), st));
-  SBW_CUDA_CHECK(cudaMemsetAsync(counters, 0, sizeof(unsigned) * (1 + 2 * size_t(ncomp)), st));
-  K3Args a{};
-  a.ta.planes = planes;
-  a.ta.plane_words = (int64_t(1) << n) >> 5;
-  a.ta.m = m;
-  a.ta.n_full = n;
-  a.pb.n = n;
-  a.pb.max_abs = max_abs;
-  a.pb.key = key;
-  a.pb.out = out;
-  a.pb.ld = ld;
-  a.v_lo = v_lo;
-  a.ncomp = ncomp;
-  a.ring = ring;
-  a.ring_slots = R;
-  a.lookahead = lookahead(n, ncomp);
-  a.counters = counters;
-  // SBW_K3_PROF=1 (debugging aid): per-item cycle accounting printed to stderr
-  static const bool prof = getenv("SBW_K3_PROF") != nullptr;
-  unsigned long long* dprof = nullptr;
-  if (prof) {
-    SBW_CUDA_CHECK(cudaMallocAsync(&dprof, 16 * sizeof(unsigned long long), st));
-    SBW_CUDA_CHECK(cudaMemsetAsync(dprof, 0, 16 * sizeof(unsigned long long), st));
-    a.prof = dprof;
-    a.ta.phase_prof = dprof + 8;
-  }
-  const int rc = out ? dispatch_h<MODE_SPEC>(n - 15, a, st) : dispatch_h<MODE_NL>(n - 15, a, st);
-  if (prof) {
-    unsigned long long h[16];
-    SBW_CUDA_CHECK(cudaMemcpyAsync(h, dprof, sizeof(h), cudaMemcpyDeviceToHost, st));
-    SBW_CUDA_CHECK(cudaStreamSynchronize(st));
-    cudaFreeAsync(dprof, st);
-    fprintf(stderr,
-            "[k3 prof] n=%d comps=%lld R=%d D=%lld | A items %llu avg %.0f cyc (wait %.0f) | "
-            "B items %llu avg %.0f cyc (counter wait %.0f, stage wait %.0f, prefetched %llu)\n",
-            n, (long long)ncomp, R, (long long)a.lookahead, h[5], h[5] ? double(h[0]) / h[5] : 0.0,
-            h[5] ? double(h[1]) / h[5] : 0.0, h[6], h[6] ? double(h[2]) / h[6] : 0.0,
-            h[6] ? double(h[3]) / h[6] : 0.0, h[6] ? double(h[4]) / h[6] : 0.0, h[7]);
-    if (h[5])
-      fprintf(stderr, "[k3 prof]   A tile phases: pass1 %.0f  pass2 %.0f  pass3+emit %.0f cyc\n",
-              double(h[8]) / h[5], double(h[9]) / h[5], double(h[10]) / h[5]);
-  }
-  return rc;
+  SBW_CUDA_CHECK(cudaMemsetAsync(max_abs, 0, sizeof(int32_t) * (size_t(v_hi) - v_lo), st));
+  return launch_k3_batched(planes, n, m, v_lo, v_hi, max_abs, key, out, ld, bufs, st);
 }
 
 }  // namespace sbw

@@ -177,4 +177,19 @@ int launch_fused_onchip(const void* table, int tbytes, int n, int m, uint32_t v_
   return rc;
 }
 
+int launch_emit_tiles(const uint32_t* planes, int n, int m, uint32_t v_first, int64_t n_comp,
+                      uint32_t* emit, cudaStream_t st) {
+  TileArgs a{};
+  a.planes = planes;
+  a.plane_words = (int64_t(1) << n) >> 5;
+  a.m = m;
+  a.v_first = v_first;
+  a.n_comp = n_comp;
+  a.n_full = n;
+  a.emit = emit;
+  a.t_begin = 0;
+  a.t_count = n_comp << (n - 16);  // (block pair, component) tiles, component fastest
+  return run_tile<15, MODE_EMIT>(a, a.t_count, st);
+}
+
 }  // namespace sbw

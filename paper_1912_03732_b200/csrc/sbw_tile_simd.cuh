@@ -281,38 +281,6 @@ struct GenState {
 // One tile t (see the file comment): three passes over the shared-memory
 // tile, result published per component (NL / SPEC) or emitted (EMIT).  Must be
 // called by all THREADS threads of the CTA.
-// Plane segments of one tile staged in shared memory by the caller (the
-// multi-pass kernel prefetches them during the previous work item): the j-th
-// set bit of v has its 2048-word segment at words[j * 2048 ...], j < count.
-struct StagedPlanes {
-  const uint32_t* words = nullptr;
-  int count = 0;
-  int64_t base_word = 0;  // first plane word of the tile
-};
-
-// Component bits of one task from staged plane segments (shared memory),
-// falling back to global memory for set bits beyond the staged count.
-__device__ __forceinline__ void planes_staged(const StagedPlanes& sp, const uint32_t* planes,
-                                              int64_t pw, uint32_t v, int64_t cw, uint32_t& w0,
-                                              uint32_t& w1) {
-  const int lw = int(cw - sp.base_word);
-  uint32_t a = 0, b = 0;
-  int j = 0;
-  for (uint32_t d = v; d; d &= d - 1, ++j) {
-    uint2 p;
-    if (j < sp.count) {
-      p = *reinterpret_cast<const uint2*>(sp.words + j * 2048 + lw);
-    } else {
-      const int i = __ffs(d) - 1;
-      p = __ldg(reinterpret_cast<const uint2*>(planes + int64_t(i) * pw + cw));
-    }
-    a ^= p.x;
-    b ^= p.y;
-  }
-  w0 = a;
-  w1 = b;
-}
-
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
@@ -320,7 +288,6 @@ struct NoHook {
 template <int N, int MODE, int THREADS, typename Hook = NoHook>
 __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* smem4, int* s_max,
                                           GenState<1024 / THREADS>& gs,
-                                          const StagedPlanes& sp = StagedPlanes(),
                                           Hook after_pass2 = Hook()) {
   constexpr int ROUNDS = 1024 / THREADS;         // pass-1 tasks per thread
   static_assert(N >= 7 && N <= 16, "tile kernel covers n = 7..16");
@@ -368,10 +335,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
         w1 = g_w1[r];
         apply_planes(a.planes, a.plane_words, v ^ g_v[r], cw, w0, w1);
       } else {
-        if (sp.words)
-          planes_staged(sp, a.planes, a.plane_words, v, cw, w0, w1);
-        else
-          planes_full(a.planes, a.plane_words, v, cw, w0, w1);
+        planes_full(a.planes, a.plane_words, v, cw, w0, w1);
       }
       g_v[r] = v;
       g_w0[r] = w0;
@@ -478,9 +442,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
 #if SBW_PHASE_PROF
   const long long ph2 = clock64();
 #endif
-  // the caller's hook (e.g. staging the next work item) overlaps pass 3,
-  // which is lighter on shared memory than pass 2
-  after_pass2();
+  after_pass2();  // caller hook between passes 2 and 3 (unused by the kernels here)
 
   // ---------------- pass 3: x bits 11 .. N-1 ------------------------------
   if constexpr (B3 > 0) {
