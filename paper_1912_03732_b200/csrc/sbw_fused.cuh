@@ -25,13 +25,11 @@ enum FusedMode { MODE_NL = 0, MODE_SPEC = 1, MODE_EMIT = 2 };
 struct FusedArgs {
   const void* table;
   uint32_t v_first;       // mask of item 0
-  int nbl;                // log2(blocks per component); 0 unless MODE_EMIT
   int64_t n_items;        // (component, block) items
   int32_t* max_abs;       // [item] for NL / SPEC
   unsigned long long* key;
   int32_t* out;           // SPEC: out[item * ld + x]
   int64_t ld;
-  uint32_t* emit;         // EMIT: int16 pairs, component stride 2^(N + nbl) elements
 };
 
 // n = 1..6: one thread owns one whole component in registers.

@@ -99,11 +99,4 @@ __device__ __forceinline__ int warp_max(int x) {
   return x;
 }
 
-// int16 pair packing for the shared-memory exchange buffer.
-__device__ __forceinline__ uint32_t pack2(int lo, int hi) {
-  return (uint32_t(lo) & 0xFFFFu) | (uint32_t(hi) << 16);
-}
-__device__ __forceinline__ int lo16(uint32_t w) { return int(int16_t(w & 0xFFFFu)); }
-__device__ __forceinline__ int hi16(uint32_t w) { return int(w) >> 16; }
-
 }  // namespace sbw

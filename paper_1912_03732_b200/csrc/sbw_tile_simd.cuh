@@ -38,9 +38,7 @@
 #define SBW_PHASE_PROF 0
 #endif
 
-#ifndef SBW_PASS2_FP16
-#define SBW_PASS2_FP16 0  // exact but measured slower (2.70 vs 2.18 ms at 16x16): HFMA2 conversions cost more than the ALU they free
-#endif
+
 
 namespace sbw {
 
@@ -94,56 +92,6 @@ __device__ __forceinline__ void stages16(uint32_t (&R)[L]) {
   }
 }
 
-
-// ---- exact fp16x2 butterflies on the FMA pipe ------------------------------
-// For 0 <= s <= 2048 the fp16 bit pattern of s * 2^-24 is the integer s itself
-// (subnormals, then exponent -14 with a 2^-24 ulp, then 2^-13), and f16x2
-// arithmetic keeps subnormals.  So a biased u16 lane s after k stages is also
-// the fp16 number s * 2^-24, and signed values |v| <= 2048 (v = 2s - 2^k) are
-// exact too.  Stages run as add/sub.f16x2 with no bias constant; the integer
-// form is restored with one fma.  All results are exact, no rounding occurs.
-__device__ __forceinline__ uint32_t h2_add(uint32_t a, uint32_t b) {
-  uint32_t r;
-  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
-  return r;
-}
-__device__ __forceinline__ uint32_t h2_sub(uint32_t a, uint32_t b) {
-  uint32_t r;
-  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
-  return r;
-}
-__device__ __forceinline__ uint32_t h2_fma(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t r;
-  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-  return r;
-}
-constexpr uint32_t kH2Two = 0x40004000u;   // (2.0, 2.0)
-constexpr uint32_t kH2Half = 0x38003800u;  // (0.5, 0.5)
-// (x * 2^-24, x * 2^-24) for 0 <= x <= 2048, as f16x2 bits
-__host__ __device__ constexpr uint32_t h2_int(uint32_t x) { return x | (x << 16); }
-__host__ __device__ constexpr uint32_t h2_neg_int(uint32_t x) { return (x | 0x8000u) | ((x | 0x8000u) << 16); }
-
-// biased s (k stages) -> signed v = 2s - 2^k, as fp16 lanes
-template <int K>
-__device__ __forceinline__ uint32_t to_signed_h2(uint32_t s) { return h2_fma(s, kH2Two, h2_neg_int(1u << K)); }
-// signed v (k stages) -> biased s = (v + 2^k) / 2, as integer u16 lanes
-template <int K>
-__device__ __forceinline__ uint32_t to_biased_h2(uint32_t v) { return h2_fma(v, kH2Half, h2_int(1u << (K - 1))); }
-
-template <int L, int SB, int SE>
-__device__ __forceinline__ void stages_h2(uint32_t (&R)[L]) {
-#pragma unroll
-  for (int sb = SB; sb < SE; ++sb) {
-#pragma unroll
-    for (int i = 0; i < L; ++i) {
-      if ((i & (1 << sb)) == 0) {
-        const uint32_t x = R[i], y = R[i | (1 << sb)];
-        R[i] = h2_add(x, y);
-        R[i | (1 << sb)] = h2_sub(x, y);
-      }
-    }
-  }
-}
 
 __device__ __forceinline__ int phys_word(int w) { return w ^ (((w >> 5) & 7) << 2); }
 
@@ -281,14 +229,9 @@ struct GenState {
 // One tile t (see the file comment): three passes over the shared-memory
 // tile, result published per component (NL / SPEC) or emitted (EMIT).  Must be
 // called by all THREADS threads of the CTA.
-struct NoHook {
-  __device__ __forceinline__ void operator()() const {}
-};
-
-template <int N, int MODE, int THREADS, typename Hook = NoHook>
+template <int N, int MODE, int THREADS>
 __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* smem4, int* s_max,
-                                          GenState<1024 / THREADS>& gs,
-                                          Hook after_pass2 = Hook()) {
+                                          GenState<1024 / THREADS>& gs) {
   constexpr int ROUNDS = 1024 / THREADS;         // pass-1 tasks per thread
   static_assert(N >= 7 && N <= 16, "tile kernel covers n = 7..16");
   static_assert(MODE != MODE_EMIT || N == 15, "EMIT works on 2^15 blocks");
@@ -421,16 +364,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
 #pragma unroll
       for (int i = 0; i < NI; ++i) E[i] = sm[(P ^ ((i & 7) << 2)) + (i << 5)];
       if constexpr (!LAST) {
-#if SBW_PASS2_FP16
-        // stages k = 6..10 as exact fp16x2 add/sub on the FMA pipe
-#pragma unroll
-        for (int i = 0; i < NI; ++i) E[i] = to_signed_h2<6>(E[i]);
-        stages_h2<NI, 0, B2>(E);
-#pragma unroll
-        for (int i = 0; i < NI; ++i) E[i] = to_biased_h2<6 + B2>(E[i]);
-#else
         stages16<NI, 0, B2, 6>(E);
-#endif
 #pragma unroll
         for (int i = 0; i < NI; ++i) sm[(P ^ ((i & 7) << 2)) + (i << 5)] = E[i];
       } else {
@@ -442,7 +376,6 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int64_t t, uint4* s
 #if SBW_PHASE_PROF
   const long long ph2 = clock64();
 #endif
-  after_pass2();  // caller hook between passes 2 and 3 (unused by the kernels here)
 
   // ---------------- pass 3: x bits 11 .. N-1 ------------------------------
   if constexpr (B3 > 0) {
