@@ -18,6 +18,12 @@ int launch_fused_onchip(const void* table, int tbytes, int n, int m, uint32_t v_
                         int32_t* max_abs, unsigned long long* key, int32_t* out, int64_t ld,
                         void* scratch, cudaStream_t st);
 
+// Tensor-core hybrid for n = 16 NL (planes already built): int8 MMA for x bits
+// 0..7, packed integer stages for bits 8..15 (sbw_tc.cu).
+int launch_tc16_nl(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
+                   unsigned long long* key, cudaStream_t st);
+bool tc_path_enabled();
+
 // Multi-pass path (n >= 17): planes, then pass A (emit) + pass B per L2-sized batch.
 size_t k3_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi);
 int launch_k3(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32_t v_hi,

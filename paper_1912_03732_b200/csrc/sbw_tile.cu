@@ -139,6 +139,8 @@ int launch_fused_onchip(const void* table, int tbytes, int n, int m, uint32_t v_
   }
   uint32_t* planes = static_cast<uint32_t*>(scratch);
   if (int rc = build_planes(table, tbytes, n, m, planes, st)) return rc;
+  if (n == 16 && out == nullptr && tc_path_enabled())
+    return launch_tc16_nl(planes, v_lo, v_hi, max_abs, key, st);
   TileArgs a{};
   a.planes = planes;
   a.plane_words = (int64_t(1) << n) >> 5;
