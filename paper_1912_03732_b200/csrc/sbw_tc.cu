@@ -47,7 +47,6 @@ namespace sbw {
 namespace {
 
 constexpr int kMathWarps = 8;
-constexpr int kTcThreads = kMathWarps * 32;
 constexpr int kAOff = 0;                       // A = -H_256, 256 x 256 s8
 constexpr int kBOff = kAOff + 256 * 256;       // 2 x (256 x 256) generated B operands
 constexpr int kBBytes = 256 * 256;
@@ -135,33 +134,52 @@ __device__ __forceinline__ void publish(const uint32_t* wmax, uint32_t v, uint32
   if (key) atomicMax(key, nl_key(m, v));
 }
 
-__device__ __forceinline__ void issue_mma(uint32_t tmem, const uint8_t* smem, int buf, uint64_t* bar) {
-  const uint32_t a0 = tc::smem_u32(smem + kAOff);
-  const uint32_t b0 = tc::smem_u32(smem + kBOff + buf * kBBytes);
+// MMA chain of one mask (2 M-halves x 8 K blocks), issued by a converged warp.
+// Descriptors differ only in the start-address field (bits 0..13, smem < 256 KiB,
+// no carry), so they are one base plus a compile-time offset each.
+__device__ __forceinline__ void issue_mma_warp(uint32_t tmem, const uint8_t* smem, int buf, uint64_t* bar) {
+  const uint64_t da0 = tc::sdesc(tc::smem_u32(smem + kAOff), 128, 2048);
+  const uint64_t db0 = tc::sdesc(tc::smem_u32(smem + kBOff + buf * kBBytes), 128, 2048);
 #pragma unroll
   for (int h = 0; h < 2; ++h)
 #pragma unroll
     for (int kb = 0; kb < 8; ++kb)
-      tc::mma_i8(tmem + h * 256, tc::sdesc(a0 + h * 32768 + kb * 256, 128, 2048),
-                 tc::sdesc(b0 + kb * 256, 128, 2048), kIdesc, kb > 0 ? 1u : 0u);
-  tc::mma_commit(bar);
+      tc::mma_i8_elect(tmem + h * 256, da0 + uint64_t((h * 32768 + kb * 256) >> 4), db0 + uint64_t(kb * 16),
+                       kIdesc, kb > 0 ? 1u : 0u);
+  tc::mma_commit_elect(bar);
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1)
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+
+// Warp roles.  tcgen05.mma blocks its issuing thread while the tensor core's
+// queue is full (~one MMA per 128 cycles here), so the 16 MMAs of a mask
+// would stall a transform warp for ~2K cycles; they get their own warp.
+// setmaxnreg moves the registers: the issuer warpgroup keeps 32 per thread,
+// the two transform warpgroups get 232 (3 warps per SM sub-partition:
+// 32 + 232 + 232 = 496 of the 512 registers per lane of a sub-partition;
+// an exact 512 fit hung setmaxnreg.inc on B200).
+constexpr int kIssuerRegs = 32;
+constexpr int kMathRegs = 232;
+constexpr int kAllThreads = 128 + kMathWarps * 32;  // warpgroup 0: issuer (+3 idle warps)
+
+__global__ void __launch_bounds__(kAllThreads, 1)
     k_tc16_nl(const uint32_t* __restrict__ planes, uint32_t v_lo, uint32_t v_hi,
               int32_t* __restrict__ max_abs, unsigned long long* key) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar_full;
+  // full: MMA(i) done.  tmem_empty: all transform threads read D(i).
+  // bfull[b]: all transform threads generated the B operand in buffer b.
+  __shared__ uint64_t bar_full, bar_tmem_empty, bar_bfull[2], bar_done;
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(16) uint32_t s_wmax[4][kMathWarps];  // per-warp max|W|, slot = mask index & 3
-  __shared__ unsigned s_read;                  // warps done reading TMEM, cumulative
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t total = int64_t(v_hi) - v_lo;
   const int64_t q_lo = v_lo + total * blockIdx.x / gridDim.x;
   const int n_my = int(v_lo + total * (blockIdx.x + 1) / gridDim.x - q_lo);
 
   // A = -H_256 with the K permutation of store_row
-  for (int e = tid; e < 256 * 16; e += kTcThreads) {
+  for (int e = tid; e < 256 * 16; e += kAllThreads) {
     const int u = e >> 4, pc = e & 15;
     uint32_t wv[4];
 #pragma unroll
@@ -178,12 +196,45 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0) tc::tmem_alloc(&tmem_slot, 512);
   if (tid == 0) {
     tc::mbar_init(&bar_full, 1);
-    s_read = 0;
+    tc::mbar_init(&bar_tmem_empty, kMathWarps * 32);
+    tc::mbar_init(&bar_bfull[0], kMathWarps * 32);
+    tc::mbar_init(&bar_bfull[1], kMathWarps * 32);
+    tc::mbar_init(&bar_done, kMathWarps * 32);
   }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_slot;
 
-  {
-    // ---------------- math warps ----------------
-    const int c = tid;  // generation row
+  if (warp < 4) {
+    // ---------------- issuer warpgroup ----------------
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kIssuerRegs));
+    if (warp == 0) {
+      for (int i = 0; i < n_my; ++i) {
+        tc::mbar_wait(&bar_bfull[i & 1], uint32_t((i >> 1) & 1));
+        if (i > 0) tc::mbar_wait(&bar_tmem_empty, uint32_t((i - 1) & 1));
+        tc::fence_after();
+        issue_mma_warp(tmem, smem, i & 1, &bar_full);
+        // bfull for mask i (i >= 2) is produced after each thread stored its
+        // max of mask i - 2
+        if (i >= 2 && lane == 0)
+          publish(s_wmax[(i - 2) & 3], mask_at(q_lo + i - 2, v_lo, v_hi), v_lo, max_abs, key);
+      }
+      // every transform thread has read D(last) and stored its last max
+      tc::mbar_wait(&bar_done, 0u);
+      tc::fence_after();
+      if (lane == 0)
+        for (int i = n_my - 2 < 0 ? 0 : n_my - 2; i < n_my; ++i)
+          publish(s_wmax[i & 3], mask_at(q_lo + i, v_lo, v_hi), v_lo, max_abs, key);
+      __syncwarp();
+      tc::tmem_dealloc(tmem, 512);
+    }
+  } else {
+    // ---------------- transform warps ----------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kMathRegs));
+    const int mt = tid - 128, mw = mt >> 5;  // transform thread / warp index
+    const int c = mt;                        // generation row
     uint32_t g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t vcur = 0;
     for (int k = 0; k < 2 && k < n_my; ++k) {
@@ -191,16 +242,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       xor_planes(planes, vcur ^ vn, g, c);
       vcur = vn;
       store_row(g, smem + kBOff + k * kBBytes, c);
+      tc::fence_proxy_async();
+      mbar_arrive(&bar_bfull[k]);
     }
-    tc::fence_proxy_async();
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    const uint32_t tmem = tmem_slot;
-    if (tid == 0 && n_my > 0) issue_mma(tmem, smem, 0, &bar_full);
-    // this thread's TMEM lane: u = 128 * (warp >> 2) + 32 * (warp & 3) + lane
-    const uint32_t tbase = tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(warp >> 2) * 256;
-    const uint32_t corr0 = (tid == 0) ? 0x8000u : 0u;  // row u = 0 offset, see above
+    // this thread's TMEM lane: u = 128 * (mw >> 2) + 32 * (mw & 3) + lane
+    // (warp w may only touch lanes 32 * (w % 4) .. +31; here w % 4 == mw % 4)
+    const uint32_t tbase = tmem + (uint32_t((mw & 3) * 32) << 16) + uint32_t(mw >> 2) * 256;
+    const uint32_t corr0 = (mt == 0) ? 0x8000u : 0u;  // row u = 0 offset, see above
     for (int i = 0; i < n_my; ++i) {
       // prefetch the first plane of the mask two steps ahead
       const bool gen = i + 2 < n_my;
@@ -236,20 +284,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
       tc::fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();
-        if ((atomicAdd(&s_read, 1u) & (kMathWarps - 1)) == kMathWarps - 1) {
-          // last reader of D(i): TMEM is free, B(i+1) was generated and the
-          // per-warp maxima of mask i-1 were stored by every warp
-          __threadfence_block();
-          if (i + 1 < n_my) {
-            tc::fence_after();
-            issue_mma(tmem, smem, (i + 1) & 1, &bar_full);
-          }
-          if (i > 0) publish(s_wmax[(i - 1) & 3], mask_at(q_lo + i - 1, v_lo, v_hi), v_lo, max_abs, key);
-        }
-      }
+      mbar_arrive(&bar_tmem_empty);
       // c bits 1..6 (stages 9..14)
 #pragma unroll
       for (int q = 0; q < 4; ++q) stages_sub<5, 9>(R, 32 * q);
@@ -266,20 +301,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         mn = __vimin3_u16x2(mn, S, D);
       }
       const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<16>(mx, mn)));
-      if (lane == 0) s_wmax[i & 3][warp] = m;
+      if (lane == 0) s_wmax[i & 3][mw] = m;
       if (gen) {
         xor_plane(g, pa, pb);
         xor_planes(planes, d, g, c);  // rare: more than one changed bit
         vcur = vn;
         store_row(g, smem + kBOff + (i & 1) * kBBytes, c);
         tc::fence_proxy_async();
+        mbar_arrive(&bar_bfull[i & 1]);
       }
     }
     tc::fence_before();
-    __syncthreads();
-    if (tid == 0 && n_my > 0)
-      publish(s_wmax[(n_my - 1) & 3], mask_at(q_lo + n_my - 1, v_lo, v_hi), v_lo, max_abs, key);
-    if (warp == 0) tc::tmem_dealloc(tmem, 512);
+    mbar_arrive(&bar_done);
   }
 }
 
@@ -306,7 +339,7 @@ int launch_tc16_nl(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t
   }
   const int64_t count = int64_t(v_hi) - v_lo;
   const int grid = int(count < dp.sm_count ? count : dp.sm_count);
-  k_tc16_nl<<<grid, kTcThreads, kTcSmem, st>>>(planes, v_lo, v_hi, max_abs, key);
+  k_tc16_nl<<<grid, kAllThreads, kTcSmem, st>>>(planes, v_lo, v_hi, max_abs, key);
   SBW_LAUNCH_CHECK("k_tc16_nl");
   return SBW_OK;
 }

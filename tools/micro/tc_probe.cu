@@ -160,6 +160,62 @@ __global__ void __launch_bounds__(128) k_mma_i8(const int8_t* A, const uint8_t* 
   if (warp == 0) tmem_dealloc(tm, 256);
 }
 
+// MMA chain time while other warps stream STS.128 (MODE 1) / LDS.128 (MODE 2) / nothing (0)
+template <int MODE>
+__global__ void __launch_bounds__(256) k_mma_contention(int reps, unsigned long long* cycles, uint32_t* sink) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* sA = sm;
+  uint8_t* sB = sm + 128 * 256;
+  uint4* sX = reinterpret_cast<uint4*>(sm + 96 * 1024);  // 64 KiB scratch
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  __shared__ volatile int done;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 96 * 1024 / 16; i += 256) reinterpret_cast<uint4*>(sm)[i] = make_uint4(i, 1, 2, 3);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 0) tmem_alloc(&slot, 256);
+  if (tid == 0) { mbar_init(&bar, 1); done = 0; }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = slot;
+  const uint32_t idesc = idesc_i8(128, 256, 1, 0);
+  if (warp == 0) {
+    if (tid == 0) {
+      const unsigned long long t0 = clock64();
+      for (int r = 0; r < reps; ++r)
+#pragma unroll
+        for (int kb = 0; kb < 8; ++kb)
+          mma_i8(tm, sdesc(smem_u32(sA) + kb * 256, 128, 2048), sdesc(smem_u32(sB) + kb * 256, 128, 2048), idesc,
+                 (r | kb) ? 1u : 0u);
+      const unsigned long long t1 = clock64();
+      mma_commit(&bar);
+      mbar_wait(&bar, 0);
+      cycles[blockIdx.x] = clock64() - t0;
+      cycles[512 + blockIdx.x] = t1 - t0;
+      done = 1;
+    }
+    __syncwarp();
+  } else {
+    uint32_t acc = 0;
+    int it = 0;
+    while (!done) {
+      for (int k = 0; k < 64; ++k) {
+        const int idx = ((it * 64 + k) * 224 + (tid - 32)) & 4095;
+        if (MODE == 1) sX[idx] = make_uint4(k, it, tid, acc);
+        if (MODE == 2) { const uint4 v = sX[idx]; acc ^= v.x ^ v.w; }
+      }
+      ++it;
+    }
+    sink[blockIdx.x * 256 + tid] = acc + it;
+    if (tid == 32) cycles[1024 + blockIdx.x] = it;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tm, 256);
+}
+
 int main() {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -167,7 +223,7 @@ int main() {
   CK(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0));
   unsigned long long* d_cyc;
   uint32_t* d_sink;
-  CK(cudaMalloc(&d_cyc, sizeof(unsigned long long) * 1024));
+  CK(cudaMalloc(&d_cyc, sizeof(unsigned long long) * 2048));
   CK(cudaMalloc(&d_sink, 1 << 24));
   std::vector<unsigned long long> cyc(1024);
 
@@ -228,6 +284,28 @@ int main() {
     const double macs = double(reps) * 8 * 128 * 256 * 32;
     printf("mma_i8 reps=%d: %.1f cyc/instr, %.0f MAC/clk/SM, chip %.2f POPS at %d MHz\n", reps,
            avg / (reps * 8), macs / avg, 2 * macs / avg * sms * clk_khz * 1e3 / 1e15, clk_khz / 1000);
+  }
+  // 4. MMA chain under smem contention
+  const int smem2 = 160 * 1024;
+  CK(cudaFuncSetAttribute(k_mma_contention<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+  CK(cudaFuncSetAttribute(k_mma_contention<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+  CK(cudaFuncSetAttribute(k_mma_contention<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+  std::vector<unsigned long long> c2(2048);
+  for (int mode = 0; mode < 3; ++mode) {
+    const int reps = 2;
+    for (int rep = 0; rep < 2; ++rep) {
+      if (mode == 0) k_mma_contention<0><<<sms, 256, smem2>>>(reps, d_cyc, d_sink);
+      if (mode == 1) k_mma_contention<1><<<sms, 256, smem2>>>(reps, d_cyc, d_sink);
+      if (mode == 2) k_mma_contention<2><<<sms, 256, smem2>>>(reps, d_cyc, d_sink);
+      CK(cudaDeviceSynchronize());
+    }
+    CK(cudaMemcpy(c2.data(), d_cyc, sizeof(unsigned long long) * 2048, cudaMemcpyDeviceToHost));
+    double avg = 0, its = 0, iss = 0;
+    for (int i = 0; i < sms; ++i) { avg += double(c2[i]) / sms; its += double(c2[1024 + i]) / sms; iss += double(c2[512 + i]) / sms; }
+    printf("  issue-only %.1f cyc/instr\n", iss / (reps * 8));
+    const double bytes = its * 64 * 16 * 224;
+    printf("mma under contention mode=%d: %.1f cyc/instr, other warps moved %.1f B/clk\n", mode,
+           avg / (reps * 8), bytes / avg);
   }
   return 0;
 }
