@@ -172,13 +172,14 @@ def cpu_baseline(name, target_s=12.0, procs=None):
 
 
 # ------------------------------------------------------------------- GPU ----
-def int32_peak(lib, d):
+def live_peak(lib, d, fn):
+    """Best of 2 runs of a libsbw peak microbenchmark (sbw_int32_peak / sbw_int8_mma_peak)."""
     import ctypes
 
     best = 0.0
     for _ in range(2):
         ops, ms = ctypes.c_double(0), ctypes.c_double(0)
-        d.check(lib.sbw_int32_peak(ctypes.byref(ops), ctypes.byref(ms), None))
+        d.check(getattr(lib, fn)(ctypes.byref(ops), ctypes.byref(ms), None))
         best = max(best, ops.value)
     return best
 
@@ -288,14 +289,64 @@ def run_ours(args, rank, world, local_rank):
     assert np.array_equal(h_nl, nl.cpu().numpy())
 
     # ---- roofline of the dominant kernel (fused NL) ----------------------
-    peak = int32_peak(lib, d)
-    alg_ops = n * (1 << n) * nmask  # butterfly element-ops
-    achieved = alg_ops / (kern_ms * 1e-3)
+    peak = live_peak(lib, d, "sbw_int32_peak")
+    tc_path = n == 16 and os.environ.get("SBW_TC", "1") != "0"
     prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_traffic.json")
     traffic = None
     if os.path.exists(prof):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
+    if tc_path:
+        # k_tc16_nl: x bits 0..7 as an int8 GEMM on the tensor cores, bits 8..15
+        # (plus the max fold) as packed 16-bit integer stages.  The integer
+        # half is the limiter (issue-bound), so it is the primary roofline:
+        # 8 stages x 2^16 butterfly element-ops per component against the
+        # packed-16x2 rate (2 x the live int32 lane-op peak).  The tensor half
+        # is reported beside it: 2 * 256 * 2^16 int8 ops per component
+        # (M = u 256 x K = r 256 x N = c 256) against the live kind::i8 peak.
+        peak_i8 = live_peak(lib, d, "sbw_int8_mma_peak")
+        alu_ops = 8 * (1 << n) * nmask
+        mma_ops = 2 * 256 * (1 << n) * nmask
+        achieved = alu_ops / (kern_ms * 1e-3)
+        roofline = {
+            "bound": "int32_alu", "kernel": "k_tc16_nl (tcgen05 int8 MMA + packed int16 stages)",
+            "achieved": achieved / 1e12, "peak": 2 * peak / 1e12, "unit": "Tops/s",
+            "frac": achieved / (2 * peak), "traffic": traffic,
+            "ops_per_launch": alu_ops,
+            "ops_definition": "integer half: 8 stages x 2^16 butterfly element-ops per component "
+                              "(x bits 8..15 incl. the max fold); the other 8 stages run as the "
+                              "int8 GEMM below",
+            "kernel_ms": kern_ms,
+            "peak_source": "measured live by sbw_int32_peak (int32 lane-ops/s) x 2 lanes for "
+                           "packed 16-bit; not in MEASURED_PEAKS.json",
+            "tensor": {"achieved": mma_ops / (kern_ms * 1e-3) / 1e15, "peak": peak_i8 / 1e15,
+                       "unit": "POP/s int8", "frac": mma_ops / (kern_ms * 1e-3) / peak_i8,
+                       "ops_per_launch": mma_ops,
+                       "peak_source": "measured live by sbw_int8_mma_peak (tcgen05.mma.kind::i8 "
+                                      "128x256x32 chains, one CTA per SM)"},
+            "whole_fwht_equiv": {"ops_per_launch": n * (1 << n) * nmask,
+                                 "achieved": n * (1 << n) * nmask / (kern_ms * 1e-3) / 1e12,
+                                 "unit": "T butterfly element-ops/s",
+                                 "vs_packed16_alu_peak": n * (1 << n) * nmask / (kern_ms * 1e-3)
+                                 / (2 * peak)},
+        }
+    else:
+        alg_ops = n * (1 << n) * nmask  # butterfly element-ops
+        achieved = alg_ops / (kern_ms * 1e-3)
+        # The kernel's butterflies run on packed 16-bit (and 8-bit) integer
+        # lanes, two or four per 32-bit instruction, so the denominator is the
+        # packed-16x2 rate: 2 x the measured int32 lane-op peak (same
+        # instruction issue rate, two lanes each).  frac_int32 is the same
+        # number against the plain int32 peak (can exceed 1 because of packing).
+        roofline = {"bound": "int32_alu", "kernel": "k_tile_simd" if n <= 16 else "k3 pass A+B",
+                    "achieved": achieved / 1e12, "peak": 2 * peak / 1e12, "unit": "Tops/s",
+                    "frac": achieved / (2 * peak), "traffic": traffic,
+                    "peak_int32": peak / 1e12, "frac_int32": achieved / peak,
+                    "ops_per_launch": alg_ops, "ops_definition": "n * 2^n butterfly element-ops "
+                    "per component (SURVEY.md 8d)", "kernel_ms": kern_ms,
+                    "peak_source": "measured live by sbw_int32_peak (IADD3/LOP3 + IMAD chains, "
+                                   "int32 lane-ops/s) x 2 lanes for packed 16-bit; "
+                                   "not in MEASURED_PEAKS.json"}
 
     if rank != 0:
         if dist is not None:
@@ -318,27 +369,14 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": (value / world) / (coeffs(16, 16) / (PAPER_16x16_NL_MS * 1e-3))
         if args.config == "16x16" and not args.masks else None,
         "vs_baseline_ref": "PAPER.md:421 fused NL 16x16 = 83,015 ms on i7-8700K-class CPU (BASELINE.md)",
-        "dtype": "int32",
+        "dtype": "int8 MMA (s32 acc) + packed int16" if tc_path else "int32 (packed int8/int16 lanes)",
         "data": "synthetic: generate_sbox(n, m, seed=rank) -- numpy PCG64 like the reference",
         "config": {"workload": f"{args.config} S-box (n={n}, m={m}, bijective={bij}), "
                                f"masks [{v_lo},{v_hi}), full NL per step",
                    "parallelism": f"weak x{world} (one S-box per GPU)",
                    "l2": "flushed between timed steps (256 MiB write), per-step CUDA events"},
         "result": check,
-        # The kernel's butterflies run on packed 16-bit (and 8-bit) integer
-        # lanes, two or four per 32-bit instruction, so the denominator is the
-        # packed-16x2 rate: 2 x the measured int32 lane-op peak (same
-        # instruction issue rate, two lanes each).  frac_int32 is the same
-        # number against the plain int32 peak (can exceed 1 because of packing).
-        "roofline": {"bound": "int32_alu", "kernel": "k_tile_simd" if n <= 16 else "k3 pass A+B",
-                     "achieved": achieved / 1e12, "peak": 2 * peak / 1e12, "unit": "Tops/s",
-                     "frac": achieved / (2 * peak), "traffic": traffic,
-                     "peak_int32": peak / 1e12, "frac_int32": achieved / peak,
-                     "ops_per_launch": alg_ops, "ops_definition": "n * 2^n butterfly element-ops "
-                     "per component (SURVEY.md 8d)", "kernel_ms": kern_ms,
-                     "peak_source": "measured live by sbw_int32_peak (IADD3/LOP3 + IMAD chains, "
-                                    "int32 lane-ops/s) x 2 lanes for packed 16-bit; "
-                                    "not in MEASURED_PEAKS.json"},
+        "roofline": roofline,
         "e2e": {"value": coeffs(n, m, nmask) * world * args.steps / e2e_s, "unit": "coeff/s",
                 "h2d_bytes_per_step": int(table_host.nbytes),
                 "d2h_bytes_per_step": int(h_nl.nbytes + 8 * 4),

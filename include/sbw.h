@@ -160,6 +160,14 @@ int sbw_nl_host(const uint32_t* h_table, int n, int m, uint32_t v_lo, uint32_t v
  */
 int sbw_int32_peak(double* ops_per_s, double* ms, void* stream);
 
+/*
+ * Dense int8 tensor-core peak microbenchmark on the current device: one CTA
+ * per SM issues back-to-back tcgen05.mma.kind::i8 (M=128, N=256, K=32, s32
+ * accumulators in TMEM) from shared-memory operands.  Writes int8 ops per
+ * second (2 per multiply-add) and the kernel time.
+ */
+int sbw_int8_mma_peak(double* ops_per_s, double* ms, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

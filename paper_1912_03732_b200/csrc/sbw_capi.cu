@@ -356,4 +356,9 @@ int sbw_int32_peak(double* ops_per_s, double* ms, void* stream) {
   return run_int32_peak(ops_per_s, ms, as_stream(stream));
 }
 
+int sbw_int8_mma_peak(double* ops_per_s, double* ms, void* stream) {
+  if (!ops_per_s) return set_error(SBW_EINVAL, "null output");
+  return run_int8_mma_peak(ops_per_s, ms, as_stream(stream));
+}
+
 }  // extern "C"

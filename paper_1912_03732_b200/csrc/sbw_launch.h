@@ -59,5 +59,6 @@ int launch_walsh_direct(const void* table, int tbytes, int n, const uint32_t* u,
 int launch_bruteforce(const void* table, int tbytes, int n, int m, int32_t* best,
                       cudaStream_t st);
 int run_int32_peak(double* ops_per_s, double* ms_out, cudaStream_t st);
+int run_int8_mma_peak(double* ops_per_s, double* ms_out, cudaStream_t st);
 
 }  // namespace sbw

@@ -15,14 +15,17 @@
 //   columns (c) of s32 = all 512 TMEM columns.
 //
 //   Stages over c (8 of them) run on the integer pipes, one TMEM lane (one u)
-//   per thread, 256 values in registers as biased 16-bit lane pairs (the
-//   representation of sbw_tile_simd.cuh: after k stages s = W_k / 2 + 2^(k-1)).
-//   The c-bit-0 stage is fused into the packing, two IMADs per pair:
-//   (a, b) -> lanes (a + b + 2^8, a - b + 2^8); c bits 1..6 are packed
-//   stages; c bit 7 (top) is fused with the VIMNMX3 max/min fold.  The TMEM
-//   reads come in 4 chunks of 64 columns, each overlapped with the stages of
-//   the previous chunk.  The row u = 0 offset (-128 on every c) only reaches
-//   the coefficient u = 0; its thread adds 2^15 there.
+//   per thread, 256 values in registers, two 16-bit lanes per register.  A
+//   register is the exact integer lo + 2^16 hi (mod 2^32) of its two lane
+//   values, so every butterfly is one plain 32-bit add or sub with no per-stage
+//   bias, and borrows between the lanes cancel out.  The c-bit-0 stage is
+//   fused into the packing, (a, b) -> (a + b) + 2^16 (a - b) (two IMADs);
+//   c bits 1..6 are add/sub stages; the c-bit-7 (top) stage adds 2^15 per
+//   lane, which turns the lanes into the non-negative s = W / 2 + 2^15 of
+//   sbw_tile_simd.cuh, and feeds the VIMNMX3 max/min fold.  The row u = 0
+//   offset (-128 on every c) only reaches the coefficient u = 0; its thread
+//   adds 2^15 there.  TMEM is read in two pairs of 64-column loads and
+//   released before the stages start.
 //
 // Scheduling (one CTA of 8 warps per SM, persistent over a contiguous range of
 // masks; each thread owns one TMEM lane for the transform and one B row c for
@@ -90,40 +93,37 @@ __device__ __forceinline__ void store_row(const uint32_t (&g)[8], uint8_t* bbuf,
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const uint32_t w = g[j];
+#if SBW_TC_MULHI
+    // w >> k as a high multiply moves the shifts to the FMA pipe
+    *reinterpret_cast<uint4*>(row + (2 * j) * 128) =
+        make_uint4(w & M, __umulhi(w, 1u << 31) & M, __umulhi(w, 1u << 30) & M, __umulhi(w, 1u << 29) & M);
+    *reinterpret_cast<uint4*>(row + (2 * j + 1) * 128) =
+        make_uint4(__umulhi(w, 1u << 28) & M, __umulhi(w, 1u << 27) & M, __umulhi(w, 1u << 26) & M,
+                   __umulhi(w, 1u << 25) & M);
+#else
     *reinterpret_cast<uint4*>(row + (2 * j) * 128) =
         make_uint4(w & M, (w >> 1) & M, (w >> 2) & M, (w >> 3) & M);
     *reinterpret_cast<uint4*>(row + (2 * j + 1) * 128) =
         make_uint4((w >> 4) & M, (w >> 5) & M, (w >> 6) & M, (w >> 7) & M);
+#endif
   }
 }
 
-// Biased packed stages (see sbw_tile_simd.cuh): stage k on (x, y) gives
-// (x + y, x - y + 2^k) per 16-bit lane.  Register-index bits [0, NB) of
-// R[off .. off + 2^NB), first stage index K0 (off is a compile-time constant
-// after unrolling).
-template <int NB, int K0>
-__device__ __forceinline__ void stages_sub(uint32_t (&R)[128], int off) {
-#pragma unroll
-  for (int sb = 0; sb < NB; ++sb)
-#pragma unroll
-    for (int k = 0; k < (1 << NB); ++k)
-      if ((k & (1 << sb)) == 0) {
-        const uint32_t x = R[off + k], y = R[off + (k | (1 << sb))];
-        R[off + k] = x + y;
-        R[off + (k | (1 << sb))] = x - y + ((1u << (K0 + sb)) * 0x00010001u);
-      }
-}
-// one stage over register-index bit SB of R[off .. off + 2^(SB+1)), stage index K
-template <int SB, int K>
-__device__ __forceinline__ void stages_bit(uint32_t (&R)[128], int off) {
-#pragma unroll
-  for (int k = 0; k < (2 << SB); ++k)
-    if ((k & (1 << SB)) == 0) {
-      const uint32_t x = R[off + k], y = R[off + (k | (1 << SB))];
-      R[off + k] = x + y;
-      R[off + (k | (1 << SB))] = x - y + ((1u << K) * 0x00010001u);
-    }
-}
+#ifndef SBW_TC_BIASFREE
+#define SBW_TC_BIASFREE 0
+#endif
+#ifndef SBW_TC_MULHI
+#define SBW_TC_MULHI 0
+#endif
+// Lane biases.  Bias-free: exact integer add/sub, +2^15 per lane at the top.
+// Biased (sbw_tile_simd.cuh form, s = W/2 + 2^(k-1) after k stages): the
+// diffs carry +2^k per lane, which makes them 3-input IADD3s on the ALU pipe
+// while the sums go to the FMA pipe.
+#if SBW_TC_BIASFREE
+constexpr uint32_t kPackBias = 0u, kStageBias = 0u, kTopBias = 0x80008000u;
+#else
+constexpr uint32_t kPackBias = 0x01000100u, kStageBias = 0x02000200u, kTopBias = 0u;
+#endif
 
 __device__ __forceinline__ void publish(const uint32_t* wmax, uint32_t v, uint32_t v_lo,
                                         int32_t* max_abs, unsigned long long* key) {
@@ -276,26 +276,32 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         tc::tmem_ld_x64(tbase + h * 128 + 64, t1);
         tc::wait_ld_tied(t0);
         tc::wait_ld_tied(t1);
-        // c bit 0 stage + packing: biased lanes (a + b + 256, a - b + 256)
+        // c bit 0 stage + packing: (a, b) -> the integer (a + b) + 2^16 (a - b) (+ bias)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          R[64 * h + j] = t0[2 * j] * 0x10001u + t0[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
-          R[64 * h + 32 + j] = t1[2 * j] * 0x10001u + t1[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
+          R[64 * h + j] = t0[2 * j] * 0x10001u + t0[2 * j + 1] * 0xFFFF0001u + kPackBias;
+          R[64 * h + 32 + j] = t1[2 * j] * 0x10001u + t1[2 * j + 1] * 0xFFFF0001u + kPackBias;
         }
       }
       tc::fence_before();
       mbar_arrive(&bar_tmem_empty);
-      // c bits 1..6 (stages 9..14)
+      // c bits 1..6 (stages 9..14), exact integer add / sub
 #pragma unroll
-      for (int q = 0; q < 4; ++q) stages_sub<5, 9>(R, 32 * q);
-      stages_bit<5, 14>(R, 0);
-      stages_bit<5, 14>(R, 64);
+      for (int sb = 0; sb < 6; ++sb)
+#pragma unroll
+        for (int k = 0; k < 128; ++k)
+          if ((k & (1 << sb)) == 0) {
+            const uint32_t x = R[k], y = R[k | (1 << sb)];
+            R[k] = x + y;
+            R[k | (1 << sb)] = x - y + (kStageBias << sb);
+          }
       // c bit 7 (stage 15, top) fused with the max/min fold (carry argument: tile_last_pass)
       uint32_t mx = 0u, mn = 0xFFFFFFFFu;
 #pragma unroll
       for (int k = 0; k < 64; ++k) {
         const uint32_t x = R[k], y = R[k + 64];
-        const uint32_t S = x + y + (k == 0 ? corr0 : 0u);
+        // + 2^15 per lane: the biased s = W / 2 + 2^15 of tile_last_pass
+        const uint32_t S = x + y + (k == 0 ? kTopBias + corr0 : kTopBias);
         const uint32_t D = x - y + 0x80008000u;
         mx = __vimax3_u16x2(mx, S, D);
         mn = __vimin3_u16x2(mn, S, D);
@@ -316,7 +322,76 @@ __global__ void __launch_bounds__(kAllThreads, 1)
   }
 }
 
+// int8 MMA peak: one CTA per SM, one thread issues `reps` chains of 8
+// accumulating 128x256x32 MMAs on fixed smem operands (A 32 KiB, B 64 KiB).
+__global__ void __launch_bounds__(128, 1) k_int8_mma_peak(int reps, int* sink) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 96 * 1024 / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(i, 3 * i, 5, 7);
+  if (warp == 0) tc::tmem_alloc(&slot, 256);
+  if (tid == 0) tc::mbar_init(&bar, 1);
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = slot;
+  if (warp == 0) {
+    const uint64_t da = tc::sdesc(tc::smem_u32(smem), 128, 2048);
+    const uint64_t db = tc::sdesc(tc::smem_u32(smem + 32768), 128, 2048);
+    for (int r = 0; r < reps; ++r)
+#pragma unroll
+      for (int kb = 0; kb < 8; ++kb)
+        tc::mma_i8_elect(tmem, da + uint64_t(kb * 16), db + uint64_t(kb * 16), kIdesc, (r | kb) ? 1u : 0u);
+    tc::mma_commit_elect(&bar);
+    tc::mbar_wait(&bar, 0u);
+    tc::fence_after();
+    uint32_t t[32];
+    tc::tmem_ld_x32(tmem, t);
+    tc::wait_ld();
+    if (t[0] == 0x12345678u) sink[0] = 1;  // keeps the chain observable
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+}
+
 }  // namespace
+
+int run_int8_mma_peak(double* ops_per_s, double* ms_out, cudaStream_t st) {
+  DeviceProps dp;
+  if (int rc = device_props(&dp)) return rc;
+  const int smem = 96 * 1024;
+  SBW_CUDA_CHECK(cudaFuncSetAttribute(k_int8_mma_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int* sink = nullptr;
+  SBW_CUDA_CHECK(cudaMallocAsync(&sink, sizeof(int), st));
+  cudaEvent_t e0, e1;
+  SBW_CUDA_CHECK(cudaEventCreate(&e0));
+  SBW_CUDA_CHECK(cudaEventCreate(&e1));
+  const int reps = 2048;
+  double best = 0, best_ms = 0;
+  for (int rep = 0; rep < 4; ++rep) {
+    SBW_CUDA_CHECK(cudaEventRecord(e0, st));
+    k_int8_mma_peak<<<dp.sm_count, 128, smem, st>>>(reps, sink);
+    SBW_LAUNCH_CHECK("k_int8_mma_peak");
+    SBW_CUDA_CHECK(cudaEventRecord(e1, st));
+    SBW_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0;
+    SBW_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    const double ops = 2.0 * dp.sm_count * double(reps) * 8 * 128 * 256 * 32;
+    if (rep > 0 && ops / (ms * 1e-3) > best) {
+      best = ops / (ms * 1e-3);
+      best_ms = ms;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  SBW_CUDA_CHECK(cudaFreeAsync(sink, st));
+  *ops_per_s = best;
+  if (ms_out) *ms_out = best_ms;
+  return SBW_OK;
+}
 
 // SBW_TC=0 selects the all-ALU tile kernel instead (A/B experiments only).
 bool tc_path_enabled() {

@@ -14,7 +14,8 @@ import weakref
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsbw.so")
+# SBW_LIB_PATH: an alternative build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("SBW_LIB_PATH") or os.path.join(_HERE, "libsbw.so")
 
 SBW_OK, SBW_EINVAL, SBW_ECUDA, SBW_EPARITY, SBW_ERANGE = 0, -1, -2, -3, -4
 LAYOUT_MASK_MAJOR, LAYOUT_X_MAJOR = 0, 1
@@ -42,6 +43,7 @@ SIGNATURES = {
     "sbw_nl_bruteforce": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp]),
     "sbw_nl_host": (_i32, [_vp, _i32, _i32, _u32, _u32, _vp, _vp, _i32]),
     "sbw_int32_peak": (_i32, [_c.POINTER(_c.c_double), _c.POINTER(_c.c_double), _vp]),
+    "sbw_int8_mma_peak": (_i32, [_c.POINTER(_c.c_double), _c.POINTER(_c.c_double), _vp]),
 }
 
 
