@@ -1,0 +1,88 @@
+"""Parity of the n = 16 tensor-core kernel (k_tc16_nl, sbw_tc.cu).
+
+sbw_nl at n = 16 runs the hybrid kernel: x bits 0..7 as an int8 tcgen05 GEMM,
+bits 8..15 as packed integer stages.  These cases target what is specific to
+it -- the u = 0 row correction, the Gray-code mask order inside aligned
+blocks of 256, CTA ranges of one or two masks, m > 16 -- and cross-check it
+against the all-ALU tile kernel (SBW_TC=0, k_tile_simd) on the same inputs.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import paper_1912_03732_b200 as sw
+from oracle import sbw_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _maxima(s, lo, hi):
+    mx, key = sw.component_max_abs_device(s, lo, hi)
+    return mx.cpu().numpy().astype(np.int64), sw.transforms.decode_key(key, s.n)
+
+
+def test_constant_components_w0_extremes():
+    """Bit 15 of S is constant 1 and bit 14 constant 0: the components v =
+    0x8000 and 0x4000 are constant, so the maximum is W(0) = -2^16 / +2^16 --
+    the coefficient that carries the row u = 0 correction."""
+    rng = np.random.default_rng(5)
+    t = (rng.integers(0, 1 << 14, 1 << 16, dtype=np.uint32) | 0x8000)
+    s = sw.SBox(16, 16, t)
+    for lo, hi in [(0x4000 - 3, 0x4000 + 3), (0x8000 - 2, 0x8000 + 5), (0xC000 - 1, 0xC000 + 1)]:
+        got, _ = _maxima(s, lo, hi)
+        assert np.array_equal(got, orc.component_max_abs(s.table, 16, lo, hi))
+    got, _ = _maxima(s, 0x8000, 0x8001)
+    assert got[0] == 1 << 16
+
+
+@pytest.mark.parametrize("lo,hi", [(1, 2), (1, 149), (1, 297), (255, 258), (256, 512),
+                                   (200, 1000), (65280, 65536), (12345, 12345 + 777)])
+def test_ranges_and_gray_blocks(lo, hi):
+    """One or two masks per CTA, ranges that start/end inside aligned blocks
+    of 256 (natural order there) and whole blocks (Gray-code order)."""
+    s = sw.generate_sbox(16, 16, 21, bijective=True)
+    got, (nl, v, m) = _maxima(s, lo, hi)
+    want = orc.component_max_abs(s.table, 16, lo, hi)
+    assert np.array_equal(got, want)
+    i = int(np.argmax(want))  # first maximum = smallest v
+    assert (v, m) == (lo + i, int(want[i]))
+    assert nl == ((1 << 16) - int(want[i])) // 2
+
+
+@pytest.mark.parametrize("m", [1, 5, 20, 24])
+def test_output_widths(m):
+    s = sw.generate_sbox(16, m, 3 + m, bijective=False)
+    hi = min(1 << m, 700)
+    got, _ = _maxima(s, 1, hi)
+    assert np.array_equal(got, orc.component_max_abs(s.table, 16, 1, hi))
+
+
+_ARM = r'''
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1912_03732_b200 as sw
+out = {}
+for seed, m, lo, hi in [(0, 16, 1, 65536), (9, 18, 1, 40000), (4, 16, 999, 4242)]:
+    s = sw.generate_sbox(16, m, seed, bijective=(m == 16))
+    mx, key = sw.component_max_abs_device(s, lo, hi)
+    out[f"{seed},{m},{lo},{hi}"] = [mx.cpu().numpy().astype(np.int64).tolist(), int(key.item())]
+print(json.dumps(out))
+'''
+
+
+def test_tensor_core_kernel_matches_alu_kernel():
+    """Same maxima and key from k_tc16_nl and from k_tile_simd<16> (SBW_TC=0)."""
+    res = {}
+    for tc in ("1", "0"):
+        p = subprocess.run([sys.executable, "-c", _ARM, ROOT], env=dict(os.environ, SBW_TC=tc),
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[tc] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["1"] == res["0"]
