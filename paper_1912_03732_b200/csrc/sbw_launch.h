@@ -23,6 +23,12 @@ int launch_fused_onchip(const void* table, int tbytes, int n, int m, uint32_t v_
 int launch_tc16_nl(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
                    unsigned long long* key, cudaStream_t st);
 bool tc_path_enabled();
+// Tensor-core pass A of the multi-pass NL path (n = 17..24): 15 stages per
+// 2^15 block, biased u16 out in a block-internal word order of its own
+// (pass B pairs equal word positions across blocks only, so any fixed order
+// works for NL; SPEC keeps launch_emit_tiles).
+int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_comp, uint32_t* emit,
+                   cudaStream_t st);
 
 // Multi-pass path (n >= 17): planes, then pass A (emit) + pass B per L2-sized batch.
 size_t k3_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi);

@@ -120,7 +120,10 @@ int launch_k3_batched(const uint32_t* planes, int n, int m, uint32_t v_lo, uint3
     const uint32_t vf = v_lo + uint32_t(c0);
     const int buf = int(nb & 1);
     if (nb >= 2) SBW_CUDA_CHECK(cudaStreamWaitEvent(ks->a, ks->done_b[buf], 0));  // buffer free
-    if (int rc = launch_emit_tiles(planes, n, m, vf, nc, emit[buf], ks->a)) return rc;
+    if (int rc = (out == nullptr && tc_path_enabled())
+                     ? launch_tc_emit(planes, n, vf, nc, emit[buf], ks->a)
+                     : launch_emit_tiles(planes, n, m, vf, nc, emit[buf], ks->a))
+      return rc;
     SBW_CUDA_CHECK(cudaEventRecord(ks->done_a[buf], ks->a));
     SBW_CUDA_CHECK(cudaStreamWaitEvent(ks->b, ks->done_a[buf], 0));
     PassBArgs a{};

@@ -75,17 +75,6 @@ __device__ __forceinline__ void xor_plane(uint32_t (&g)[8], const uint4& a, cons
   g[4] ^= b.x; g[5] ^= b.y; g[6] ^= b.z; g[7] ^= b.w;
 }
 
-// XOR in the planes of every set bit of d (row c's 8 plane words)
-__device__ __forceinline__ void xor_planes(const uint32_t* __restrict__ planes, uint32_t d,
-                                           uint32_t (&g)[8], int c) {
-  while (d) {
-    const int i = __ffs(d) - 1;
-    d &= d - 1;
-    const uint4* p = reinterpret_cast<const uint4*>(planes + (int64_t(i) << 11) + c * 8);
-    xor_plane(g, __ldg(p), __ldg(p + 1));
-  }
-}
-
 // Expand the 256 bits of row c into the u8 B operand (K-major core matrices).
 __device__ __forceinline__ void store_row(const uint32_t (&g)[8], uint8_t* bbuf, int c) {
   uint8_t* row = bbuf + (c >> 3) * 2048 + (c & 7) * 16;
@@ -93,37 +82,12 @@ __device__ __forceinline__ void store_row(const uint32_t (&g)[8], uint8_t* bbuf,
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const uint32_t w = g[j];
-#if SBW_TC_MULHI
-    // w >> k as a high multiply moves the shifts to the FMA pipe
-    *reinterpret_cast<uint4*>(row + (2 * j) * 128) =
-        make_uint4(w & M, __umulhi(w, 1u << 31) & M, __umulhi(w, 1u << 30) & M, __umulhi(w, 1u << 29) & M);
-    *reinterpret_cast<uint4*>(row + (2 * j + 1) * 128) =
-        make_uint4(__umulhi(w, 1u << 28) & M, __umulhi(w, 1u << 27) & M, __umulhi(w, 1u << 26) & M,
-                   __umulhi(w, 1u << 25) & M);
-#else
     *reinterpret_cast<uint4*>(row + (2 * j) * 128) =
         make_uint4(w & M, (w >> 1) & M, (w >> 2) & M, (w >> 3) & M);
     *reinterpret_cast<uint4*>(row + (2 * j + 1) * 128) =
         make_uint4((w >> 4) & M, (w >> 5) & M, (w >> 6) & M, (w >> 7) & M);
-#endif
   }
 }
-
-#ifndef SBW_TC_BIASFREE
-#define SBW_TC_BIASFREE 0
-#endif
-#ifndef SBW_TC_MULHI
-#define SBW_TC_MULHI 0
-#endif
-// Lane biases.  Bias-free: exact integer add/sub, +2^15 per lane at the top.
-// Biased (sbw_tile_simd.cuh form, s = W/2 + 2^(k-1) after k stages): the
-// diffs carry +2^k per lane, which makes them 3-input IADD3s on the ALU pipe
-// while the sums go to the FMA pipe.
-#if SBW_TC_BIASFREE
-constexpr uint32_t kPackBias = 0u, kStageBias = 0u, kTopBias = 0x80008000u;
-#else
-constexpr uint32_t kPackBias = 0x01000100u, kStageBias = 0x02000200u, kTopBias = 0u;
-#endif
 
 __device__ __forceinline__ void publish(const uint32_t* wmax, uint32_t v, uint32_t v_lo,
                                         int32_t* max_abs, unsigned long long* key) {
@@ -164,19 +128,56 @@ constexpr int kIssuerRegs = 32;
 constexpr int kMathRegs = 232;
 constexpr int kAllThreads = 128 + kMathWarps * 32;  // warpgroup 0: issuer (+3 idle warps)
 
-__global__ void __launch_bounds__(kAllThreads, 1)
-    k_tc16_nl(const uint32_t* __restrict__ planes, uint32_t v_lo, uint32_t v_hi,
-              int32_t* __restrict__ max_abs, unsigned long long* key) {
+struct TcArgs {
+  const uint32_t* planes;
+  int64_t plane_words;  // 2^n / 32
+  // NL (n = 16): masks [v_lo, v_hi), Gray order inside aligned 256-blocks
+  uint32_t v_lo, v_hi;
+  int32_t* max_abs;
+  unsigned long long* key;
+  // EMIT (pass A of the multi-pass path, n = 17..24): item t = (component
+  // v_first + t % n_comp, 2^16-block bp = t / n_comp); 15 stages per 2^15 block
+  uint32_t v_first;
+  int64_t n_comp, n_items;
+  int n_full;
+  uint32_t* emit;
+};
+
+template <bool EMIT>
+__device__ __forceinline__ int64_t items_total(const TcArgs& a) {
+  return EMIT ? a.n_items : int64_t(a.v_hi) - a.v_lo;
+}
+// item t of the launch -> (mask v, 2^16-block index bp)
+template <bool EMIT>
+__device__ __forceinline__ void item_at(const TcArgs& a, int64_t t, uint32_t& v, uint32_t& bp) {
+  if constexpr (EMIT) {
+    bp = uint32_t(t / a.n_comp);
+    v = a.v_first + uint32_t(t - int64_t(bp) * a.n_comp);
+  } else {
+    bp = 0;
+    v = mask_at(a.v_lo + t, a.v_lo, a.v_hi);
+  }
+}
+
+// Generation state of one transform thread: row c's 8 plane words for mask
+// vcur in block bpcur.
+struct GenState16 {
+  uint32_t g[8];
+  uint32_t vcur, bpcur;
+};
+
+template <bool EMIT>
+__global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   // full: MMA(i) done.  tmem_empty: all transform threads read D(i).
   // bfull[b]: all transform threads generated the B operand in buffer b.
   __shared__ uint64_t bar_full, bar_tmem_empty, bar_bfull[2], bar_done;
   __shared__ uint32_t tmem_slot;
-  __shared__ __align__(16) uint32_t s_wmax[4][kMathWarps];  // per-warp max|W|, slot = mask index & 3
+  __shared__ __align__(16) uint32_t s_wmax[4][kMathWarps];  // per-warp max|W|, slot = item index & 3
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t total = int64_t(v_hi) - v_lo;
-  const int64_t q_lo = v_lo + total * blockIdx.x / gridDim.x;
-  const int n_my = int(v_lo + total * (blockIdx.x + 1) / gridDim.x - q_lo);
+  const int64_t total = items_total<EMIT>(a);
+  const int64_t t_lo = total * blockIdx.x / gridDim.x;
+  const int n_my = int(total * (blockIdx.x + 1) / gridDim.x - t_lo);
 
   // A = -H_256 with the K permutation of store_row
   for (int e = tid; e < 256 * 16; e += kAllThreads) {
@@ -216,17 +217,23 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         if (i > 0) tc::mbar_wait(&bar_tmem_empty, uint32_t((i - 1) & 1));
         tc::fence_after();
         issue_mma_warp(tmem, smem, i & 1, &bar_full);
-        // bfull for mask i (i >= 2) is produced after each thread stored its
-        // max of mask i - 2
-        if (i >= 2 && lane == 0)
-          publish(s_wmax[(i - 2) & 3], mask_at(q_lo + i - 2, v_lo, v_hi), v_lo, max_abs, key);
+        if constexpr (!EMIT) {
+          // bfull for mask i (i >= 2) is produced after each thread stored
+          // its max of mask i - 2
+          if (i >= 2 && lane == 0)
+            publish(s_wmax[(i - 2) & 3], mask_at(a.v_lo + t_lo + i - 2, a.v_lo, a.v_hi), a.v_lo,
+                    a.max_abs, a.key);
+        }
       }
       // every transform thread has read D(last) and stored its last max
       tc::mbar_wait(&bar_done, 0u);
       tc::fence_after();
-      if (lane == 0)
-        for (int i = n_my - 2 < 0 ? 0 : n_my - 2; i < n_my; ++i)
-          publish(s_wmax[i & 3], mask_at(q_lo + i, v_lo, v_hi), v_lo, max_abs, key);
+      if constexpr (!EMIT) {
+        if (lane == 0)
+          for (int i = n_my - 2 < 0 ? 0 : n_my - 2; i < n_my; ++i)
+            publish(s_wmax[i & 3], mask_at(a.v_lo + t_lo + i, a.v_lo, a.v_hi), a.v_lo, a.max_abs,
+                    a.key);
+      }
       __syncwarp();
       tc::tmem_dealloc(tmem, 512);
     }
@@ -235,30 +242,55 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kMathRegs));
     const int mt = tid - 128, mw = mt >> 5;  // transform thread / warp index
     const int c = mt;                        // generation row
-    uint32_t g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    uint32_t vcur = 0;
+    const uint32_t* __restrict__ planes = a.planes;
+    const int64_t pw = a.plane_words;
+    GenState16 gs;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) gs.g[k] = 0;
+    gs.vcur = 0;
+    gs.bpcur = 0;
+    // rows c of block bp start at plane word bp * 2048 + 8 c
+    auto row_off = [&](uint32_t bp) { return int64_t(bp) * 2048 + c * 8; };
+    auto xor_all = [&](uint32_t d, uint32_t bp) {
+      while (d) {
+        const int i = __ffs(d) - 1;
+        d &= d - 1;
+        const uint4* p = reinterpret_cast<const uint4*>(planes + int64_t(i) * pw + row_off(bp));
+        xor_plane(gs.g, __ldg(p), __ldg(p + 1));
+      }
+    };
     for (int k = 0; k < 2 && k < n_my; ++k) {
-      const uint32_t vn = mask_at(q_lo + k, v_lo, v_hi);
-      xor_planes(planes, vcur ^ vn, g, c);
-      vcur = vn;
-      store_row(g, smem + kBOff + k * kBBytes, c);
+      uint32_t vn, bpn;
+      item_at<EMIT>(a, t_lo + k, vn, bpn);
+      if (bpn != gs.bpcur) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) gs.g[q] = 0;
+        gs.vcur = 0;
+        gs.bpcur = bpn;
+      }
+      xor_all(gs.vcur ^ vn, bpn);
+      gs.vcur = vn;
+      store_row(gs.g, smem + kBOff + k * kBBytes, c);
       tc::fence_proxy_async();
       mbar_arrive(&bar_bfull[k]);
     }
     // this thread's TMEM lane: u = 128 * (mw >> 2) + 32 * (mw & 3) + lane
     // (warp w may only touch lanes 32 * (w % 4) .. +31; here w % 4 == mw % 4)
+    const int u = 128 * (mw >> 2) + 32 * (mw & 3) + lane;
     const uint32_t tbase = tmem + (uint32_t((mw & 3) * 32) << 16) + uint32_t(mw >> 2) * 256;
-    const uint32_t corr0 = (mt == 0) ? 0x8000u : 0u;  // row u = 0 offset, see above
     for (int i = 0; i < n_my; ++i) {
-      // prefetch the first plane of the mask two steps ahead
+      // prefetch the first plane of the item two steps ahead
       const bool gen = i + 2 < n_my;
-      uint32_t vn = 0, d = 0;
+      uint32_t vn = 0, bpn = 0, d = 0;
+      bool reset = false;
       uint4 pa = make_uint4(0, 0, 0, 0), pb = pa;
       if (gen) {
-        vn = mask_at(q_lo + i + 2, v_lo, v_hi);
-        d = vcur ^ vn;
+        item_at<EMIT>(a, t_lo + i + 2, vn, bpn);
+        reset = bpn != gs.bpcur;
+        d = reset ? vn : (gs.vcur ^ vn);
         if (d) {
-          const uint4* p = reinterpret_cast<const uint4*>(planes + (int64_t(__ffs(d) - 1) << 11) + c * 8);
+          const uint4* p =
+              reinterpret_cast<const uint4*>(planes + int64_t(__ffs(d) - 1) * pw + row_off(bpn));
           pa = __ldg(p);
           pb = __ldg(p + 1);
           d &= d - 1;
@@ -276,16 +308,16 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         tc::tmem_ld_x64(tbase + h * 128 + 64, t1);
         tc::wait_ld_tied(t0);
         tc::wait_ld_tied(t1);
-        // c bit 0 stage + packing: (a, b) -> the integer (a + b) + 2^16 (a - b) (+ bias)
+        // c bit 0 stage + packing: biased lanes (a + b + 256, a - b + 256)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          R[64 * h + j] = t0[2 * j] * 0x10001u + t0[2 * j + 1] * 0xFFFF0001u + kPackBias;
-          R[64 * h + 32 + j] = t1[2 * j] * 0x10001u + t1[2 * j + 1] * 0xFFFF0001u + kPackBias;
+          R[64 * h + j] = t0[2 * j] * 0x10001u + t0[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
+          R[64 * h + 32 + j] = t1[2 * j] * 0x10001u + t1[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
         }
       }
       tc::fence_before();
       mbar_arrive(&bar_tmem_empty);
-      // c bits 1..6 (stages 9..14), exact integer add / sub
+      // c bits 1..6 (stages 9..14)
 #pragma unroll
       for (int sb = 0; sb < 6; ++sb)
 #pragma unroll
@@ -293,26 +325,55 @@ __global__ void __launch_bounds__(kAllThreads, 1)
           if ((k & (1 << sb)) == 0) {
             const uint32_t x = R[k], y = R[k | (1 << sb)];
             R[k] = x + y;
-            R[k | (1 << sb)] = x - y + (kStageBias << sb);
+            R[k | (1 << sb)] = x - y + (0x02000200u << sb);
           }
-      // c bit 7 (stage 15, top) fused with the max/min fold (carry argument: tile_last_pass)
-      uint32_t mx = 0u, mn = 0xFFFFFFFFu;
+      if constexpr (EMIT) {
+        // 15 stages per 2^15 block (c bit 7 = the block's parity is left to
+        // pass B).  Lanes are s = W_15 / 2 + 2^14; the row u = 0 offset sits in
+        // the lo lane of R[0] / R[64] (-128 x 128 columns).  Block word layout
+        // (pass B only pairs equal positions across blocks):
+        //   word (j >> 2) * 1024 + 4 u + (j & 3)  <-  R[64 h + j]
+        if (u == 0) {
+          R[0] += 0x4000u;
+          R[64] += 0x4000u;
+        }
+        uint32_t vi, bpi;
+        item_at<EMIT>(a, t_lo + i, vi, bpi);
+        uint32_t* dst = a.emit + (int64_t(vi - a.v_first) << (a.n_full - 1)) +
+                        (int64_t(2 * bpi) << 14) + 4 * u;
 #pragma unroll
-      for (int k = 0; k < 64; ++k) {
-        const uint32_t x = R[k], y = R[k + 64];
-        // + 2^15 per lane: the biased s = W / 2 + 2^15 of tile_last_pass
-        const uint32_t S = x + y + (k == 0 ? kTopBias + corr0 : kTopBias);
-        const uint32_t D = x - y + 0x80008000u;
-        mx = __vimax3_u16x2(mx, S, D);
-        mn = __vimin3_u16x2(mn, S, D);
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            *reinterpret_cast<uint4*>(dst + (h << 14) + q * 1024) =
+                make_uint4(R[64 * h + 4 * q], R[64 * h + 4 * q + 1], R[64 * h + 4 * q + 2],
+                           R[64 * h + 4 * q + 3]);
+      } else {
+        // c bit 7 (stage 15, top) fused with the max/min fold (carry argument:
+        // tile_last_pass); the row u = 0 offset reaches only S of k = 0
+        const uint32_t corr0 = (u == 0) ? 0x8000u : 0u;
+        uint32_t mx = 0u, mn = 0xFFFFFFFFu;
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          const uint32_t x = R[k], y = R[k + 64];
+          const uint32_t S = x + y + (k == 0 ? corr0 : 0u);
+          const uint32_t D = x - y + 0x80008000u;
+          mx = __vimax3_u16x2(mx, S, D);
+          mn = __vimin3_u16x2(mn, S, D);
+        }
+        const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<16>(mx, mn)));
+        if (lane == 0) s_wmax[i & 3][mw] = m;
       }
-      const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<16>(mx, mn)));
-      if (lane == 0) s_wmax[i & 3][mw] = m;
       if (gen) {
-        xor_plane(g, pa, pb);
-        xor_planes(planes, d, g, c);  // rare: more than one changed bit
-        vcur = vn;
-        store_row(g, smem + kBOff + (i & 1) * kBBytes, c);
+        if (reset) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) gs.g[q] = 0;
+          gs.bpcur = bpn;
+        }
+        xor_plane(gs.g, pa, pb);
+        xor_all(d, bpn);  // rare: more than one changed bit
+        gs.vcur = vn;
+        store_row(gs.g, smem + kBOff + (i & 1) * kBBytes, c);
         tc::fence_proxy_async();
         mbar_arrive(&bar_bfull[i & 1]);
       }
@@ -402,21 +463,48 @@ bool tc_path_enabled() {
   return on;
 }
 
-int launch_tc16_nl(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
-                   unsigned long long* key, cudaStream_t st) {
-  if (v_hi <= v_lo) return SBW_OK;
+namespace {
+template <bool EMIT>
+int run_tc_hybrid(const TcArgs& a, int64_t items, cudaStream_t st) {
+  if (items <= 0) return SBW_OK;
   DeviceProps dp;
   if (int rc = device_props(&dp)) return rc;
-  static unsigned long long attr_done = 0;
+  static unsigned long long attr_done = 0;  // per device; the call is idempotent
   if (!(attr_done >> (dp.device & 63) & 1ull)) {
-    SBW_CUDA_CHECK(cudaFuncSetAttribute(k_tc16_nl, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
+    SBW_CUDA_CHECK(cudaFuncSetAttribute(k_tc_hybrid<EMIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kTcSmem));
     attr_done |= 1ull << (dp.device & 63);
   }
-  const int64_t count = int64_t(v_hi) - v_lo;
-  const int grid = int(count < dp.sm_count ? count : dp.sm_count);
-  k_tc16_nl<<<grid, kAllThreads, kTcSmem, st>>>(planes, v_lo, v_hi, max_abs, key);
-  SBW_LAUNCH_CHECK("k_tc16_nl");
+  const int grid = int(items < dp.sm_count ? items : dp.sm_count);
+  k_tc_hybrid<EMIT><<<grid, kAllThreads, kTcSmem, st>>>(a);
+  SBW_LAUNCH_CHECK(EMIT ? "k_tc_hybrid<emit>" : "k_tc_hybrid<nl>");
   return SBW_OK;
+}
+}  // namespace
+
+int launch_tc16_nl(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
+                   unsigned long long* key, cudaStream_t st) {
+  TcArgs a{};
+  a.planes = planes;
+  a.plane_words = 2048;
+  a.v_lo = v_lo;
+  a.v_hi = v_hi;
+  a.max_abs = max_abs;
+  a.key = key;
+  return run_tc_hybrid<false>(a, int64_t(v_hi) - v_lo, st);
+}
+
+int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_comp, uint32_t* emit,
+                   cudaStream_t st) {
+  TcArgs a{};
+  a.planes = planes;
+  a.plane_words = (int64_t(1) << n) >> 5;
+  a.v_first = v_first;
+  a.n_comp = n_comp;
+  a.n_items = n_comp << (n - 16);
+  a.n_full = n;
+  a.emit = emit;
+  return run_tc_hybrid<true>(a, a.n_items, st);
 }
 
 }  // namespace sbw
