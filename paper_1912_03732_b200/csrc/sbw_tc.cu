@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     const int mt = tid - 128, mw = mt >> 5;  // transform thread / warp index
     const int c = mt;                        // generation row
     const uint32_t* __restrict__ planes = a.planes;
-    const int64_t pw = a.plane_words;
+    const int64_t pw = EMIT ? a.plane_words : 2048;
     GenState16 gs;
 #pragma unroll
     for (int k = 0; k < 8; ++k) gs.g[k] = 0;
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     for (int k = 0; k < 2 && k < n_my; ++k) {
       uint32_t vn, bpn;
       item_at<EMIT>(a, t_lo + k, vn, bpn);
-      if (bpn != gs.bpcur) {
+      if (EMIT && bpn != gs.bpcur) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) gs.g[q] = 0;
         gs.vcur = 0;
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
       uint4 pa = make_uint4(0, 0, 0, 0), pb = pa;
       if (gen) {
         item_at<EMIT>(a, t_lo + i + 2, vn, bpn);
-        reset = bpn != gs.bpcur;
+        reset = EMIT && bpn != gs.bpcur;
         d = reset ? vn : (gs.vcur ^ vn);
         if (d) {
           const uint4* p =
