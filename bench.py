@@ -270,9 +270,17 @@ def run_ours(args, rank, world, local_rank):
         assert (res[0], res[1]) == (31942, 44828), res
 
     # ---- e2e through the C ABI with host buffers (sbw_nl_host) ------------
+    # The caller's table and result buffers are page-locked once
+    # (cudaHostRegister), as a repeated caller would: sbw_nl_host then DMAs
+    # them directly, every step, inside the timed region.
     h_nl = np.empty(nmask, dtype=np.int64)
     out3 = np.empty(3, dtype=np.int64)
     table_host = np.ascontiguousarray(s.table)
+    cudart = torch.cuda.cudart()
+    registered = []
+    for arr in (table_host, h_nl):
+        if int(cudart.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)) == 0:
+            registered.append(arr)
     for _ in range(2):
         d.check(lib.sbw_nl_host(table_host.ctypes.data, n, m, v_lo, v_hi, h_nl.ctypes.data,
                                 out3.ctypes.data, local_rank))
@@ -287,6 +295,8 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t[0])
     assert np.array_equal(h_nl, nl.cpu().numpy())
+    for arr in registered:
+        cudart.cudaHostUnregister(arr.ctypes.data)
 
     # ---- roofline of the dominant kernel (fused NL) ----------------------
     peak = live_peak(lib, d, "sbw_int32_peak")
@@ -378,9 +388,10 @@ def run_ours(args, rank, world, local_rank):
         "result": check,
         "roofline": roofline,
         "e2e": {"value": coeffs(n, m, nmask) * world * args.steps / e2e_s, "unit": "coeff/s",
-                "h2d_bytes_per_step": int(table_host.nbytes),
+                "h2d_bytes_per_step": int(table_host.nbytes),  # uint32 table
                 "d2h_bytes_per_step": int(h_nl.nbytes + 8 * 4),
-                "path": "sbw_nl_host C ABI (host table in, host NL out), wall clock"},
+                "path": "sbw_nl_host C ABI (host table in, host NL out, page-locked caller "
+                        "buffers), wall clock"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

@@ -148,7 +148,9 @@ int sbw_nl_bruteforce(const void* d_table, int table_bytes, int n, int m, int32_
  * Host-buffer end-to-end call (what a plugin binding makes): copies the
  * uint32 table host->device, runs sbw_nl over [v_lo, v_hi) on `device`,
  * copies per-component NL (int64) device->host and returns
- * out3 = {NL value, argmin_v, max|W|}.  Synchronous.
+ * out3 = {NL value, argmin_v, max|W|}.  Synchronous.  Page-locked h_table /
+ * h_nl (cudaHostRegister, cudaMallocHost) are DMA'd directly; pageable ones
+ * are staged through an internal pinned buffer.
  */
 int sbw_nl_host(const uint32_t* h_table, int n, int m, uint32_t v_lo, uint32_t v_hi,
                 int64_t* h_nl, int64_t* out3, int device);

@@ -294,7 +294,7 @@ int sbw_nl_host(const uint32_t* h_table, int n, int m, uint32_t v_lo, uint32_t v
   cudaStream_t st = ws.st;
   const int64_t nx = int64_t(1) << n, nv = int64_t(v_hi) - int64_t(v_lo);
   const int tb = m <= 16 ? 2 : 4;
-  const size_t tbl = align_up(size_t(nx) * tb), mxb = align_up(sizeof(int32_t) * nv),
+  const size_t tbl = align_up(size_t(nx) * 4), mxb = align_up(sizeof(int32_t) * nv),
                nlb = align_up(sizeof(int64_t) * nv), small = 256;
   const size_t sb = nl_scratch_bytes(n, m, v_lo, v_hi);
   const size_t dneed = tbl + mxb + nlb + 2 * small + sb;
@@ -323,25 +323,44 @@ int sbw_nl_host(const uint32_t* h_table, int n, int m, uint32_t v_lo, uint32_t v
   char* h = static_cast<char*>(ws.h_stage);
   long long* h_bad = reinterpret_cast<long long*>(h + (tbl > nlb ? tbl : nlb));
   unsigned long long* h_key = reinterpret_cast<unsigned long long*>(h_bad + 32);
-  // narrow the caller's uint32 table into pinned staging, then one H2D copy
-  if (tb == 2) {
+  // Page-locked caller buffers (cudaHostRegister / cudaMallocHost) are
+  // copied to and from directly; pageable ones go through the pinned staging.
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();  // clear the sticky-free error of an unknown pointer
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool tbl_pinned = pinned(h_table), nl_pinned = h_nl != nullptr && pinned(h_nl);
+  int tbw = tb;
+  if (tbl_pinned) {
+    // uint32 straight from the caller; sbw_nl reads 4-byte tables too
+    tbw = 4;
+    if (size_t(nx) * 4 > tbl) return set_error(SBW_EINVAL, "table workspace too small");
+    SBW_CUDA_CHECK(cudaMemcpyAsync(d_table, h_table, size_t(nx) * 4, cudaMemcpyHostToDevice, st));
+  } else if (tb == 2) {
+    // narrow the caller's uint32 table into pinned staging, then one H2D copy
     uint16_t* s16 = reinterpret_cast<uint16_t*>(h);
     for (int64_t i = 0; i < nx; ++i) s16[i] = uint16_t(h_table[i]);
+    SBW_CUDA_CHECK(cudaMemcpyAsync(d_table, h, size_t(nx) * tb, cudaMemcpyHostToDevice, st));
   } else {
     memcpy(h, h_table, size_t(nx) * 4);
+    SBW_CUDA_CHECK(cudaMemcpyAsync(d_table, h, size_t(nx) * tb, cudaMemcpyHostToDevice, st));
   }
-  SBW_CUDA_CHECK(cudaMemcpyAsync(d_table, h, size_t(nx) * tb, cudaMemcpyHostToDevice, st));
   SBW_CUDA_CHECK(cudaMemsetAsync(d_key, 0, sizeof(unsigned long long), st));
-  if (int rc = sbw_nl(d_table, tb, n, m, v_lo, v_hi, d_mx, d_key, scratch, sb, st)) return rc;
+  if (int rc = sbw_nl(d_table, tbw, n, m, v_lo, v_hi, d_mx, d_key, scratch, sb, st)) return rc;
   if (int rc = sbw_maxabs_to_nl(d_mx, nv, n, d_nl, d_bad, st)) return rc;
   // the staging buffer is reused for the results once the table copy is done
-  SBW_CUDA_CHECK(cudaMemcpyAsync(h, d_nl, sizeof(int64_t) * nv, cudaMemcpyDeviceToHost, st));
+  int64_t* nl_dst = nl_pinned ? h_nl : reinterpret_cast<int64_t*>(h);
+  SBW_CUDA_CHECK(cudaMemcpyAsync(nl_dst, d_nl, sizeof(int64_t) * nv, cudaMemcpyDeviceToHost, st));
   SBW_CUDA_CHECK(cudaMemcpyAsync(h_bad, d_bad, sizeof(long long), cudaMemcpyDeviceToHost, st));
   SBW_CUDA_CHECK(cudaMemcpyAsync(h_key, d_key, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   SBW_CUDA_CHECK(cudaStreamSynchronize(st));
   if (*h_bad != LLONG_MAX)
     return set_error(SBW_EPARITY, "odd spectrum gap at mask %lld", (long long)(v_lo + *h_bad));
-  if (h_nl) memcpy(h_nl, h, sizeof(int64_t) * nv);
+  if (h_nl && !nl_pinned) memcpy(h_nl, h, sizeof(int64_t) * nv);
   if (out3) {
     const int64_t mxw = int64_t(*h_key >> 32);
     out3[0] = (nx - mxw) >> 1;

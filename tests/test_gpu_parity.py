@@ -5,6 +5,8 @@ pkg/tests/test_walsh.py, test_nonlinearity.py, test_parallel.py,
 test_acceptance.py (known answers, 250-box equivalence, Parseval,
 determinism across worker counts, stream accounting).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -422,6 +424,34 @@ def test_sbw_nl_host_entry_point():
     assert out3.tolist() == [1872, 3572, 352]
     assert np.array_equal(nl, orc.component_nl(s.table, 12, 1, 4096))
     del ctypes
+
+
+@pytest.mark.parametrize("pin_table,pin_nl", [(True, True), (True, False), (False, True)])
+def test_sbw_nl_host_page_locked_buffers(pin_table, pin_nl):
+    """Page-locked caller buffers take the direct-DMA branch of sbw_nl_host
+    (uint32 table straight to the device, NL straight into the caller's array)."""
+    import torch
+
+    import paper_1912_03732_b200.device as d
+
+    s = box("16x16")
+    table = np.ascontiguousarray(s.table)
+    nl = np.zeros(65535, dtype=np.int64)
+    out3 = np.empty(3, dtype=np.int64)
+    cudart = torch.cuda.cudart()
+    regs = [a for a, p in ((table, pin_table), (nl, pin_nl)) if p]
+    for a in regs:
+        assert int(cudart.cudaHostRegister(a.ctypes.data, a.nbytes, 0)) == 0
+    try:
+        d.check(d.load_library().sbw_nl_host(table.ctypes.data, 16, 16, 1, 65536, nl.ctypes.data,
+                                             out3.ctypes.data, 0))
+    finally:
+        for a in regs:
+            cudart.cudaHostUnregister(a.ctypes.data)
+    assert out3.tolist() == [31942, 44828, 1652]
+    # the reference's ColumnMaxima.values for 16x16 are the per-component NLs
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_arrays.npz"))["maxima_16x16"]
+    assert np.array_equal(nl, g.astype(np.int64))
 
 
 def test_distributed_single_rank_nccl():
