@@ -301,22 +301,51 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
       // TMEM -> registers: two pairs of 64-column loads, two waits; TMEM is
       // released before any of the stages run.  R[j] holds c = 2j, 2j+1.
       uint32_t R[128];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      {
         uint32_t t0[64], t1[64];
-        tc::tmem_ld_x64(tbase + h * 128, t0);
-        tc::tmem_ld_x64(tbase + h * 128 + 64, t1);
+        tc::tmem_ld_x64(tbase, t0);
+        tc::tmem_ld_x64(tbase + 64, t1);
         tc::wait_ld_tied(t0);
         tc::wait_ld_tied(t1);
         // c bit 0 stage + packing: biased lanes (a + b + 256, a - b + 256)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          R[64 * h + j] = t0[2 * j] * 0x10001u + t0[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
-          R[64 * h + 32 + j] = t1[2 * j] * 0x10001u + t1[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
+          R[j] = t0[2 * j] * 0x10001u + t0[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
+          R[32 + j] = t1[2 * j] * 0x10001u + t1[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
         }
       }
-      tc::fence_before();
-      mbar_arrive(&bar_tmem_empty);
+      {
+        uint32_t t2[64], t3[64];
+        tc::tmem_ld_x64(tbase + 128, t2);
+        tc::tmem_ld_x64(tbase + 192, t3);
+        tc::wait_ld_tied(t2);
+        tc::wait_ld_tied(t3);
+        tc::fence_before();
+        mbar_arrive(&bar_tmem_empty);
+        // The second packing (IMAD, FMA pipe) shares its basic block with the
+        // byte expansion of item i+2 (LOP3/SHF, ALU pipe), so the two
+        // half-rate streams interleave.  B buffer i & 1 was released by MMA(i).
+        if (gen) {
+          if (reset) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) gs.g[q] = 0;
+            gs.bpcur = bpn;
+          }
+          xor_plane(gs.g, pa, pb);
+          if (d) xor_all(d, bpn);  // rare: more than one changed bit
+          gs.vcur = vn;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          R[64 + j] = t2[2 * j] * 0x10001u + t2[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
+          R[96 + j] = t3[2 * j] * 0x10001u + t3[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
+        }
+        if (gen) {
+          store_row(gs.g, smem + kBOff + (i & 1) * kBBytes, c);
+          tc::fence_proxy_async();
+          mbar_arrive(&bar_bfull[i & 1]);
+        }
+      }
       // c bits 1..6 (stages 9..14)
 #pragma unroll
       for (int sb = 0; sb < 6; ++sb)
@@ -363,19 +392,6 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         }
         const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<16>(mx, mn)));
         if (lane == 0) s_wmax[i & 3][mw] = m;
-      }
-      if (gen) {
-        if (reset) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) gs.g[q] = 0;
-          gs.bpcur = bpn;
-        }
-        xor_plane(gs.g, pa, pb);
-        xor_all(d, bpn);  // rare: more than one changed bit
-        gs.vcur = vn;
-        store_row(gs.g, smem + kBOff + (i & 1) * kBBytes, c);
-        tc::fence_proxy_async();
-        mbar_arrive(&bar_bfull[i & 1]);
       }
     }
     tc::fence_before();
