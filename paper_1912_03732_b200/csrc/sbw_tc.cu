@@ -49,17 +49,41 @@
 namespace sbw {
 namespace {
 
+#ifndef SBW_TC_C0MMA
+#define SBW_TC_C0MMA 1
+#endif
+// SBW_TC_C0MMA: the c-bit-0 butterfly also runs in the GEMM (B rows
+// b_2j + b_2j+1 and b_2j - b_2j+1 + 1, a bias K block, .pack::16b loads);
+// otherwise B rows are plain bits and the transform warps pack with IMADs.
+constexpr bool kC0Mma = SBW_TC_C0MMA != 0;
 constexpr int kMathWarps = 8;
-constexpr int kAOff = 0;                       // A = -H_256, 256 x 256 s8
-constexpr int kBOff = kAOff + 256 * 256;       // 2 x (256 x 256) generated B operands
+constexpr int kKA = kC0Mma ? 288 : 256;        // K of A: 256 (r) [+ 32 bias block]
+constexpr int kAHalf = 128 * kKA;              // one M = 128 half of A
+constexpr int kAOff = 0;                       // A = -H_256 [| bias], 256 x kKA s8
+constexpr int kBbOff = kAOff + 2 * kAHalf;     // bias block of B (C0MMA), 256 x 32
+constexpr int kBOff = kBbOff + (kC0Mma ? 256 * 32 : 0);  // 2 x (256 x 256) generated B
 constexpr int kBBytes = 256 * 256;
-constexpr int kTcSmem = kBOff + 2 * kBBytes;   // 196608 bytes
+constexpr int kTcSmem = kBOff + 2 * kBBytes;   // 212992 (C0MMA) / 196608 bytes
 constexpr uint32_t kIdesc = tc::idesc_i8(128, 256, /*A s8*/ true, /*B u8*/ false);
+static_assert(kBOff % 1024 == 0, "SW128 B atoms need 1024-byte alignment");
 
 // K position of bit r inside its 32-bit plane word after the byte expansion
 // (w >> k) & 0x01010101 (k = 0..7): element r = 32 j + 8 jb + k lands at
 // byte 32 j + 4 k + jb.  A's columns carry the same permutation.
 __device__ __forceinline__ int r_of_p(int p) { return (p & ~31) | ((p & 3) << 3) | ((p >> 2) & 7); }
+
+// A[u][p]: -H[u][r(p)] for p < 256.  Bias block (C0MMA, against B's all-ones
+// bias columns 0..5): +256 on every row (columns 0..2) and +256 more on row
+// u = 0 (columns 3..5).  That makes every D entry the biased s = W_9/2 + 2^8:
+// the polarity 1 - 2b puts +2^8 on row 0's sums, and the diff rows' "+1"
+// (b0 - b1 + 1, to stay unsigned) costs -sum_r H[u][r] = -256 [u = 0].
+__device__ __forceinline__ int a_value(int u, int p) {
+  if (p < 256) return (__popc(u & r_of_p(p)) & 1) ? 1 : -1;
+  const int k = p - 256;
+  if (k < 3) return k < 2 ? 127 : 2;
+  if (k < 6) return u == 0 ? (k < 5 ? 127 : 2) : 0;
+  return 0;
+}
 
 __device__ __forceinline__ uint32_t mask_at(int64_t q, uint32_t v_lo, uint32_t v_hi) {
   const int64_t b = q & ~int64_t(255);
@@ -76,7 +100,7 @@ __device__ __forceinline__ void xor_plane(uint32_t (&g)[8], const uint4& a, cons
 }
 
 // Expand the 256 bits of row c into the u8 B operand (K-major core matrices).
-__device__ __forceinline__ void store_row(const uint32_t (&g)[8], uint8_t* bbuf, int c) {
+[[maybe_unused]] __device__ __forceinline__ void store_row(const uint32_t (&g)[8], uint8_t* bbuf, int c) {
   uint8_t* row = bbuf + (c >> 3) * 2048 + (c & 7) * 16;
   constexpr uint32_t M = 0x01010101u;
 #pragma unroll
@@ -89,6 +113,38 @@ __device__ __forceinline__ void store_row(const uint32_t (&g)[8], uint8_t* bbuf,
   }
 }
 
+// C0MMA generation: thread (j, kh) owns K half kh (= SW128 atom column kh)
+// of rows 2j and 2j+1: g[0..3] = row 2j's plane words 4kh..4kh+3, g[4..7] =
+// row 2j+1's.  Sum row 2j: b0 + b1; diff row 2j+1: b0 - b1 + 1 (u8).
+// SW128 layout: atom (kh, g8 = n >> 3) at (kh * 32 + g8) * 1024, row i = n & 7
+// at i * 128, logical chunk c at chunk c ^ i.  The two K halves of a row pair
+// write chunks 2w + kh first and 2w + 1 - kh second, so the 8 threads of a
+// store phase hit 8 different 16-byte bank groups.
+__device__ __forceinline__ void store_rows_sw128(const uint32_t (&g)[8], uint8_t* bbuf, int j, int kh) {
+  const int i0 = (2 * j) & 7;
+  uint8_t* a0 = bbuf + (kh * 32 + (j >> 2)) * 1024 + i0 * 128;  // row 2j (sum)
+  uint8_t* a1 = a0 + 128;                                          // row 2j+1 (diff)
+  constexpr uint32_t M = 0x01010101u;
+  const int s4 = 4 * kh;  // first chunk holds bits 0..3 (kh = 0) or 4..7 (kh = 1)
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      uint32_t sv[4], dv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = (4 * half + q) ^ s4;
+        const uint32_t b0 = (g[w] >> k) & M, b1 = (g[4 + w] >> k) & M;
+        sv[q] = b0 + b1;
+        dv[q] = b0 + M - b1;  // per byte in {0, 1, 2}: no borrow
+      }
+      const int c = 2 * w + (half ^ kh);  // logical chunk of this store
+      *reinterpret_cast<uint4*>(a0 + ((c ^ i0) << 4)) = make_uint4(sv[0], sv[1], sv[2], sv[3]);
+      *reinterpret_cast<uint4*>(a1 + ((c ^ (i0 + 1)) << 4)) = make_uint4(dv[0], dv[1], dv[2], dv[3]);
+    }
+  }
+}
+
 __device__ __forceinline__ void publish(const uint32_t* wmax, uint32_t v, uint32_t v_lo,
                                         int32_t* max_abs, unsigned long long* key) {
   const uint4 a = *reinterpret_cast<const uint4*>(wmax);
@@ -98,18 +154,24 @@ __device__ __forceinline__ void publish(const uint32_t* wmax, uint32_t v, uint32
   if (key) atomicMax(key, nl_key(m, v));
 }
 
-// MMA chain of one mask (2 M-halves x 8 K blocks), issued by a converged warp.
-// Descriptors differ only in the start-address field (bits 0..13, smem < 256 KiB,
-// no carry), so they are one base plus a compile-time offset each.
+// MMA chain of one mask (2 M-halves x 8 (+1 bias) K blocks), issued by a
+// converged warp.  Descriptors differ only in the start-address field (bits
+// 0..13, smem < 256 KiB, no carry): one base plus a compile-time offset each.
 __device__ __forceinline__ void issue_mma_warp(uint32_t tmem, const uint8_t* smem, int buf, uint64_t* bar) {
-  const uint64_t da0 = tc::sdesc(tc::smem_u32(smem + kAOff), 128, 2048);
-  const uint64_t db0 = tc::sdesc(tc::smem_u32(smem + kBOff + buf * kBBytes), 128, 2048);
+  const uint64_t da0 = tc::sdesc(tc::smem_u32(smem + kAOff), 128, kKA / 16 * 128);
+  const uint32_t b0 = tc::smem_u32(smem + kBOff + buf * kBBytes);
+  const uint64_t db0 = kC0Mma ? tc::sdesc_sw128(b0, 1024) : tc::sdesc(b0, 128, 2048);
+  const uint64_t dbb = tc::sdesc(tc::smem_u32(smem + kBbOff), 128, 256);
 #pragma unroll
   for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int kb = 0; kb < 8; ++kb)
-      tc::mma_i8_elect(tmem + h * 256, da0 + uint64_t((h * 32768 + kb * 256) >> 4), db0 + uint64_t(kb * 16),
-                       kIdesc, kb > 0 ? 1u : 0u);
+    for (int kb = 0; kb < (kC0Mma ? 9 : 8); ++kb) {
+      // SW128: K block kb = atom column kb >> 2 (32 KiB apart), 32 B steps inside
+      const uint64_t db = kb == 8 ? dbb
+                                  : db0 + uint64_t(kC0Mma ? ((kb >> 2) * 32768 + (kb & 3) * 32) >> 4 : kb * 16);
+      tc::mma_i8_elect(tmem + h * 256, da0 + uint64_t((h * kAHalf + kb * 256) >> 4), db, kIdesc,
+                       kb > 0 ? 1u : 0u);
+    }
   tc::mma_commit_elect(bar);
 }
 
@@ -179,20 +241,27 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
   const int64_t t_lo = total * blockIdx.x / gridDim.x;
   const int n_my = int(total * (blockIdx.x + 1) / gridDim.x - t_lo);
 
-  // A = -H_256 with the K permutation of store_row
-  for (int e = tid; e < 256 * 16; e += kAllThreads) {
-    const int u = e >> 4, pc = e & 15;
+  // constant operands: A (with the K permutation of the byte expansion) and,
+  // for C0MMA, B's bias block (columns 0..5 = 1 on every row)
+  for (int e = tid; e < 256 * (kKA / 16); e += kAllThreads) {
+    const int uu = e / (kKA / 16), pc = e % (kKA / 16);
     uint32_t wv[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       uint32_t x = 0;
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
-        x |= ((__popc(u & r_of_p(pc * 16 + q * 4 + b)) & 1) ? 0x01u : 0xFFu) << (8 * b);
+      for (int b = 0; b < 4; ++b) x |= uint32_t(uint8_t(a_value(uu, pc * 16 + q * 4 + b))) << (8 * b);
       wv[q] = x;
     }
-    *reinterpret_cast<uint4*>(smem + kAOff + ((u >> 3) * 16 + pc) * 128 + (u & 7) * 16) =
+    *reinterpret_cast<uint4*>(smem + kAOff + ((uu >> 3) * (kKA / 16) + pc) * 128 + (uu & 7) * 16) =
         make_uint4(wv[0], wv[1], wv[2], wv[3]);
+  }
+  if constexpr (kC0Mma) {
+    for (int n = tid; n < 256; n += kAllThreads) {
+      uint8_t* row = smem + kBbOff + (n >> 3) * 256 + (n & 7) * 16;
+      *reinterpret_cast<uint4*>(row) = make_uint4(0x01010101u, 0x00000101u, 0u, 0u);
+      *reinterpret_cast<uint4*>(row + 128) = make_uint4(0u, 0u, 0u, 0u);
+    }
   }
   if (warp == 0) tc::tmem_alloc(&tmem_slot, 512);
   if (tid == 0) {
@@ -241,7 +310,8 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     // ---------------- transform warps ----------------
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kMathRegs));
     const int mt = tid - 128, mw = mt >> 5;  // transform thread / warp index
-    const int c = mt;                        // generation row
+    const int c = mt;                        // generation row (plain B rows)
+    const int gj = mt >> 1, gkh = mt & 1;    // C0MMA: row pair, K half
     const uint32_t* __restrict__ planes = a.planes;
     const int64_t pw = EMIT ? a.plane_words : 2048;
     GenState16 gs;
@@ -249,15 +319,31 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     for (int k = 0; k < 8; ++k) gs.g[k] = 0;
     gs.vcur = 0;
     gs.bpcur = 0;
-    // rows c of block bp start at plane word bp * 2048 + 8 c
-    auto row_off = [&](uint32_t bp) { return int64_t(bp) * 2048 + c * 8; };
+    // plane words of this thread's generation state in block bp: row c's 8
+    // words at bp * 2048 + 8 c, or (C0MMA) 4 words of row 2j and 4 of row
+    // 2j+1 at bp * 2048 + 16 j + 4 kh (+ 8)
+    auto row_off = [&](uint32_t bp) {
+      return int64_t(bp) * 2048 + (kC0Mma ? 16 * gj + 4 * gkh : c * 8);
+    };
+    auto load_pl = [&](int i, uint32_t bp, uint4& x, uint4& y) {
+      const uint4* p = reinterpret_cast<const uint4*>(planes + int64_t(i) * pw + row_off(bp));
+      x = __ldg(p);
+      y = __ldg(p + (kC0Mma ? 2 : 1));
+    };
     auto xor_all = [&](uint32_t d, uint32_t bp) {
       while (d) {
         const int i = __ffs(d) - 1;
         d &= d - 1;
-        const uint4* p = reinterpret_cast<const uint4*>(planes + int64_t(i) * pw + row_off(bp));
-        xor_plane(gs.g, __ldg(p), __ldg(p + 1));
+        uint4 x, y;
+        load_pl(i, bp, x, y);
+        xor_plane(gs.g, x, y);
       }
+    };
+    auto store_b = [&](int buf) {
+      if constexpr (kC0Mma)
+        store_rows_sw128(gs.g, smem + kBOff + buf * kBBytes, gj, gkh);
+      else
+        store_row(gs.g, smem + kBOff + buf * kBBytes, c);
     };
     for (int k = 0; k < 2 && k < n_my; ++k) {
       uint32_t vn, bpn;
@@ -270,7 +356,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
       }
       xor_all(gs.vcur ^ vn, bpn);
       gs.vcur = vn;
-      store_row(gs.g, smem + kBOff + k * kBBytes, c);
+      store_b(k);
       tc::fence_proxy_async();
       mbar_arrive(&bar_bfull[k]);
     }
@@ -289,42 +375,14 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         reset = EMIT && bpn != gs.bpcur;
         d = reset ? vn : (gs.vcur ^ vn);
         if (d) {
-          const uint4* p =
-              reinterpret_cast<const uint4*>(planes + int64_t(__ffs(d) - 1) * pw + row_off(bpn));
-          pa = __ldg(p);
-          pb = __ldg(p + 1);
+          load_pl(__ffs(d) - 1, bpn, pa, pb);
           d &= d - 1;
         }
       }
       tc::mbar_wait(&bar_full, uint32_t(i & 1));
       tc::fence_after();
-      // TMEM -> registers: two pairs of 64-column loads, two waits; TMEM is
-      // released before any of the stages run.  R[j] holds c = 2j, 2j+1.
       uint32_t R[128];
-      {
-        uint32_t t0[64], t1[64];
-        tc::tmem_ld_x64(tbase, t0);
-        tc::tmem_ld_x64(tbase + 64, t1);
-        tc::wait_ld_tied(t0);
-        tc::wait_ld_tied(t1);
-        // c bit 0 stage + packing: biased lanes (a + b + 256, a - b + 256)
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          R[j] = t0[2 * j] * 0x10001u + t0[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
-          R[32 + j] = t1[2 * j] * 0x10001u + t1[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
-        }
-      }
-      {
-        uint32_t t2[64], t3[64];
-        tc::tmem_ld_x64(tbase + 128, t2);
-        tc::tmem_ld_x64(tbase + 192, t3);
-        tc::wait_ld_tied(t2);
-        tc::wait_ld_tied(t3);
-        tc::fence_before();
-        mbar_arrive(&bar_tmem_empty);
-        // The second packing (IMAD, FMA pipe) shares its basic block with the
-        // byte expansion of item i+2 (LOP3/SHF, ALU pipe), so the two
-        // half-rate streams interleave.  B buffer i & 1 was released by MMA(i).
+      auto gen_update = [&]() {
         if (gen) {
           if (reset) {
 #pragma unroll
@@ -335,16 +393,60 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
           if (d) xor_all(d, bpn);  // rare: more than one changed bit
           gs.vcur = vn;
         }
+      };
+      auto gen_store = [&]() {
+        if (gen) {
+          store_b(i & 1);  // buffer i & 1 was released by MMA(i)
+          tc::fence_proxy_async();
+          mbar_arrive(&bar_bfull[i & 1]);
+        }
+      };
+      if constexpr (kC0Mma) {
+        // TMEM -> registers already packed: R[j] = lanes (c = 2j sum, diff),
+        // biased s = W_9 / 2 + 2^8 straight from the GEMM
+        uint32_t(&R0)[64] = *reinterpret_cast<uint32_t(*)[64]>(&R[0]);
+        uint32_t(&R1)[64] = *reinterpret_cast<uint32_t(*)[64]>(&R[64]);
+        tc::tmem_ld_x64_p16(tbase, R0);
+        tc::tmem_ld_x64_p16(tbase + 128, R1);
+        tc::wait_ld_tied(R0);
+        tc::wait_ld_tied(R1);
+        tc::fence_before();
+        mbar_arrive(&bar_tmem_empty);
+        gen_update();
+        gen_store();
+      } else {
+        // TMEM -> registers: two pairs of 64-column loads, two waits; TMEM is
+        // released before any of the stages run.  R[j] holds c = 2j, 2j+1.
+        {
+          uint32_t t0[64], t1[64];
+          tc::tmem_ld_x64(tbase, t0);
+          tc::tmem_ld_x64(tbase + 64, t1);
+          tc::wait_ld_tied(t0);
+          tc::wait_ld_tied(t1);
+          // c bit 0 stage + packing: biased lanes (a + b + 256, a - b + 256)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            R[j] = t0[2 * j] * 0x10001u + t0[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
+            R[32 + j] = t1[2 * j] * 0x10001u + t1[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
+          }
+        }
+        uint32_t t2[64], t3[64];
+        tc::tmem_ld_x64(tbase + 128, t2);
+        tc::tmem_ld_x64(tbase + 192, t3);
+        tc::wait_ld_tied(t2);
+        tc::wait_ld_tied(t3);
+        tc::fence_before();
+        mbar_arrive(&bar_tmem_empty);
+        // The second packing (IMAD, FMA pipe) shares its basic block with the
+        // byte expansion of item i+2 (LOP3/SHF, ALU pipe), so the two
+        // half-rate streams interleave.
+        gen_update();
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           R[64 + j] = t2[2 * j] * 0x10001u + t2[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
           R[96 + j] = t3[2 * j] * 0x10001u + t3[2 * j + 1] * 0xFFFF0001u + 0x01000100u;
         }
-        if (gen) {
-          store_row(gs.g, smem + kBOff + (i & 1) * kBBytes, c);
-          tc::fence_proxy_async();
-          mbar_arrive(&bar_bfull[i & 1]);
-        }
+        gen_store();
       }
       // c bits 1..6 (stages 9..14)
 #pragma unroll
@@ -362,7 +464,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         // the lo lane of R[0] / R[64] (-128 x 128 columns).  Block word layout
         // (pass B only pairs equal positions across blocks):
         //   word (j >> 2) * 1024 + 4 u + (j & 3)  <-  R[64 h + j]
-        if (u == 0) {
+        if (!kC0Mma && u == 0) {
           R[0] += 0x4000u;
           R[64] += 0x4000u;
         }
@@ -380,7 +482,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
       } else {
         // c bit 7 (stage 15, top) fused with the max/min fold (carry argument:
         // tile_last_pass); the row u = 0 offset reaches only S of k = 0
-        const uint32_t corr0 = (u == 0) ? 0x8000u : 0u;
+        const uint32_t corr0 = (!kC0Mma && u == 0) ? 0x8000u : 0u;
         uint32_t mx = 0u, mn = 0xFFFFFFFFu;
 #pragma unroll
         for (int k = 0; k < 64; ++k) {

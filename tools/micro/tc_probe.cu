@@ -160,6 +160,56 @@ __global__ void __launch_bounds__(128) k_mma_i8(const int8_t* A, const uint8_t* 
   if (warp == 0) tmem_dealloc(tm, 256);
 }
 
+// B operand in K-major SWIZZLE_128B layout: atoms of 8 rows x 128 B,
+// chunk c of row i at c ^ i; atom (ka, g) at (ka * 32 + g) * 1024.
+__device__ __forceinline__ uint32_t sw128_off(int n, int k) {
+  const int ka = k >> 7, g = n >> 3, i = n & 7, c = (k & 127) >> 4;
+  return uint32_t((ka * 32 + g) * 1024 + i * 128 + ((c ^ i) << 4) + (k & 15));
+}
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t sbo) {
+  return uint64_t((saddr & 0x3FFFFu) >> 4) | (uint64_t(1) << 16) | (uint64_t((sbo >> 4) & 0x3FFFu) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+__global__ void __launch_bounds__(128) k_mma_i8_sw128(const int8_t* A, const uint8_t* B, int32_t* D) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* sA = sm;                  // 32 KiB, no swizzle
+  uint8_t* sB = sm + 32768;          // 64 KiB, SW128 (1024-aligned)
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 128 * 256; i += 128) sA[kmaj_off(i >> 8, i & 255)] = uint8_t(A[i]);
+  for (int i = tid; i < 256 * 256; i += 128) sB[sw128_off(i >> 8, i & 255)] = B[i];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 0) tmem_alloc(&slot, 256);
+  if (tid == 0) mbar_init(&bar, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = slot;
+  if (tid == 0) {
+#pragma unroll
+    for (int kb = 0; kb < 8; ++kb)
+      mma_i8(tm, sdesc(smem_u32(sA) + kb * 256, 128, 2048),
+             sdesc_sw128(smem_u32(sB) + (kb >> 2) * 32768 + (kb & 3) * 32, 1024), idesc_i8(128, 256, 1, 0),
+             kb ? 1u : 0u);
+    mma_commit(&bar);
+  }
+  __syncwarp();
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  const uint32_t lane_off = uint32_t(warp * 32) << 16;
+  for (int c = 0; c < 256; c += 64) {
+    uint32_t r[64];
+    tmem_ld_x64(tm + lane_off + c, r);
+    tmem_wait_ld();
+    for (int j = 0; j < 64; ++j) D[(warp * 32 + (tid & 31)) * 256 + c + j] = int32_t(r[j]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tm, 256);
+}
+
 // MMA chain time while other warps stream STS.128 (MODE 1) / LDS.128 (MODE 2) / nothing (0)
 template <int MODE>
 __global__ void __launch_bounds__(256) k_mma_contention(int reps, unsigned long long* cycles, uint32_t* sink) {
@@ -273,6 +323,21 @@ int main() {
       }
     }
   printf("mma_i8 128x256x256 correctness: %ld mismatches\n", bad);
+
+  // 2b. SW128 B operand
+  CK(cudaFuncSetAttribute(k_mma_i8_sw128, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CK(cudaMemset(dD, 0, 128 * 256 * 4));
+  k_mma_i8_sw128<<<1, 128, smem>>>(dA, dB, dD);
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
+  bad = 0;
+  for (int m = 0; m < 128; ++m)
+    for (int n = 0; n < 256; ++n) {
+      int32_t ref = 0;
+      for (int k = 0; k < 256; ++k) ref += int32_t(A[m * 256 + k]) * int32_t(B[n * 256 + k]);
+      if (ref != D[m * 256 + n]) ++bad;
+    }
+  printf("mma_i8 SW128 B correctness: %ld mismatches\n", bad);
 
   // 3. MMA throughput: all SMs, reps chains of 8 K=32 MMAs
   for (int reps : {64, 512}) {
