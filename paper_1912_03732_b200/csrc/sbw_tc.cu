@@ -1,43 +1,45 @@
-// Tensor-core + packed-integer hybrid kernel for the n = 16 nonlinearity path.
+// Tensor-core + packed-integer hybrid kernel k_tc_hybrid<EMIT>:
+//   EMIT = false: the n = 16 nonlinearity path (sbw_nl), K2 in DESIGN.md;
+//   EMIT = true : pass A of the multi-pass path (n = 17..24), 15 stages per
+//                 2^15 block, biased u16 out for pass B (sbw_passb.cuh).
 //
 // Replaces, per output mask v, polarity_row (sbox.py:145-152) +
 // fwht_column_in_place (walsh.py:73-104) + column_nonlinearity
-// (walsh.py:107-114), like k_tile_simd, but splits the 16 butterfly stages:
+// (walsh.py:107-114), like k_tile_simd, with the 16 butterfly stages of a
+// 2^16-element item split as x = c * 256 + r (r = x bits 0..7, c = bits 8..15,
+// c = 2 j + c0):
 //
-//   x = c * 256 + r  (r = x bits 0..7, c = x bits 8..15).
+//   GEMM (stages over r and c0).  With b_c[r] = g_v(c * 256 + r) in {0, 1}
+//   (bit planes -> bytes, straight into shared memory), the B operand (u8)
+//   has rows B[2j] = b_2j + b_2j+1 and B[2j+1] = b_2j - b_2j+1 + 1 (the c0
+//   butterfly, kept unsigned), A = -H_256 (s8), and a 9th K block adds a bias
+//   against constant all-ones B columns, so that
+//     D[u][2j + e] = W_9 / 2 + 2^8   in [0, 512]
+//   exactly -- the biased "s = W/2 + 2^(k-1) after k stages" form of
+//   sbw_tile_simd.cuh, row u = 0 included.  tcgen05.mma.kind::i8, M = 128,
+//   N = 256, K = 32; 2 M-halves x 9 K blocks; s32 accumulators fill all 512
+//   TMEM columns.  B is K-major SWIZZLE_128B; A and B's bias block are
+//   K-major without swizzle (layouts validated in tools/micro/tc_probe.cu).
 //
-//   Stages over r (8 of them) are one int8 GEMM on the 5th-gen tensor cores:
-//     t[u][c] = - sum_r H[u][r] * B[c][r]
-//   with B[c][r] = g_v(c * 256 + r) in {0, 1} (u8, generated from bit planes
-//   straight into shared memory) and A = -H_256 (s8).  Since the polarity is
-//   1 - 2 B, t = W_8 / 2 exactly (half the 8-stage partial transform), except
-//   on row u = 0 where t = W_8 / 2 - 128.  Accumulators: 256 rows (u) x 256
-//   columns (c) of s32 = all 512 TMEM columns.
+//   Integer stages (c bits 1..7).  One TMEM lane (one u) per transform
+//   thread: tcgen05.ld .pack::16b returns columns (2j, 2j+1) as the 16-bit
+//   lanes of register j, so the 256 values arrive packed in 128 registers.
+//   c bits 1..6 are packed biased stages (sum IMAD.IADD, diff IADD3 with the
+//   lane bias); c bit 7 is fused with the VIMNMX3 max/min fold (NL) or left
+//   to pass B (EMIT, which writes the stage-15 lanes).
 //
-//   Stages over c (8 of them) run on the integer pipes, one TMEM lane (one u)
-//   per thread, 256 values in registers, two 16-bit lanes per register.  A
-//   register is the exact integer lo + 2^16 hi (mod 2^32) of its two lane
-//   values, so every butterfly is one plain 32-bit add or sub with no per-stage
-//   bias, and borrows between the lanes cancel out.  The c-bit-0 stage is
-//   fused into the packing, (a, b) -> (a + b) + 2^16 (a - b) (two IMADs);
-//   c bits 1..6 are add/sub stages; the c-bit-7 (top) stage adds 2^15 per
-//   lane, which turns the lanes into the non-negative s = W / 2 + 2^15 of
-//   sbw_tile_simd.cuh, and feeds the VIMNMX3 max/min fold.  The row u = 0
-//   offset (-128 on every c) only reaches the coefficient u = 0; its thread
-//   adds 2^15 there.  TMEM is read in two pairs of 64-column loads and
-//   released before the stages start.
-//
-// Scheduling (one CTA of 8 warps per SM, persistent over a contiguous range of
-// masks; each thread owns one TMEM lane for the transform and one B row c for
-// the generation).  Per mask i a warp waits for the MMA of i (mbarrier), reads
-// its TMEM rows, and counts itself done; the LAST warp to finish reading
-// issues the MMA chain of i+1 at once -- at that point every warp has both
-// released TMEM and generated B(i+1) one step earlier -- so the tensor core
-// works on i+1 while the warps transform i and generate B(i+2) into the
-// buffer MMA(i) released.  No CTA-wide barrier inside the loop.
-// Masks are visited in Gray-code order inside every aligned block of 256 that
-// lies in [v_lo, v_hi), so consecutive masks differ in one bit and each row is
-// updated with a single (prefetched) plane XOR.
+// Warp roles (one persistent CTA per SM over a contiguous range of items):
+// warpgroup 0 = one MMA-issuing warp (tcgen05.mma blocks its thread while the
+// tensor core queue is full; the other 3 warps exit), warpgroups 1-2 = 8
+// transform warps; setmaxnreg gives them 232 registers and the issuer 32.
+// mbarriers: full (MMA(i) done) -> transform warps read D(i) -> tmem_empty ->
+// issuer starts MMA(i+1) once bfull says B(i+1) is ready; meanwhile the
+// transform warps generate B(i+2) into the buffer MMA(i) released and run
+// the integer stages of item i.  In NL mode masks are visited in Gray-code
+// order inside every aligned block of 256 that lies in [v_lo, v_hi), so
+// consecutive masks differ in one bit: one (prefetched) plane XOR per row.
+// SBW_TC_C0MMA=0 builds the earlier form (plain bit rows, c0 packed on the
+// FMA pipe with two IMADs per pair), kept for A/B measurements.
 #include <cstdio>
 #include <cstdlib>
 
