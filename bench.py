@@ -307,24 +307,26 @@ def run_ours(args, rank, world, local_rank):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
     if tc_path:
-        # k_tc16_nl: x bits 0..7 as an int8 GEMM on the tensor cores, bits 8..15
-        # (plus the max fold) as packed 16-bit integer stages.  The integer
-        # half is the limiter (issue-bound), so it is the primary roofline:
-        # 8 stages x 2^16 butterfly element-ops per component against the
-        # packed-16x2 rate (2 x the live int32 lane-op peak).  The tensor half
-        # is reported beside it: 2 * 256 * 2^16 int8 ops per component
-        # (M = u 256 x K = r 256 x N = c 256) against the live kind::i8 peak.
+        # k_tc_hybrid<NL>: x bits 0..7 and the c0 butterfly (9 stages) as an
+        # int8 GEMM on the tensor cores, x bits 9..15 (7 stages, incl. the max
+        # fold) as packed 16-bit integer stages.  The integer half is the
+        # limiter (ALU pipe ~82 %), so it is the primary roofline: 7 stages x
+        # 2^16 butterfly element-ops per component against the packed-16x2
+        # rate (2 x the live int32 lane-op peak).  The GEMM half is reported
+        # beside it: 2 * 256 (M) * 256 (N) * 288 (K incl. the bias block) int8
+        # ops executed per component against the live kind::i8 peak.
         peak_i8 = live_peak(lib, d, "sbw_int8_mma_peak")
-        alu_ops = 8 * (1 << n) * nmask
-        mma_ops = 2 * 256 * (1 << n) * nmask
+        alu_ops = 7 * (1 << n) * nmask
+        mma_ops = 2 * 256 * 256 * 288 * nmask
         achieved = alu_ops / (kern_ms * 1e-3)
         roofline = {
-            "bound": "int32_alu", "kernel": "k_tc16_nl (tcgen05 int8 MMA + packed int16 stages)",
+            "bound": "int32_alu",
+            "kernel": "k_tc_hybrid<NL> (tcgen05 int8 GEMM for 9 stages + packed int16 stages for 7)",
             "achieved": achieved / 1e12, "peak": 2 * peak / 1e12, "unit": "Tops/s",
             "frac": achieved / (2 * peak), "traffic": traffic,
             "ops_per_launch": alu_ops,
-            "ops_definition": "integer half: 8 stages x 2^16 butterfly element-ops per component "
-                              "(x bits 8..15 incl. the max fold); the other 8 stages run as the "
+            "ops_definition": "integer half: 7 stages x 2^16 butterfly element-ops per component "
+                              "(x bits 9..15 incl. the max fold); the other 9 stages run as the "
                               "int8 GEMM below",
             "kernel_ms": kern_ms,
             "peak_source": "measured live by sbw_int32_peak (int32 lane-ops/s) x 2 lanes for "
@@ -348,7 +350,8 @@ def run_ours(args, rank, world, local_rank):
         # packed-16x2 rate: 2 x the measured int32 lane-op peak (same
         # instruction issue rate, two lanes each).  frac_int32 is the same
         # number against the plain int32 peak (can exceed 1 because of packing).
-        roofline = {"bound": "int32_alu", "kernel": "k_tile_simd" if n <= 16 else "k3 pass A+B",
+        roofline = {"bound": "int32_alu",
+                    "kernel": "k_tile_simd" if n <= 16 else "k3: k_tc_hybrid<emit> + k_passb",
                     "achieved": achieved / 1e12, "peak": 2 * peak / 1e12, "unit": "Tops/s",
                     "frac": achieved / (2 * peak), "traffic": traffic,
                     "peak_int32": peak / 1e12, "frac_int32": achieved / peak,

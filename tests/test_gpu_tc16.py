@@ -1,7 +1,7 @@
-"""Parity of the n = 16 tensor-core kernel (k_tc16_nl, sbw_tc.cu).
+"""Parity of the n = 16 tensor-core kernel (k_tc_hybrid<NL>, sbw_tc.cu).
 
-sbw_nl at n = 16 runs the hybrid kernel: x bits 0..7 as an int8 tcgen05 GEMM,
-bits 8..15 as packed integer stages.  These cases target what is specific to
+sbw_nl at n = 16 runs the hybrid kernel: x bits 0..7 and the c0 butterfly as
+an int8 tcgen05 GEMM, x bits 9..15 as packed integer stages.  These cases target what is specific to
 it -- the u = 0 row correction, the Gray-code mask order inside aligned
 blocks of 256, CTA ranges of one or two masks, m > 16 -- and cross-check it
 against the all-ALU tile kernel (SBW_TC=0, k_tile_simd) on the same inputs.
@@ -78,7 +78,7 @@ print(json.dumps(out))
 
 
 def test_tensor_core_kernel_matches_alu_kernel():
-    """Same maxima and key from k_tc16_nl and from k_tile_simd<16> (SBW_TC=0)."""
+    """Same maxima and key from k_tc_hybrid<NL> and from k_tile_simd<16> (SBW_TC=0)."""
     res = {}
     for tc in ("1", "0"):
         p = subprocess.run([sys.executable, "-c", _ARM, ROOT], env=dict(os.environ, SBW_TC=tc),
