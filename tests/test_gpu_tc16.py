@@ -86,3 +86,18 @@ def test_tensor_core_kernel_matches_alu_kernel():
         assert p.returncode == 0, p.stderr[-2000:]
         res[tc] = json.loads(p.stdout.strip().splitlines()[-1])
     assert res["1"] == res["0"]
+
+
+def test_live_peak_microbenchmarks():
+    """The roofline denominators bench.py measures live: int32 lane-ops and
+    tcgen05 kind::i8 MMA throughput, both in a sane range for a B200."""
+    import ctypes
+
+    import paper_1912_03732_b200.device as d
+
+    lib = d.load_library()
+    for fn, lo, hi in (("sbw_int32_peak", 5e12, 2e14), ("sbw_int8_mma_peak", 1e15, 1e16)):
+        ops, ms = ctypes.c_double(0), ctypes.c_double(0)
+        d.check(getattr(lib, fn)(ctypes.byref(ops), ctypes.byref(ms), None))
+        assert lo < ops.value < hi, (fn, ops.value)
+        assert ms.value > 0
