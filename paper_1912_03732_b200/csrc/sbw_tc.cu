@@ -9,22 +9,24 @@
 // 2^16-element item split as x = c * 256 + r (r = x bits 0..7, c = bits 8..15,
 // c = 2 j + c0):
 //
-//   GEMM (stages over r and c0).  With b_c[r] = g_v(c * 256 + r) in {0, 1}
-//   (bit planes -> bytes, straight into shared memory), the B operand (u8)
-//   has rows B[2j] = b_2j + b_2j+1 and B[2j+1] = b_2j - b_2j+1 + 1 (the c0
-//   butterfly, kept unsigned), A = -H_256 (s8), and a 9th K block adds a bias
-//   against constant all-ones B columns, so that
-//     D[u][2j + e] = W_9 / 2 + 2^8   in [0, 512]
+//   GEMM (stages over r and c bits 0..2).  With b_c[r] = g_v(c * 256 + r)
+//   in {0, 1} (bit planes -> bytes, straight into shared memory), the B
+//   operand (u8) holds, for each group of 8 consecutive c, the 8-point WHT of
+//   their bit rows (biased butterflies, every byte in [0, 8]), A = -H_256
+//   (s8), and a 9th K block adds a bias against constant all-ones B columns,
+//   so that
+//     D[u][8 j + e] = W_11 / 2 + 2^10   in [0, 2^11]
 //   exactly -- the biased "s = W/2 + 2^(k-1) after k stages" form of
-//   sbw_tile_simd.cuh, row u = 0 included.  tcgen05.mma.kind::i8, M = 128,
+//   sbw_tile_simd.cuh, row u = 0 included.  (SBW_TC_ROWS = 2 builds the
+//   pair form: c bit 0 only, D = W_9 / 2 + 2^8.)  tcgen05.mma.kind::i8, M = 128,
 //   N = 256, K = 32; 2 M-halves x 9 K blocks; s32 accumulators fill all 512
 //   TMEM columns.  B is K-major SWIZZLE_128B; A and B's bias block are
 //   K-major without swizzle (layouts validated in tools/micro/tc_probe.cu).
 //
-//   Integer stages (c bits 1..7).  One TMEM lane (one u) per transform
+//   Integer stages (c bits 3..7).  One TMEM lane (one u) per transform
 //   thread: tcgen05.ld .pack::16b returns columns (2j, 2j+1) as the 16-bit
 //   lanes of register j, so the 256 values arrive packed in 128 registers.
-//   c bits 1..6 are packed biased stages (sum IMAD.IADD, diff IADD3 with the
+//   c bits 3..6 are packed biased stages (sum IMAD.IADD, diff IADD3 with the
 //   lane bias); c bit 7 is fused with the VIMNMX3 max/min fold (NL) or left
 //   to pass B (EMIT, which writes the stage-15 lanes).
 //
@@ -38,7 +40,7 @@
 // the integer stages of item i.  In NL mode masks are visited in Gray-code
 // order inside every aligned block of 256 that lies in [v_lo, v_hi), so
 // consecutive masks differ in one bit: one (prefetched) plane XOR per row.
-// SBW_TC_C0MMA=0 builds the earlier form (plain bit rows, c0 packed on the
+// SBW_TC_ROWS=1 builds the earliest form (plain bit rows, c0 packed on the
 // FMA pipe with two IMADs per pair), kept for A/B measurements.
 #include <cstdio>
 #include <cstdlib>
@@ -51,13 +53,22 @@
 namespace sbw {
 namespace {
 
-#ifndef SBW_TC_C0MMA
-#define SBW_TC_C0MMA 1
+#ifndef SBW_TC_ROWS
+#define SBW_TC_ROWS 8
 #endif
-// SBW_TC_C0MMA: the c-bit-0 butterfly also runs in the GEMM (B rows
-// b_2j + b_2j+1 and b_2j - b_2j+1 + 1, a bias K block, .pack::16b loads);
-// otherwise B rows are plain bits and the transform warps pack with IMADs.
-constexpr bool kC0Mma = SBW_TC_C0MMA != 0;
+// SBW_TC_ROWS = R: the B operand rows come in groups of R = 2^L consecutive c
+// holding the R-point WHT of their bit rows (unsigned, offset R/2 on all but
+// the first), so the GEMM also runs c bits 0..L-1; a bias K block and
+// .pack::16b loads deliver the biased lanes.  R = 1: plain bit rows, the
+// transform warps pack c0 with IMADs (the earlier form, kept for A/B).
+constexpr int kRows = SBW_TC_ROWS;
+static_assert(kRows == 1 || kRows == 2 || kRows == 8, "SBW_TC_ROWS must be 1, 2 or 8");
+constexpr int kLogRows = kRows == 8 ? 3 : (kRows == 2 ? 1 : 0);
+constexpr bool kC0Mma = kRows > 1;
+// bias per D entry: 128 R on every row, 128 R more on row u = 0, as columns of
+// 127 (plus a remainder) against all-ones B columns
+constexpr int kBiasT = 128 * kRows;
+constexpr int kBiasCols = (kBiasT + 126) / 127;
 constexpr int kMathWarps = 8;
 constexpr int kKA = kC0Mma ? 288 : 256;        // K of A: 256 (r) [+ 32 bias block]
 constexpr int kAHalf = 128 * kKA;              // one M = 128 half of A
@@ -74,16 +85,17 @@ static_assert(kBOff % 1024 == 0, "SW128 B atoms need 1024-byte alignment");
 // byte 32 j + 4 k + jb.  A's columns carry the same permutation.
 __device__ __forceinline__ int r_of_p(int p) { return (p & ~31) | ((p & 3) << 3) | ((p >> 2) & 7); }
 
-// A[u][p]: -H[u][r(p)] for p < 256.  Bias block (C0MMA, against B's all-ones
-// bias columns 0..5): +256 on every row (columns 0..2) and +256 more on row
-// u = 0 (columns 3..5).  That makes every D entry the biased s = W_9/2 + 2^8:
-// the polarity 1 - 2b puts +2^8 on row 0's sums, and the diff rows' "+1"
-// (b0 - b1 + 1, to stay unsigned) costs -sum_r H[u][r] = -256 [u = 0].
+// A[u][p]: -H[u][r(p)] for p < 256.  Bias block (against B's all-ones bias
+// columns): +128 R on every row and +128 R more on row u = 0.  That makes
+// every D entry the biased s = W_(8+L)/2 + 2^(7+L): the polarity 1 - 2b puts
+// +128 R on row 0's first row of each group, and the unsigned offset R/2 of
+// the other rows costs -(R/2) sum_r H[u][r] = -128 R [u = 0].
 __device__ __forceinline__ int a_value(int u, int p) {
   if (p < 256) return (__popc(u & r_of_p(p)) & 1) ? 1 : -1;
   const int k = p - 256;
-  if (k < 3) return k < 2 ? 127 : 2;
-  if (k < 6) return u == 0 ? (k < 5 ? 127 : 2) : 0;
+  const int col = k % kBiasCols, last = kBiasT - 127 * (kBiasCols - 1);
+  if (k < kBiasCols) return col < kBiasCols - 1 ? 127 : last;
+  if (k < 2 * kBiasCols) return u == 0 ? (col < kBiasCols - 1 ? 127 : last) : 0;
   return 0;
 }
 
@@ -122,7 +134,7 @@ __device__ __forceinline__ void xor_plane(uint32_t (&g)[8], const uint4& a, cons
 // at i * 128, logical chunk c at chunk c ^ i.  The two K halves of a row pair
 // write chunks 2w + kh first and 2w + 1 - kh second, so the 8 threads of a
 // store phase hit 8 different 16-byte bank groups.
-__device__ __forceinline__ void store_rows_sw128(const uint32_t (&g)[8], uint8_t* bbuf, int j, int kh) {
+[[maybe_unused]] __device__ __forceinline__ void store_rows_sw128(const uint32_t (&g)[8], uint8_t* bbuf, int j, int kh) {
   const int i0 = (2 * j) & 7;
   uint8_t* a0 = bbuf + (kh * 32 + (j >> 2)) * 1024 + i0 * 128;  // row 2j (sum)
   uint8_t* a1 = a0 + 128;                                          // row 2j+1 (diff)
@@ -144,6 +156,45 @@ __device__ __forceinline__ void store_rows_sw128(const uint32_t (&g)[8], uint8_t
       *reinterpret_cast<uint4*>(a0 + ((c ^ i0) << 4)) = make_uint4(sv[0], sv[1], sv[2], sv[3]);
       *reinterpret_cast<uint4*>(a1 + ((c ^ (i0 + 1)) << 4)) = make_uint4(dv[0], dv[1], dv[2], dv[3]);
     }
+  }
+}
+
+// R = 8 generation: thread (j, ks) owns plane word ks (K positions
+// 32 ks .. 32 ks + 31 = SW128 atom column ks >> 2, chunks 2 (ks & 3) + 0/1)
+// of the 8 rows 8j .. 8j+7 (g[e] = row 8j + e).  Per bit k the 8 byte
+// vectors b_e run through a biased 8-point WHT (diff + 2^t at stage t, so
+// every output is in [0, 8]); output e goes to row 8j + e.  Threads with
+// ks >= 4 store their second chunk first, so a store phase (8 threads, one
+// row e, ks = 0..7) covers all 8 chunk positions c ^ e: no bank conflicts.
+[[maybe_unused]] __device__ __forceinline__ void store_rows8_sw128(const uint32_t (&g)[8], uint8_t* bbuf, int j, int ks) {
+  uint8_t* base = bbuf + ((ks >> 2) * 32 + j) * 1024;
+  constexpr uint32_t M = 0x01010101u;
+  const int s4 = 4 * (ks >> 2);
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    uint32_t o[8][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = (4 * half + q) ^ s4;
+      uint32_t b[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) b[e] = (g[e] >> k) & M;
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if ((e & (1 << t)) == 0) {
+            const uint32_t x = b[e], y = b[e | (1 << t)];
+            b[e] = x + y;
+            b[e | (1 << t)] = x - y + (M << t);  // per byte in [0, 2^(t+1)]: no borrow
+          }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e][q] = b[e];
+    }
+    const int c = 2 * (ks & 3) + (half ^ (ks >> 2));  // logical chunk of this store
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      *reinterpret_cast<uint4*>(base + e * 128 + ((c ^ e) << 4)) = make_uint4(o[e][0], o[e][1], o[e][2], o[e][3]);
   }
 }
 
@@ -259,10 +310,10 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         make_uint4(wv[0], wv[1], wv[2], wv[3]);
   }
   if constexpr (kC0Mma) {
-    for (int n = tid; n < 256; n += kAllThreads) {
-      uint8_t* row = smem + kBbOff + (n >> 3) * 256 + (n & 7) * 16;
-      *reinterpret_cast<uint4*>(row) = make_uint4(0x01010101u, 0x00000101u, 0u, 0u);
-      *reinterpret_cast<uint4*>(row + 128) = make_uint4(0u, 0u, 0u, 0u);
+    static_assert(2 * kBiasCols <= 32, "bias block is one K block");
+    for (int e = tid; e < 256 * 32; e += kAllThreads) {
+      const int n = e >> 5, k = e & 31;  // bias columns 0 .. 2 kBiasCols - 1 = 1
+      smem[kBbOff + ((n >> 3) * 2 + (k >> 4)) * 128 + (n & 7) * 16 + (k & 15)] = k < 2 * kBiasCols ? 1 : 0;
     }
   }
   if (warp == 0) tc::tmem_alloc(&tmem_slot, 512);
@@ -313,7 +364,8 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kMathRegs));
     const int mt = tid - 128, mw = mt >> 5;  // transform thread / warp index
     const int c = mt;                        // generation row (plain B rows)
-    const int gj = mt >> 1, gkh = mt & 1;    // C0MMA: row pair, K half
+    const int gj = kRows == 8 ? mt >> 3 : mt >> 1;  // C0MMA: row group
+    const int gkh = kRows == 8 ? mt & 7 : mt & 1;   // C0MMA: plane word (R = 8) / K half (R = 2)
     const uint32_t* __restrict__ planes = a.planes;
     const int64_t pw = EMIT ? a.plane_words : 2048;
     GenState16 gs;
@@ -325,12 +377,18 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     // words at bp * 2048 + 8 c, or (C0MMA) 4 words of row 2j and 4 of row
     // 2j+1 at bp * 2048 + 16 j + 4 kh (+ 8)
     auto row_off = [&](uint32_t bp) {
-      return int64_t(bp) * 2048 + (kC0Mma ? 16 * gj + 4 * gkh : c * 8);
+      return int64_t(bp) * 2048 +
+             (kRows == 8 ? 64 * gj + gkh : (kRows == 2 ? 16 * gj + 4 * gkh : c * 8));
     };
     auto load_pl = [&](int i, uint32_t bp, uint4& x, uint4& y) {
-      const uint4* p = reinterpret_cast<const uint4*>(planes + int64_t(i) * pw + row_off(bp));
-      x = __ldg(p);
-      y = __ldg(p + (kC0Mma ? 2 : 1));
+      const uint32_t* p = planes + int64_t(i) * pw + row_off(bp);
+      if constexpr (kRows == 8) {  // word gkh of rows 8 j + e: stride 8 words
+        x = make_uint4(__ldg(p), __ldg(p + 8), __ldg(p + 16), __ldg(p + 24));
+        y = make_uint4(__ldg(p + 32), __ldg(p + 40), __ldg(p + 48), __ldg(p + 56));
+      } else {
+        x = __ldg(reinterpret_cast<const uint4*>(p));
+        y = __ldg(reinterpret_cast<const uint4*>(p) + (kC0Mma ? 2 : 1));
+      }
     };
     auto xor_all = [&](uint32_t d, uint32_t bp) {
       while (d) {
@@ -342,7 +400,9 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
       }
     };
     auto store_b = [&](int buf) {
-      if constexpr (kC0Mma)
+      if constexpr (kRows == 8)
+        store_rows8_sw128(gs.g, smem + kBOff + buf * kBBytes, gj, gkh);
+      else if constexpr (kRows == 2)
         store_rows_sw128(gs.g, smem + kBOff + buf * kBBytes, gj, gkh);
       else
         store_row(gs.g, smem + kBOff + buf * kBBytes, c);
@@ -404,8 +464,8 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         }
       };
       if constexpr (kC0Mma) {
-        // TMEM -> registers already packed: R[j] = lanes (c = 2j sum, diff),
-        // biased s = W_9 / 2 + 2^8 straight from the GEMM
+        // TMEM -> registers already packed: R[j] = lanes (columns 2j, 2j+1),
+        // biased s = W_(8+L) / 2 + 2^(7+L) straight from the GEMM
         uint32_t(&R0)[64] = *reinterpret_cast<uint32_t(*)[64]>(&R[0]);
         uint32_t(&R1)[64] = *reinterpret_cast<uint32_t(*)[64]>(&R[64]);
         tc::tmem_ld_x64_p16(tbase, R0);
@@ -450,9 +510,10 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         }
         gen_store();
       }
-      // c bits 1..6 (stages 9..14)
+      // c bits L..6 (register bits L-1..5, stages 8+L..14); register bit b is
+      // c bit b+1, stage 9+b, diff bias 2^(9+b) per lane
 #pragma unroll
-      for (int sb = 0; sb < 6; ++sb)
+      for (int sb = (kLogRows > 0 ? kLogRows - 1 : 0); sb < 6; ++sb)
 #pragma unroll
         for (int k = 0; k < 128; ++k)
           if ((k & (1 << sb)) == 0) {
