@@ -307,27 +307,32 @@ def run_ours(args, rank, world, local_rank):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
     if tc_path:
-        # k_tc_hybrid<NL>: x bits 0..7 and the c0 butterfly (9 stages) as an
-        # int8 GEMM on the tensor cores, x bits 9..15 (7 stages, incl. the max
-        # fold) as packed 16-bit integer stages.  The integer half is the
-        # limiter (ALU pipe ~82 %), so it is the primary roofline: 7 stages x
-        # 2^16 butterfly element-ops per component against the packed-16x2
-        # rate (2 x the live int32 lane-op peak).  The GEMM half is reported
-        # beside it: 2 * 256 (M) * 256 (N) * 288 (K incl. the bias block) int8
-        # ops executed per component against the live kind::i8 peak.
+        # k_tc_hybrid<NL>: the r stages (x bits 0..7) run as an int8 GEMM on
+        # the tensor cores; the c stages (x bits 8..15) run on the integer
+        # ALUs -- 3 of them as byte-lane butterflies on the bit rows of the
+        # GEMM's B operand (c bits 0..2, inside the generation), 5 as packed
+        # 16-bit stages after the GEMM (c bits 3..7, incl. the max fold).  The
+        # integer half is the limiter (ALU pipe ~80 %), so it is the primary
+        # roofline: 8 stages x 2^16 butterfly element-ops per component
+        # against the packed-16x2 rate (2 x the live int32 lane-op peak; the
+        # byte-lane stages would allow 4x, so this is conservative).  The GEMM
+        # half is reported beside it: 2 * 256 (M) * 256 (N) * 288 (K incl. the
+        # bias block) int8 ops executed per component against the live
+        # kind::i8 peak.
         peak_i8 = live_peak(lib, d, "sbw_int8_mma_peak")
-        alu_ops = 7 * (1 << n) * nmask
+        alu_ops = 8 * (1 << n) * nmask
         mma_ops = 2 * 256 * 256 * 288 * nmask
         achieved = alu_ops / (kern_ms * 1e-3)
         roofline = {
             "bound": "int32_alu",
-            "kernel": "k_tc_hybrid<NL> (tcgen05 int8 GEMM for 9 stages + packed int16 stages for 7)",
+            "kernel": "k_tc_hybrid<NL> (tcgen05 int8 GEMM over x bits 0..7; x bits 8..15 on the "
+                      "integer ALUs: 3 byte-lane stages on the GEMM operand + 5 packed int16 stages)",
             "achieved": achieved / 1e12, "peak": 2 * peak / 1e12, "unit": "Tops/s",
             "frac": achieved / (2 * peak), "traffic": traffic,
             "ops_per_launch": alu_ops,
-            "ops_definition": "integer half: 7 stages x 2^16 butterfly element-ops per component "
-                              "(x bits 9..15 incl. the max fold); the other 9 stages run as the "
-                              "int8 GEMM below",
+            "ops_definition": "integer half: 8 stages x 2^16 butterfly element-ops per component "
+                              "(x bits 8..15: 3 byte-lane + 5 int16-lane stages incl. the max "
+                              "fold); the r stages run as the int8 GEMM below",
             "kernel_ms": kern_ms,
             "peak_source": "measured live by sbw_int32_peak (int32 lane-ops/s) x 2 lanes for "
                            "packed 16-bit; not in MEASURED_PEAKS.json",
