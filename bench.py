@@ -344,6 +344,7 @@ def run_ours(args, rank, world, local_rank):
             "whole_fwht_equiv": {"ops_per_launch": n * (1 << n) * nmask,
                                  "achieved": n * (1 << n) * nmask / (kern_ms * 1e-3) / 1e12,
                                  "unit": "T butterfly element-ops/s",
+                                 "vs_int32_alu_peak": n * (1 << n) * nmask / (kern_ms * 1e-3) / peak,
                                  "vs_packed16_alu_peak": n * (1 << n) * nmask / (kern_ms * 1e-3)
                                  / (2 * peak)},
         }
