@@ -101,3 +101,28 @@ def test_live_peak_microbenchmarks():
         d.check(getattr(lib, fn)(ctypes.byref(ops), ctypes.byref(ms), None))
         assert lo < ops.value < hi, (fn, ops.value)
         assert ms.value > 0
+
+
+@pytest.mark.parametrize("trial", range(12))
+def test_random_ranges_n16(trial):
+    """Random S-boxes, widths and mask ranges through the tensor-core kernel."""
+    rng = np.random.default_rng(1000 + trial)
+    m = int(rng.integers(1, 25))
+    s = sw.generate_sbox(16, m, int(rng.integers(0, 1 << 30)), bijective=(m == 16))
+    top = 1 << m
+    lo = int(rng.integers(1, top))
+    hi = int(min(top, lo + rng.integers(1, 600)))
+    got, (nl, v, mxw) = _maxima(s, lo, hi)
+    want = orc.component_max_abs(s.table, 16, lo, hi)
+    assert np.array_equal(got, want)
+    i = int(np.argmax(want))
+    assert (v, mxw) == (lo + i, int(want[i]))
+
+
+@pytest.mark.parametrize("n,m,seed,lo,hi", [(17, 9, 1, 1, 40), (18, 12, 2, 100, 140), (19, 5, 3, 1, 32),
+                                             (20, 20, 4, 777, 800), (21, 16, 5, 1, 12), (24, 16, 6, 60000, 60004)])
+def test_multipass_tensor_core_pass_a(n, m, seed, lo, hi):
+    """n = 17..24 NL: the tensor-core pass A (k_tc_hybrid<EMIT>) + pass B."""
+    s = sw.generate_sbox(n, m, seed, bijective=False)
+    got, _ = _maxima(s, lo, hi)
+    assert np.array_equal(got, orc.component_max_abs(s.table, n, lo, hi))
