@@ -182,21 +182,48 @@ int launch_polarity(const void* table, int tbytes, int n, uint32_t v_lo, uint32_
 // 32x32 tiled transpose: mask-major rows -> x-major (walsh.py:174 is the
 // reference's inverse copy `np.ascontiguousarray(wt.T)`).
 // ---------------------------------------------------------------------------
-__global__ void k_transpose(const int32_t* __restrict__ in, int64_t rows, int64_t cols,
-                            int64_t ld_in, int32_t* __restrict__ out, int64_t ld_out) {
-  __shared__ int32_t t[32][33];
-  const int64_t tiles_c = (cols + 31) / 32;
-  const int64_t tiles = ((rows + 31) / 32) * tiles_c;
+// 64 x 64 tiles, 256 threads: 16 loads and 16 stores in flight per thread
+// (the 32 x 32 version kept too few bytes in flight to saturate HBM).  The
+// 65-int row pitch makes both the row-wise fill and the column-wise drain of
+// the shared tile conflict-free.
+template <int T>
+__global__ void __launch_bounds__(256) k_transpose(const int32_t* __restrict__ in, int64_t rows,
+                                                   int64_t cols, int64_t ld_in, int32_t* __restrict__ out,
+                                                   int64_t ld_out) {
+  __shared__ int32_t t[T][T + 1];
+  const int64_t tiles_c = (cols + T - 1) / T;
+  const int64_t tiles = ((rows + T - 1) / T) * tiles_c;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
   for (int64_t b = blockIdx.x; b < tiles; b += gridDim.x) {
-    const int64_t r0 = (b / tiles_c) * 32, c0 = (b % tiles_c) * 32;
-    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
-      const int64_t r = r0 + j, c = c0 + threadIdx.x;
-      if (r < rows && c < cols) t[j][threadIdx.x] = in[r * ld_in + c];
-    }
-    __syncthreads();
-    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
-      const int64_t c = c0 + j, r = r0 + threadIdx.x;
-      if (r < rows && c < cols) out[c * ld_out + r] = t[threadIdx.x][j];
+    const int64_t r0 = (b / tiles_c) * T, c0 = (b % tiles_c) * T;
+    if (r0 + T <= rows && c0 + T <= cols) {
+      int32_t v[T / 8][T / 32];
+#pragma unroll
+      for (int j = 0; j < T / 8; ++j)
+#pragma unroll
+        for (int h = 0; h < T / 32; ++h) v[j][h] = __ldcs(in + (r0 + ty + 8 * j) * ld_in + c0 + tx + 32 * h);
+#pragma unroll
+      for (int j = 0; j < T / 8; ++j)
+#pragma unroll
+        for (int h = 0; h < T / 32; ++h) t[ty + 8 * j][tx + 32 * h] = v[j][h];
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < T / 8; ++j)
+#pragma unroll
+        for (int h = 0; h < T / 32; ++h)
+          __stcs(out + (c0 + ty + 8 * j) * ld_out + r0 + tx + 32 * h, t[tx + 32 * h][ty + 8 * j]);
+    } else {
+      for (int j = ty; j < T; j += 8)
+        for (int h = tx; h < T; h += 32) {
+          const int64_t r = r0 + j, c = c0 + h;
+          if (r < rows && c < cols) t[j][h] = in[r * ld_in + c];
+        }
+      __syncthreads();
+      for (int j = ty; j < T; j += 8)
+        for (int h = tx; h < T; h += 32) {
+          const int64_t c = c0 + j, r = r0 + h;
+          if (r < rows && c < cols) out[c * ld_out + r] = t[h][j];
+        }
     }
     __syncthreads();
   }
@@ -205,8 +232,9 @@ __global__ void k_transpose(const int32_t* __restrict__ in, int64_t rows, int64_
 int launch_transpose_i32(const int32_t* in, int64_t rows, int64_t cols, int64_t ld_in,
                          int32_t* out, int64_t ld_out, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return SBW_OK;
-  const int64_t tiles = ((rows + 31) / 32) * ((cols + 31) / 32);
-  k_transpose<<<grid_for(tiles, 1, 16), dim3(32, 8), 0, st>>>(in, rows, cols, ld_in, out, ld_out);
+  constexpr int T = 64;
+  const int64_t tiles = ((rows + T - 1) / T) * ((cols + T - 1) / T);
+  k_transpose<T><<<grid_for(tiles, 1, 8), dim3(32, 8), 0, st>>>(in, rows, cols, ld_in, out, ld_out);
   SBW_LAUNCH_CHECK("k_transpose");
   return SBW_OK;
 }
