@@ -23,6 +23,9 @@ int launch_fused_onchip(const void* table, int tbytes, int n, int m, uint32_t v_
 int launch_tc16_nl(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
                    unsigned long long* key, cudaStream_t st);
 bool tc_path_enabled();
+// Tensor-core n = 16 materialised spectrum, mask-major rows out[(v - v_lo) * ld + u].
+int launch_tc16_spec(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
+                     int32_t* out, int64_t ld, cudaStream_t st);
 // Tensor-core pass A of the multi-pass NL path (n = 17..24): 15 stages per
 // 2^15 block, biased u16 out in a block-internal word order of its own
 // (pass B pairs equal word positions across blocks only, so any fixed order

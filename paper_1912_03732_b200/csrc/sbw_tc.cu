@@ -256,16 +256,21 @@ struct TcArgs {
   int64_t n_comp, n_items;
   int n_full;
   uint32_t* emit;
+  // SPEC (n = 16 materialised spectrum, mask-major): out[(v - v_lo) * ld + u]
+  int32_t* out;
+  int64_t ld;
 };
 
-template <bool EMIT>
+constexpr int kTcNL = 0, kTcEmit = 1, kTcSpec = 2;
+
+template <int MODE>
 __device__ __forceinline__ int64_t items_total(const TcArgs& a) {
-  return EMIT ? a.n_items : int64_t(a.v_hi) - a.v_lo;
+  return MODE == kTcEmit ? a.n_items : int64_t(a.v_hi) - a.v_lo;
 }
 // item t of the launch -> (mask v, 2^16-block index bp)
-template <bool EMIT>
+template <int MODE>
 __device__ __forceinline__ void item_at(const TcArgs& a, int64_t t, uint32_t& v, uint32_t& bp) {
-  if constexpr (EMIT) {
+  if constexpr (MODE == kTcEmit) {
     bp = uint32_t(t / a.n_comp);
     v = a.v_first + uint32_t(t - int64_t(bp) * a.n_comp);
   } else {
@@ -281,8 +286,10 @@ struct GenState16 {
   uint32_t vcur, bpcur;
 };
 
-template <bool EMIT>
+template <int MODE>
 __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
+  constexpr bool EMIT = MODE == kTcEmit;
+  static_assert(MODE != kTcSpec || kC0Mma, "exact SPEC output needs the bias-block GEMM");
   extern __shared__ __align__(1024) uint8_t smem[];
   // full: MMA(i) done.  tmem_empty: all transform threads read D(i).
   // bfull[b]: all transform threads generated the B operand in buffer b.
@@ -290,7 +297,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(16) uint32_t s_wmax[4][kMathWarps];  // per-warp max|W|, slot = item index & 3
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t total = items_total<EMIT>(a);
+  const int64_t total = items_total<MODE>(a);
   const int64_t t_lo = total * blockIdx.x / gridDim.x;
   const int n_my = int(total * (blockIdx.x + 1) / gridDim.x - t_lo);
 
@@ -409,7 +416,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     };
     for (int k = 0; k < 2 && k < n_my; ++k) {
       uint32_t vn, bpn;
-      item_at<EMIT>(a, t_lo + k, vn, bpn);
+      item_at<MODE>(a, t_lo + k, vn, bpn);
       if (EMIT && bpn != gs.bpcur) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) gs.g[q] = 0;
@@ -433,7 +440,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
       bool reset = false;
       uint4 pa = make_uint4(0, 0, 0, 0), pb = pa;
       if (gen) {
-        item_at<EMIT>(a, t_lo + i + 2, vn, bpn);
+        item_at<MODE>(a, t_lo + i + 2, vn, bpn);
         reset = EMIT && bpn != gs.bpcur;
         d = reset ? vn : (gs.vcur ^ vn);
         if (d) {
@@ -532,7 +539,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
           R[64] += 0x4000u;
         }
         uint32_t vi, bpi;
-        item_at<EMIT>(a, t_lo + i, vi, bpi);
+        item_at<MODE>(a, t_lo + i, vi, bpi);
         uint32_t* dst = a.emit + (int64_t(vi - a.v_first) << (a.n_full - 1)) +
                         (int64_t(2 * bpi) << 14) + 4 * u;
 #pragma unroll
@@ -557,6 +564,24 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         }
         const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<16>(mx, mn)));
         if (lane == 0) s_wmax[i & 3][mw] = m;
+        if constexpr (MODE == kTcSpec) {
+          // exact W of the top stage per lane (the packed S / D above may wrap
+          // at |W| = 2^16), stored at u = u_c * 256 + u_r with
+          // u_c = lane + 2 k (+ 128 for the diff) -- 32 consecutive u_r per
+          // warp store, 128 B coalesced
+          uint32_t vi, bpi;
+          item_at<MODE>(a, t_lo + i, vi, bpi);
+          int32_t* row = a.out + int64_t(vi - a.v_lo) * a.ld + u;
+#pragma unroll
+          for (int k = 0; k < 64; ++k) {
+            const int x0 = int(R[k] & 0xFFFFu), x1 = int(R[k] >> 16);
+            const int y0 = int(R[k + 64] & 0xFFFFu), y1 = int(R[k + 64] >> 16);
+            __stcs(row + (2 * k) * 256, 2 * (x0 + y0) - 65536);
+            __stcs(row + (2 * k + 1) * 256, 2 * (x1 + y1) - 65536);
+            __stcs(row + (2 * k + 128) * 256, 2 * (x0 - y0));
+            __stcs(row + (2 * k + 129) * 256, 2 * (x1 - y1));
+          }
+        }
       }
     }
     tc::fence_before();
@@ -645,20 +670,20 @@ bool tc_path_enabled() {
 }
 
 namespace {
-template <bool EMIT>
+template <int MODE>
 int run_tc_hybrid(const TcArgs& a, int64_t items, cudaStream_t st) {
   if (items <= 0) return SBW_OK;
   DeviceProps dp;
   if (int rc = device_props(&dp)) return rc;
   static unsigned long long attr_done = 0;  // per device; the call is idempotent
   if (!(attr_done >> (dp.device & 63) & 1ull)) {
-    SBW_CUDA_CHECK(cudaFuncSetAttribute(k_tc_hybrid<EMIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SBW_CUDA_CHECK(cudaFuncSetAttribute(k_tc_hybrid<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         kTcSmem));
     attr_done |= 1ull << (dp.device & 63);
   }
   const int grid = int(items < dp.sm_count ? items : dp.sm_count);
-  k_tc_hybrid<EMIT><<<grid, kAllThreads, kTcSmem, st>>>(a);
-  SBW_LAUNCH_CHECK(EMIT ? "k_tc_hybrid<emit>" : "k_tc_hybrid<nl>");
+  k_tc_hybrid<MODE><<<grid, kAllThreads, kTcSmem, st>>>(a);
+  SBW_LAUNCH_CHECK(MODE == kTcEmit ? "k_tc_hybrid<emit>" : (MODE == kTcSpec ? "k_tc_hybrid<spec>" : "k_tc_hybrid<nl>"));
   return SBW_OK;
 }
 }  // namespace
@@ -672,7 +697,21 @@ int launch_tc16_nl(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t
   a.v_hi = v_hi;
   a.max_abs = max_abs;
   a.key = key;
-  return run_tc_hybrid<false>(a, int64_t(v_hi) - v_lo, st);
+  return run_tc_hybrid<kTcNL>(a, int64_t(v_hi) - v_lo, st);
+}
+
+int launch_tc16_spec(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
+                     int32_t* out, int64_t ld, cudaStream_t st) {
+  if (!kC0Mma) return set_error(SBW_EINVAL, "tensor-core spectrum needs SBW_TC_ROWS >= 2");
+  TcArgs a{};
+  a.planes = planes;
+  a.plane_words = 2048;
+  a.v_lo = v_lo;
+  a.v_hi = v_hi;
+  a.max_abs = max_abs;
+  a.out = out;
+  a.ld = ld;
+  return run_tc_hybrid<kTcSpec>(a, int64_t(v_hi) - v_lo, st);
 }
 
 int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_comp, uint32_t* emit,
@@ -685,7 +724,7 @@ int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_co
   a.n_items = n_comp << (n - 16);
   a.n_full = n;
   a.emit = emit;
-  return run_tc_hybrid<true>(a, a.n_items, st);
+  return run_tc_hybrid<kTcEmit>(a, a.n_items, st);
 }
 
 }  // namespace sbw

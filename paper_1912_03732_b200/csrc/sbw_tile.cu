@@ -139,8 +139,9 @@ int launch_fused_onchip(const void* table, int tbytes, int n, int m, uint32_t v_
   }
   uint32_t* planes = static_cast<uint32_t*>(scratch);
   if (int rc = build_planes(table, tbytes, n, m, planes, st)) return rc;
-  if (n == 16 && out == nullptr && tc_path_enabled())
-    return launch_tc16_nl(planes, v_lo, v_hi, max_abs, key, st);
+  if (n == 16 && tc_path_enabled())
+    return out == nullptr ? launch_tc16_nl(planes, v_lo, v_hi, max_abs, key, st)
+                          : launch_tc16_spec(planes, v_lo, v_hi, max_abs, out, ld, st);
   TileArgs a{};
   a.planes = planes;
   a.plane_words = (int64_t(1) << n) >> 5;
