@@ -172,6 +172,17 @@ def cpu_baseline(name, target_s=12.0, procs=None):
 
 
 # ------------------------------------------------------------------- GPU ----
+def measured_hbm_peak():
+    """HBM copy bandwidth in GB/s from the driver-written MEASURED_PEAKS.json,
+    else the fallback B200_PROFILING.md states."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (driver-measured copy)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback 6.65 TB/s of B200_PROFILING.md (MEASURED_PEAKS.json absent)"
+
+
 def live_peak(lib, d, fn):
     """Best of 2 runs of a libsbw peak microbenchmark (sbw_int32_peak / sbw_int8_mma_peak)."""
     import ctypes
@@ -348,6 +359,24 @@ def run_ours(args, rank, world, local_rank):
                                  "vs_packed16_alu_peak": n * (1 << n) * nmask / (kern_ms * 1e-3)
                                  / (2 * peak)},
         }
+    elif n >= 17:
+        # Multi-pass K3: pass A (k_tc_hybrid<emit>) writes every component's
+        # stage-15 partial transform as u16 and pass B reads it back -- 4 B of
+        # HBM traffic per element, the bound once pass A runs on the tensor
+        # cores.  Peak: the driver-measured HBM copy bandwidth.
+        hbm_peak, hbm_src = measured_hbm_peak()
+        alg_bytes = 4 * (1 << n) * nmask
+        alg_ops = n * (1 << n) * nmask
+        roofline = {"bound": "hbm", "kernel": "k3: k_tc_hybrid<emit> (pass A) + k_passb (pass B)",
+                    "achieved": alg_bytes / (kern_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": alg_bytes / (kern_ms * 1e-3) / 1e9 / hbm_peak, "traffic": traffic,
+                    "bytes_per_launch": alg_bytes,
+                    "bytes_definition": "u16 scratch written by pass A and read by pass B: 2 + 2 B per "
+                                        "element per component",
+                    "kernel_ms": kern_ms, "peak_source": hbm_src,
+                    "int32_alu": {"achieved": alg_ops / (kern_ms * 1e-3) / 1e12, "peak": peak / 1e12,
+                                  "unit": "Tops/s", "frac": alg_ops / (kern_ms * 1e-3) / peak,
+                                  "ops_definition": "n * 2^n butterfly element-ops per component"}}
     else:
         alg_ops = n * (1 << n) * nmask  # butterfly element-ops
         achieved = alg_ops / (kern_ms * 1e-3)
@@ -357,7 +386,7 @@ def run_ours(args, rank, world, local_rank):
         # instruction issue rate, two lanes each).  frac_int32 is the same
         # number against the plain int32 peak (can exceed 1 because of packing).
         roofline = {"bound": "int32_alu",
-                    "kernel": "k_tile_simd" if n <= 16 else "k3: k_tc_hybrid<emit> + k_passb",
+                    "kernel": "k_tile_simd",
                     "achieved": achieved / 1e12, "peak": 2 * peak / 1e12, "unit": "Tops/s",
                     "frac": achieved / (2 * peak), "traffic": traffic,
                     "peak_int32": peak / 1e12, "frac_int32": achieved / peak,
