@@ -311,7 +311,9 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- roofline of the dominant kernel (fused NL) ----------------------
     peak = live_peak(lib, d, "sbw_int32_peak")
-    tc_path = n == 16 and os.environ.get("SBW_TC", "1") != "0"
+    # sbw_nl takes the tensor-core kernel for n = 11..16 (n < 16: 2^(16-n)
+    # components per 2^16 tile; needs m >= 16 - n), unless SBW_TC=0
+    tc_path = 11 <= n <= 16 and m >= 16 - n and os.environ.get("SBW_TC", "1") != "0"
     prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_traffic.json")
     traffic = None
     if os.path.exists(prof):
@@ -331,19 +333,21 @@ def run_ours(args, rank, world, local_rank):
         # bias block) int8 ops executed per component against the live
         # kind::i8 peak.
         peak_i8 = live_peak(lib, d, "sbw_int8_mma_peak")
-        alu_ops = 8 * (1 << n) * nmask
-        mma_ops = 2 * 256 * 256 * 288 * nmask
+        lc = 16 - n
+        items = ((v_hi - 1) >> lc) + 1 - (v_lo >> lc)  # 2^16 tiles
+        alu_ops = (n - 8) * (1 << n) * nmask
+        mma_ops = 2 * 256 * 256 * 288 * items
         achieved = alu_ops / (kern_ms * 1e-3)
         roofline = {
             "bound": "int32_alu",
-            "kernel": "k_tc_hybrid<NL> (tcgen05 int8 GEMM over x bits 0..7; x bits 8..15 on the "
-                      "integer ALUs: 3 byte-lane stages on the GEMM operand + 5 packed int16 stages)",
+            "kernel": f"k_tc_hybrid<NL, {n}> (tcgen05 int8 GEMM over x bits 0..7; x bits 8..{n - 1} on "
+                      "the integer ALUs: 3 byte-lane stages on the GEMM operand + packed int16 stages)",
             "achieved": achieved / 1e12, "peak": 2 * peak / 1e12, "unit": "Tops/s",
             "frac": achieved / (2 * peak), "traffic": traffic,
             "ops_per_launch": alu_ops,
-            "ops_definition": "integer half: 8 stages x 2^16 butterfly element-ops per component "
-                              "(x bits 8..15: 3 byte-lane + 5 int16-lane stages incl. the max "
-                              "fold); the r stages run as the int8 GEMM below",
+            "ops_definition": "integer half: (n-8) stages x 2^n butterfly element-ops per component "
+                              "(x bits 8..n-1: 3 byte-lane + n-11 int16-lane stages incl. the "
+                              "max fold); the r stages run as the int8 GEMM below",
             "kernel_ms": kern_ms,
             "peak_source": "measured live by sbw_int32_peak (int32 lane-ops/s) x 2 lanes for "
                            "packed 16-bit; not in MEASURED_PEAKS.json",

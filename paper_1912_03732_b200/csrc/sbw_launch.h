@@ -23,6 +23,10 @@ int launch_fused_onchip(const void* table, int tbytes, int n, int m, uint32_t v_
 int launch_tc16_nl(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
                    unsigned long long* key, cudaStream_t st);
 bool tc_path_enabled();
+// Tensor-core NL for n = 11..15 (2^(16-n) components per 2^16 tile); needs
+// m >= 16 - n so every slot's mask is a valid mask.
+int launch_tc_nl_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
+                       unsigned long long* key, cudaStream_t st);
 // Tensor-core n = 16 materialised spectrum, mask-major rows out[(v - v_lo) * ld + u].
 int launch_tc16_spec(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
                      int32_t* out, int64_t ld, cudaStream_t st);

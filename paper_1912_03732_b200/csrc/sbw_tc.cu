@@ -44,6 +44,7 @@
 // FMA pipe with two IMADs per pair), kept for A/B measurements.
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "sbw_internal.cuh"
 #include "sbw_launch.h"
@@ -244,6 +245,7 @@ constexpr int kMathRegs = 232;
 constexpr int kAllThreads = 128 + kMathWarps * 32;  // warpgroup 0: issuer (+3 idle warps)
 
 struct TcArgs {
+  const uint8_t* consts;  // smem image of A and B's bias block (kBOff bytes), k_tc_consts
   const uint32_t* planes;
   int64_t plane_words;  // 2^n / 32
   // NL (n = 16): masks [v_lo, v_hi), Gray order inside aligned 256-blocks
@@ -263,19 +265,27 @@ struct TcArgs {
 
 constexpr int kTcNL = 0, kTcEmit = 1, kTcSpec = 2;
 
-template <int MODE>
+// NL items for an n = NB <= 16 box: one 2^16 tile holds C = 2^(16 - NB)
+// components (slots); item t covers masks (base << log2 C) | slot, with base
+// running over [v_lo >> log2 C, ceil(v_hi / C)) in Gray order inside aligned
+// blocks of 256.  NB = 16: one slot, item = mask.
+template <int MODE, int NB>
 __device__ __forceinline__ int64_t items_total(const TcArgs& a) {
-  return MODE == kTcEmit ? a.n_items : int64_t(a.v_hi) - a.v_lo;
+  constexpr int LC = 16 - NB;
+  if constexpr (MODE == kTcEmit) return a.n_items;
+  return ((int64_t(a.v_hi) - 1) >> LC) + 1 - (int64_t(a.v_lo) >> LC);
 }
-// item t of the launch -> (mask v, 2^16-block index bp)
-template <int MODE>
+// item t of the launch -> (mask v of slot 0, 2^16-block index bp)
+template <int MODE, int NB>
 __device__ __forceinline__ void item_at(const TcArgs& a, int64_t t, uint32_t& v, uint32_t& bp) {
   if constexpr (MODE == kTcEmit) {
     bp = uint32_t(t / a.n_comp);
     v = a.v_first + uint32_t(t - int64_t(bp) * a.n_comp);
   } else {
+    constexpr int LC = 16 - NB;
+    const uint32_t b0 = a.v_lo >> LC, b1 = uint32_t(((int64_t(a.v_hi) - 1) >> LC) + 1);
     bp = 0;
-    v = mask_at(a.v_lo + t, a.v_lo, a.v_hi);
+    v = mask_at(b0 + t, b0, b1) << LC;
   }
 }
 
@@ -286,24 +296,11 @@ struct GenState16 {
   uint32_t vcur, bpcur;
 };
 
-template <int MODE>
-__global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
-  constexpr bool EMIT = MODE == kTcEmit;
-  static_assert(MODE != kTcSpec || kC0Mma, "exact SPEC output needs the bias-block GEMM");
-  extern __shared__ __align__(1024) uint8_t smem[];
-  // full: MMA(i) done.  tmem_empty: all transform threads read D(i).
-  // bfull[b]: all transform threads generated the B operand in buffer b.
-  __shared__ uint64_t bar_full, bar_tmem_empty, bar_bfull[2], bar_done;
-  __shared__ uint32_t tmem_slot;
-  __shared__ __align__(16) uint32_t s_wmax[4][kMathWarps];  // per-warp max|W|, slot = item index & 3
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t total = items_total<MODE>(a);
-  const int64_t t_lo = total * blockIdx.x / gridDim.x;
-  const int n_my = int(total * (blockIdx.x + 1) / gridDim.x - t_lo);
-
-  // constant operands: A (with the K permutation of the byte expansion) and,
-  // for C0MMA, B's bias block (columns 0..5 = 1 on every row)
-  for (int e = tid; e < 256 * (kKA / 16); e += kAllThreads) {
+// Shared-memory image of the constant operands: A = -H_256 with the K
+// permutation of the byte expansion (+ the bias block columns) and, for
+// C0MMA, B's bias block (columns 0 .. 2 kBiasCols - 1 = 1 on every row).
+__global__ void k_tc_consts(uint8_t* img) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 256 * (kKA / 16); e += gridDim.x * blockDim.x) {
     const int uu = e / (kKA / 16), pc = e % (kKA / 16);
     uint32_t wv[4];
 #pragma unroll
@@ -313,16 +310,48 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
       for (int b = 0; b < 4; ++b) x |= uint32_t(uint8_t(a_value(uu, pc * 16 + q * 4 + b))) << (8 * b);
       wv[q] = x;
     }
-    *reinterpret_cast<uint4*>(smem + kAOff + ((uu >> 3) * (kKA / 16) + pc) * 128 + (uu & 7) * 16) =
+    *reinterpret_cast<uint4*>(img + kAOff + ((uu >> 3) * (kKA / 16) + pc) * 128 + (uu & 7) * 16) =
         make_uint4(wv[0], wv[1], wv[2], wv[3]);
   }
   if constexpr (kC0Mma) {
     static_assert(2 * kBiasCols <= 32, "bias block is one K block");
-    for (int e = tid; e < 256 * 32; e += kAllThreads) {
-      const int n = e >> 5, k = e & 31;  // bias columns 0 .. 2 kBiasCols - 1 = 1
-      smem[kBbOff + ((n >> 3) * 2 + (k >> 4)) * 128 + (n & 7) * 16 + (k & 15)] = k < 2 * kBiasCols ? 1 : 0;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 256 * 32; e += gridDim.x * blockDim.x) {
+      const int n = e >> 5, k = e & 31;
+      img[kBbOff + ((n >> 3) * 2 + (k >> 4)) * 128 + (n & 7) * 16 + (k & 15)] = k < 2 * kBiasCols ? 1 : 0;
     }
   }
+}
+
+// publish slot `slot` of NL item t (masks outside [v_lo, v_hi) are skipped)
+template <int NB>
+__device__ __forceinline__ void publish_item(const TcArgs& a, const uint32_t* wmax, int64_t t, int slot) {
+  uint32_t v, bp;
+  item_at<kTcNL, NB>(a, t, v, bp);
+  v |= uint32_t(slot);
+  if (v >= a.v_lo && v < a.v_hi) publish(wmax, v, a.v_lo, a.max_abs, a.key);
+}
+
+template <int MODE, int NB = 16>
+__global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
+  constexpr bool EMIT = MODE == kTcEmit;
+  static_assert(NB == 16 || (MODE == kTcNL && NB >= 11 && kRows == 8), "n < 16: NL with 8-row groups");
+  constexpr int kSlots = 1 << (16 - NB);  // components per 2^16 tile
+  static_assert(MODE != kTcSpec || kC0Mma, "exact SPEC output needs the bias-block GEMM");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  // full: MMA(i) done.  tmem_empty: all transform threads read D(i).
+  // bfull[b]: all transform threads generated the B operand in buffer b.
+  __shared__ uint64_t bar_full, bar_tmem_empty, bar_bfull[2], bar_done;
+  __shared__ uint32_t tmem_slot;
+  __shared__ __align__(16) uint32_t s_wmax[4][kSlots][kMathWarps];  // per-warp max|W| [item & 3][slot]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t total = items_total<MODE, NB>(a);
+  const int64_t t_lo = total * blockIdx.x / gridDim.x;
+  const int n_my = int(total * (blockIdx.x + 1) / gridDim.x - t_lo);
+
+  // constant operands (A and B's bias block): one coalesced copy of the
+  // image k_tc_consts built once per device
+  for (int e = tid; e < kBOff / 16; e += kAllThreads)
+    reinterpret_cast<uint4*>(smem)[e] = __ldg(reinterpret_cast<const uint4*>(a.consts) + e);
   if (warp == 0) tc::tmem_alloc(&tmem_slot, 512);
   if (tid == 0) {
     tc::mbar_init(&bar_full, 1);
@@ -347,21 +376,18 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         tc::fence_after();
         issue_mma_warp(tmem, smem, i & 1, &bar_full);
         if constexpr (!EMIT) {
-          // bfull for mask i (i >= 2) is produced after each thread stored
-          // its max of mask i - 2
-          if (i >= 2 && lane == 0)
-            publish(s_wmax[(i - 2) & 3], mask_at(a.v_lo + t_lo + i - 2, a.v_lo, a.v_hi), a.v_lo,
-                    a.max_abs, a.key);
+          // bfull for item i (i >= 2) is produced after each thread stored
+          // its maxima of item i - 2
+          if (i >= 2 && lane < kSlots) publish_item<NB>(a, s_wmax[(i - 2) & 3][lane], t_lo + i - 2, lane);
         }
       }
       // every transform thread has read D(last) and stored its last max
       tc::mbar_wait(&bar_done, 0u);
       tc::fence_after();
       if constexpr (!EMIT) {
-        if (lane == 0)
+        if (lane < kSlots)
           for (int i = n_my - 2 < 0 ? 0 : n_my - 2; i < n_my; ++i)
-            publish(s_wmax[i & 3], mask_at(a.v_lo + t_lo + i, a.v_lo, a.v_hi), a.v_lo, a.max_abs,
-                    a.key);
+            publish_item<NB>(a, s_wmax[i & 3][lane], t_lo + i, lane);
       }
       __syncwarp();
       tc::tmem_dealloc(tmem, 512);
@@ -374,7 +400,11 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     const int gj = kRows == 8 ? mt >> 3 : mt >> 1;  // C0MMA: row group
     const int gkh = kRows == 8 ? mt & 7 : mt & 1;   // C0MMA: plane word (R = 8) / K half (R = 2)
     const uint32_t* __restrict__ planes = a.planes;
-    const int64_t pw = EMIT ? a.plane_words : 2048;
+    const int64_t pw = EMIT ? a.plane_words : (int64_t(1) << NB) >> 5;
+    // NB < 16: this thread's 8 rows belong to slot gslot; its rows within the
+    // component start at row group gj mod 2^(NB - 11)
+    const uint32_t gslot = NB < 16 ? uint32_t(gj >> (NB - 11)) : 0u;
+    const int gjc = NB < 16 ? (gj & ((1 << (NB - 11)) - 1)) : gj;
     GenState16 gs;
 #pragma unroll
     for (int k = 0; k < 8; ++k) gs.g[k] = 0;
@@ -385,7 +415,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     // 2j+1 at bp * 2048 + 16 j + 4 kh (+ 8)
     auto row_off = [&](uint32_t bp) {
       return int64_t(bp) * 2048 +
-             (kRows == 8 ? 64 * gj + gkh : (kRows == 2 ? 16 * gj + 4 * gkh : c * 8));
+             (kRows == 8 ? 64 * gjc + gkh : (kRows == 2 ? 16 * gj + 4 * gkh : c * 8));
     };
     auto load_pl = [&](int i, uint32_t bp, uint4& x, uint4& y) {
       const uint32_t* p = planes + int64_t(i) * pw + row_off(bp);
@@ -406,6 +436,22 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         xor_plane(gs.g, x, y);
       }
     };
+    // full recompute (first items): the planes of all set bits of d, 8 at a
+    // time with every load in flight, instead of one serialized load per bit
+    auto xor_full = [&](uint32_t d, uint32_t bp) {
+#pragma unroll 1
+      for (int i0 = 0; i0 < 32 && (d >> i0); i0 += 8) {
+        uint4 x[8], y[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          x[q] = make_uint4(0, 0, 0, 0);
+          y[q] = x[q];
+          if ((d >> (i0 + q)) & 1u) load_pl(i0 + q, bp, x[q], y[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) xor_plane(gs.g, x[q], y[q]);
+      }
+    };
     auto store_b = [&](int buf) {
       if constexpr (kRows == 8)
         store_rows8_sw128(gs.g, smem + kBOff + buf * kBBytes, gj, gkh);
@@ -416,14 +462,15 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     };
     for (int k = 0; k < 2 && k < n_my; ++k) {
       uint32_t vn, bpn;
-      item_at<MODE>(a, t_lo + k, vn, bpn);
+      item_at<MODE, NB>(a, t_lo + k, vn, bpn);
+      vn |= gslot;
       if (EMIT && bpn != gs.bpcur) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) gs.g[q] = 0;
         gs.vcur = 0;
         gs.bpcur = bpn;
       }
-      xor_all(gs.vcur ^ vn, bpn);
+      xor_full(gs.vcur ^ vn, bpn);
       gs.vcur = vn;
       store_b(k);
       tc::fence_proxy_async();
@@ -440,7 +487,8 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
       bool reset = false;
       uint4 pa = make_uint4(0, 0, 0, 0), pb = pa;
       if (gen) {
-        item_at<MODE>(a, t_lo + i + 2, vn, bpn);
+        item_at<MODE, NB>(a, t_lo + i + 2, vn, bpn);
+        vn |= gslot;
         reset = EMIT && bpn != gs.bpcur;
         d = reset ? vn : (gs.vcur ^ vn);
         if (d) {
@@ -520,7 +568,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
       // c bits L..6 (register bits L-1..5, stages 8+L..14); register bit b is
       // c bit b+1, stage 9+b, diff bias 2^(9+b) per lane
 #pragma unroll
-      for (int sb = (kLogRows > 0 ? kLogRows - 1 : 0); sb < 6; ++sb)
+      for (int sb = (kLogRows > 0 ? kLogRows - 1 : 0); sb < NB - 10; ++sb)
 #pragma unroll
         for (int k = 0; k < 128; ++k)
           if ((k & (1 << sb)) == 0) {
@@ -539,7 +587,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
           R[64] += 0x4000u;
         }
         uint32_t vi, bpi;
-        item_at<MODE>(a, t_lo + i, vi, bpi);
+        item_at<MODE, NB>(a, t_lo + i, vi, bpi);
         uint32_t* dst = a.emit + (int64_t(vi - a.v_first) << (a.n_full - 1)) +
                         (int64_t(2 * bpi) << 14) + 4 * u;
 #pragma unroll
@@ -550,27 +598,44 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
                 make_uint4(R[64 * h + 4 * q], R[64 * h + 4 * q + 1], R[64 * h + 4 * q + 2],
                            R[64 * h + 4 * q + 3]);
       } else {
-        // c bit 7 (stage 15, top) fused with the max/min fold (carry argument:
-        // tile_last_pass); the row u = 0 offset reaches only S of k = 0
+        // top stage (c bit NB-9 = register bit NB-10) fused with the max/min
+        // fold, per slot (register bits NB-9..6; carry argument of
+        // tile_last_pass for NB = 16).  NB = 11 has no ALU stage left: the
+        // fold runs on the GEMM output directly.  The row u = 0 offset of the
+        // R = 1 form reaches only S of register 0.
         const uint32_t corr0 = (!kC0Mma && u == 0) ? 0x8000u : 0u;
-        uint32_t mx = 0u, mn = 0xFFFFFFFFu;
+        constexpr int kTop = NB - 10;         // register bit of the top stage (NB >= 12)
+        constexpr int kPerSlot = 1 << (NB - 9);
 #pragma unroll
-        for (int k = 0; k < 64; ++k) {
-          const uint32_t x = R[k], y = R[k + 64];
-          const uint32_t S = x + y + (k == 0 ? corr0 : 0u);
-          const uint32_t D = x - y + 0x80008000u;
-          mx = __vimax3_u16x2(mx, S, D);
-          mn = __vimin3_u16x2(mn, S, D);
+        for (int sl = 0; sl < kSlots; ++sl) {
+          uint32_t mx = 0u, mn = 0xFFFFFFFFu;
+          if constexpr (NB >= 12) {
+#pragma unroll
+            for (int kk = 0; kk < kPerSlot / 2; ++kk) {
+              const int k = sl * kPerSlot + (kk & ((1 << kTop) - 1)) + ((kk >> kTop) << (kTop + 1));
+              const uint32_t x = R[k], y = R[k + (1 << kTop)];
+              const uint32_t S = x + y + (k == 0 ? corr0 : 0u);
+              const uint32_t D = x - y + ((1u << (NB - 1)) * 0x00010001u);
+              mx = __vimax3_u16x2(mx, S, D);
+              mn = __vimin3_u16x2(mn, S, D);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < kPerSlot; k += 2) {
+              mx = __vimax3_u16x2(mx, R[sl * kPerSlot + k], R[sl * kPerSlot + k + 1]);
+              mn = __vimin3_u16x2(mn, R[sl * kPerSlot + k], R[sl * kPerSlot + k + 1]);
+            }
+          }
+          const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<NB>(mx, mn)));
+          if (lane == 0) s_wmax[i & 3][sl][mw] = m;
         }
-        const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<16>(mx, mn)));
-        if (lane == 0) s_wmax[i & 3][mw] = m;
         if constexpr (MODE == kTcSpec) {
           // exact W of the top stage per lane (the packed S / D above may wrap
           // at |W| = 2^16), stored at u = u_c * 256 + u_r with
           // u_c = lane + 2 k (+ 128 for the diff) -- 32 consecutive u_r per
           // warp store, 128 B coalesced
           uint32_t vi, bpi;
-          item_at<MODE>(a, t_lo + i, vi, bpi);
+          item_at<MODE, NB>(a, t_lo + i, vi, bpi);
           int32_t* row = a.out + int64_t(vi - a.v_lo) * a.ld + u;
 #pragma unroll
           for (int k = 0; k < 64; ++k) {
@@ -670,19 +735,39 @@ bool tc_path_enabled() {
 }
 
 namespace {
-template <int MODE>
+// per-device constant-operand image, built on first use (kept for the
+// process lifetime, like the library's other per-device state)
+std::mutex g_consts_mu;
+uint8_t* g_consts[64] = {};
+int tc_consts(int dev, cudaStream_t st, const uint8_t** out) {
+  std::lock_guard<std::mutex> lk(g_consts_mu);
+  if (!g_consts[dev & 63]) {
+    uint8_t* p = nullptr;
+    SBW_CUDA_CHECK(cudaMalloc(&p, kBOff));
+    k_tc_consts<<<64, 256, 0, st>>>(p);
+    SBW_LAUNCH_CHECK("k_tc_consts");
+    SBW_CUDA_CHECK(cudaStreamSynchronize(st));  // later launches may use other streams
+    g_consts[dev & 63] = p;
+  }
+  *out = g_consts[dev & 63];
+  return SBW_OK;
+}
+
+template <int MODE, int NB = 16>
 int run_tc_hybrid(const TcArgs& a, int64_t items, cudaStream_t st) {
   if (items <= 0) return SBW_OK;
   DeviceProps dp;
   if (int rc = device_props(&dp)) return rc;
   static unsigned long long attr_done = 0;  // per device; the call is idempotent
   if (!(attr_done >> (dp.device & 63) & 1ull)) {
-    SBW_CUDA_CHECK(cudaFuncSetAttribute(k_tc_hybrid<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SBW_CUDA_CHECK(cudaFuncSetAttribute(k_tc_hybrid<MODE, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         kTcSmem));
     attr_done |= 1ull << (dp.device & 63);
   }
+  TcArgs args = a;
+  if (int rc = tc_consts(dp.device, st, &args.consts)) return rc;
   const int grid = int(items < dp.sm_count ? items : dp.sm_count);
-  k_tc_hybrid<MODE><<<grid, kAllThreads, kTcSmem, st>>>(a);
+  k_tc_hybrid<MODE, NB><<<grid, kAllThreads, kTcSmem, st>>>(args);
   SBW_LAUNCH_CHECK(MODE == kTcEmit ? "k_tc_hybrid<emit>" : (MODE == kTcSpec ? "k_tc_hybrid<spec>" : "k_tc_hybrid<nl>"));
   return SBW_OK;
 }
@@ -698,6 +783,27 @@ int launch_tc16_nl(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t
   a.max_abs = max_abs;
   a.key = key;
   return run_tc_hybrid<kTcNL>(a, int64_t(v_hi) - v_lo, st);
+}
+
+int launch_tc_nl_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
+                       unsigned long long* key, cudaStream_t st) {
+  TcArgs a{};
+  a.planes = planes;
+  a.plane_words = (int64_t(1) << n) >> 5;
+  a.v_lo = v_lo;
+  a.v_hi = v_hi;
+  a.max_abs = max_abs;
+  a.key = key;
+  const int lc = 16 - n;
+  const int64_t items = ((int64_t(v_hi) - 1) >> lc) + 1 - (int64_t(v_lo) >> lc);
+  switch (n) {
+    case 11: return run_tc_hybrid<kTcNL, 11>(a, items, st);
+    case 12: return run_tc_hybrid<kTcNL, 12>(a, items, st);
+    case 13: return run_tc_hybrid<kTcNL, 13>(a, items, st);
+    case 14: return run_tc_hybrid<kTcNL, 14>(a, items, st);
+    case 15: return run_tc_hybrid<kTcNL, 15>(a, items, st);
+    default: return set_error(SBW_EINVAL, "tensor-core NL for n < 16 needs n in 11..15");
+  }
 }
 
 int launch_tc16_spec(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,

@@ -126,3 +126,17 @@ def test_multipass_tensor_core_pass_a(n, m, seed, lo, hi):
     s = sw.generate_sbox(n, m, seed, bijective=False)
     got, _ = _maxima(s, lo, hi)
     assert np.array_equal(got, orc.component_max_abs(s.table, n, lo, hi))
+
+
+@pytest.mark.parametrize("n,m,lo,hi", [(15, 1, 1, 2), (15, 15, 1, 1 << 15), (14, 2, 1, 4), (14, 14, 5, 3001),
+                                       (13, 3, 1, 8), (13, 16, 1000, 1901), (12, 4, 1, 16), (12, 12, 1, 4096),
+                                       (11, 5, 1, 32), (11, 11, 17, 2000), (11, 20, 123456, 124000)])
+def test_small_n_tensor_core_slots(n, m, lo, hi):
+    """n = 11..15 NL packs 2^(16-n) components per tile (slots); ranges that
+    start / end inside an item, the item holding v = 0, m = 16 - n exactly."""
+    s = sw.generate_sbox(n, m, 40 + n, bijective=(n == m))
+    got, (nl, v, mxw) = _maxima(s, lo, hi)
+    want = orc.component_max_abs(s.table, n, lo, hi)
+    assert np.array_equal(got, want)
+    i = int(np.argmax(want))
+    assert (v, mxw) == (lo + i, int(want[i]))
