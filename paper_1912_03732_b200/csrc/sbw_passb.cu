@@ -74,12 +74,13 @@ int run_passb_staged(const PassBArgs& a, cudaStream_t st) {
   static unsigned long long attr_done = 0;
   if (!(attr_done >> (dp.device & 63) & 1ull)) {
     SBW_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(kPassBSmem)));
+                                        int(kStagedSmem)));
     attr_done |= 1ull << (dp.device & 63);
   }
-  const int64_t items = a.n_comp * ChunkShape<H, 512>::PER_COMP;
-  const int grid = int(items < dp.sm_count ? items : dp.sm_count);
-  kern<<<grid, 512, kPassBSmem, st>>>(a);
+  const int64_t items = a.n_comp * StagedShape<H>::PER_COMP;
+  const int64_t slots = 2 * int64_t(dp.sm_count);  // two CTAs per SM
+  const int grid = int(items < slots ? items : slots);
+  kern<<<grid, kStagedThreads, kStagedSmem, st>>>(a);
   SBW_LAUNCH_CHECK("k_passb_staged");
   return SBW_OK;
 }

@@ -10,9 +10,9 @@
 // stage order is free because the butterflies of different bits commute.
 //
 //   H <= 5: k_passb_regs   -- registers only, one thread per pair-column.
-//   H >= 6: k_passb_staged -- cp.async-staged [2^H rows x 32 pair-columns]
-//           chunks, two register passes through a 128 KiB int32 tile, the
-//           next chunk prefetched while the current one computes.
+//   H >= 6: k_passb_staged -- cp.async-staged [2^H rows x 2^(13-H) pair-columns]
+//           chunks, two register passes through a 64 KiB fp32 tile, the next
+//           chunk prefetched while the current one computes.
 #pragma once
 
 #include "sbw_tile_simd.cuh"
@@ -34,6 +34,35 @@ struct PassBArgs {
 __device__ __forceinline__ int lo_half(uint32_t u) { return int(u & 0xFFFFu) - 16384; }
 __device__ __forceinline__ int hi_half(uint32_t u) { return int(u >> 16) - 16384; }
 
+// The same halves as exact fp32 integers: PRMT places the u16 under the
+// exponent of 2^23 (0x4B000000 | s == 2^23 + s as a float), one FADD removes
+// 2^23 + 2^14.  Pass B of max|W| runs its butterflies in fp32 on the FMA pipe
+// (4 warp-instr/clk/SM, twice the IADD3 rate): every intermediate is an
+// integer with |h| <= 2^(n-1) <= 2^23, which fp32 represents exactly, and the
+// sum of two such values is rounded only above 2^24, so the arithmetic is
+// bit-exact (K3).
+__device__ __forceinline__ float lo_half_f(uint32_t u) {
+  return __int_as_float(int(__byte_perm(u, 0x4B000000u, 0x7610))) - 8404992.0f;
+}
+__device__ __forceinline__ float hi_half_f(uint32_t u) {
+  return __int_as_float(int(__byte_perm(u, 0x4B000000u, 0x7632))) - 8404992.0f;
+}
+
+template <int LEN, int S0, int SEND>
+__device__ __forceinline__ void fwht_regs_f(float (&e)[LEN]) {
+#pragma unroll
+  for (int s = S0; s < SEND; s <<= 1) {
+#pragma unroll
+    for (int i = 0; i < LEN; ++i) {
+      if ((i & s) == 0) {
+        const float a = e[i], b = e[i + s];
+        e[i] = __fadd_rn(a, b);
+        e[i + s] = __fsub_rn(a, b);
+      }
+    }
+  }
+}
+
 // Reduce a per-thread partial max over the CTA and publish it (all threads of
 // a CTA belong to the same component by construction).
 __device__ __forceinline__ void cta_publish_max(int mx, int* s_red, int32_t* slot,
@@ -51,31 +80,43 @@ __device__ __forceinline__ void cta_publish_max(int mx, int* s_red, int32_t* slo
   __syncthreads();
 }
 
-// ---- pass-B chunk bodies (called by every thread of the CTA) --------------
-// A chunk's u16-pair words are first staged in shared memory by cp.async.cg
-// (16-byte pieces, L2 only: the persistent kernel reuses ring slots, so an
-// SM's L1 may hold lines of an older component).  Staging is asynchronous, so
-// the copy of chunk i+1 overlaps the arithmetic of chunk i.
+// ---- H = 6..9: staged chunks ---------------------------------------------
+// A chunk is 2^H rows (x bits 15..n-1) x CW = 2^(13-H) pair-columns: 8192
+// u16-pair words.  Its words are first staged in shared memory by cp.async.cg
+// (16-byte pieces, L2 only: the persistent kernel reuses its staging buffer, so
+// an SM's L1 may hold lines of an older component); the copy of the CTA's next
+// chunk overlaps the arithmetic of the current one.  B1 runs row bits
+// H2..H-1 from the staging buffer into a 64 KiB fp32-pair tile, B2 runs row
+// bits 0..H2-1 with the fused top stage.  96 KiB per CTA, two 256-thread CTAs
+// per SM, so one CTA's barriers and staging waits overlap the other's
+// arithmetic.  Every warp access is 32 consecutive words (B1, staging) or two
+// contiguous 128-byte half-warp rows (tile), so shared memory is conflict-free.
+constexpr int kStagedThreads = 256;
 
-template <int H, int THREADS>
-struct ChunkShape {
-  static constexpr int R = 1 << H;                 // rows (x bits 15..n-1)
-  static constexpr int CW = H <= 5 ? THREADS : 32; // pair-columns (words) per chunk
-  static constexpr int64_t PER_COMP = (int64_t(1) << 14) / CW;
-  static constexpr int PIECES = R * CW / 4;        // 16-byte pieces
+template <int H>
+struct StagedShape {
+  static constexpr int LCW = 13 - H;               // log2 pair-columns per chunk
+  static constexpr int CW = 1 << LCW;
+  static constexpr int H1 = (H + 1) / 2;           // B1 stages (row bits H2..H-1)
+  static constexpr int H2 = H - H1;                // B2 stages (row bits 0..H2-1)
+  static constexpr int64_t PER_COMP = (int64_t(1) << 14) >> LCW;
+  static constexpr int WORDS = CW << H;            // 8192
 };
+constexpr size_t kStagedSmem = size_t(8192) * 4 + size_t(8192) * 8;  // staging + tile
 
 // Issue (not wait for) the copies of chunk `chunk` of a component whose
-// scratch starts at `comp_base` into `stg` ([R][CW] words).
-template <int H, int THREADS>
+// scratch starts at `comp_base` into `stg` ([2^H][CW] words).
+template <int H>
 __device__ __forceinline__ void stage_chunk(const uint32_t* comp_base, int64_t chunk, uint32_t* stg) {
-  using S = ChunkShape<H, THREADS>;
-  constexpr int PR = S::CW / 4;  // pieces per row
-  const int64_t col0 = chunk * S::CW;
-  for (int p = threadIdx.x; p < S::PIECES; p += THREADS) {
-    const int r = p / PR, q = p - (p / PR) * PR;
-    const uint32_t* g = comp_base + (int64_t(r) << 14) + col0 + 4 * q;
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(stg + r * S::CW + 4 * q));
+  using S = StagedShape<H>;
+  constexpr int PR = S::CW / 4;  // 16-byte pieces per row
+  const uint32_t* g0 = comp_base + chunk * S::CW;
+#pragma unroll
+  for (int k = 0; k < S::WORDS / 4 / kStagedThreads; ++k) {
+    const int p = threadIdx.x + k * kStagedThreads;
+    const int r = p / PR, q = p % PR;
+    const uint32_t* g = g0 + (int64_t(r) << 14) + 4 * q;
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(stg + 4 * p));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -86,63 +127,63 @@ __device__ __forceinline__ void stage_wait() {
   __syncthreads();
 }
 
-// H = 6..9: 32 pair-columns x 2^H rows.  B1 runs row bits 0..4 from the
-// staging buffer and parks int32 pairs in `tile`; B2 runs row bits 5..H-1
-// with the fused top stage.
 template <int H, int MODE, typename AfterRead>
-__device__ __forceinline__ void passb_smem_chunk(const PassBArgs& a, int64_t comp, int64_t chunk,
-                                                 const uint32_t* stg, int2* tile, int* s_red,
-                                                 AfterRead after_read) {
-  constexpr int H2 = H - 5;
-  constexpr int N2 = 1 << H2;
-  const int64_t col0 = chunk * 32;
-  for (int task = threadIdx.x; task < 32 * N2; task += blockDim.x) {
-    const int c = task & 31, rh = task >> 5;
-    int e[64];
+__device__ __forceinline__ void passb_staged_chunk(const PassBArgs& a, int64_t comp, int64_t chunk,
+                                                   const uint32_t* stg, float2* tile, int* s_red,
+                                                   AfterRead after_read) {
+  using S = StagedShape<H>;
+  constexpr int N1 = 1 << S::H1, N2 = 1 << S::H2;
+#pragma unroll 1
+  for (int task = threadIdx.x; task < (S::CW << S::H2); task += kStagedThreads) {
+    const int c = task & (S::CW - 1), rb = task >> S::LCW;
+    float e[2 * N1];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const uint32_t u = stg[((rh << 5) | i) * 32 + c];
-      e[2 * i] = lo_half(u);
-      e[2 * i + 1] = hi_half(u);
+    for (int i = 0; i < N1; ++i) {
+      const uint32_t u = stg[(rb + (i << S::H2)) * S::CW + c];
+      e[2 * i] = lo_half_f(u);
+      e[2 * i + 1] = hi_half_f(u);
     }
-    fwht_regs<64, 2>(e);
+    fwht_regs_f<2 * N1, 2, 2 * N1>(e);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) tile[((rh << 5) | i) * 32 + c] = make_int2(e[2 * i], e[2 * i + 1]);
+    for (int i = 0; i < N1; ++i)
+      tile[(rb + (i << S::H2)) * S::CW + c] = make_float2(e[2 * i], e[2 * i + 1]);
   }
   __syncthreads();
   after_read();
+  float mf = 0.f;
   int mx = 0;
-  for (int task = threadIdx.x; task < 32 * 32; task += blockDim.x) {
-    const int c = task & 31, rl = task >> 5;
-    int e[2 * N2];
+#pragma unroll 1
+  for (int task = threadIdx.x; task < (S::CW << S::H1); task += kStagedThreads) {
+    const int c = task & (S::CW - 1), g = task >> S::LCW;
+    float e[2 * N2];
 #pragma unroll
-    for (int i = 0; i < N2; ++i) {
-      const int2 p = tile[((i << 5) | rl) * 32 + c];
-      e[2 * i] = p.x;
-      e[2 * i + 1] = p.y;
+    for (int j = 0; j < N2; ++j) {
+      const float2 p = tile[((g << S::H2) + j) * S::CW + c];
+      e[2 * j] = p.x;
+      e[2 * j + 1] = p.y;
     }
-    fwht_regs_until<2 * N2, 2, N2>(e);
+    fwht_regs_f<2 * N2, 2, N2>(e);
     if constexpr (MODE == MODE_NL) {
-      int m2 = 0;
 #pragma unroll
-      for (int k = 0; k < N2; ++k) m2 = max(m2, abs(e[k]) + abs(e[k + N2]));
-      mx = max(mx, 2 * m2);
+      for (int k = 0; k < N2; ++k) mf = fmaxf(mf, __fadd_rn(fabsf(e[k]), fabsf(e[k + N2])));
     } else {
+      int w[2 * N2];
 #pragma unroll
       for (int k = 0; k < N2; ++k) {
-        const int p = e[k], q = e[k + N2];
-        e[k] = 2 * (p + q);
-        e[k + N2] = 2 * (p - q);
-        mx = max(mx, max(abs(e[k]), abs(e[k + N2])));
+        const float p = e[k], q = e[k + N2];  // W / 2, exact below 2^24
+        w[k] = 2 * __float2int_rn(__fadd_rn(p, q));
+        w[k + N2] = 2 * __float2int_rn(__fsub_rn(p, q));
+        mx = max(mx, max(abs(w[k]), abs(w[k + N2])));
       }
-      int32_t* dst = a.out + (a.out_row0 + comp) * a.ld + 2 * (col0 + c);
+      int32_t* dst = a.out + (a.out_row0 + comp) * a.ld + 2 * (chunk * S::CW + c);
 #pragma unroll
-      for (int i = 0; i < N2; ++i) {
-        const int64_t row = (int64_t(i) << 5) | rl;
-        *reinterpret_cast<int2*>(dst + (row << 15)) = make_int2(e[2 * i], e[2 * i + 1]);
+      for (int j = 0; j < N2; ++j) {
+        const int64_t row = (int64_t(g) << S::H2) + j;
+        __stcs(reinterpret_cast<int2*>(dst + (row << 15)), make_int2(w[2 * j], w[2 * j + 1]));
       }
     }
   }
+  if constexpr (MODE == MODE_NL) mx = 2 * __float2int_rn(mf);
   cta_publish_max(mx, s_red, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
 }
 
@@ -194,33 +235,28 @@ __global__ void __launch_bounds__(kPassBThreads) k_passb_regs(PassBArgs a) {
   }
 }
 
-// H = 6..9 standalone pass B for the batched path: grid-stride over
-// (component, chunk) items; each item's u16 rows are staged with cp.async and
-// the CTA's next item is prefetched as soon as the current staging is consumed.
-constexpr size_t kPassBSmem = size_t(kTileWords) * sizeof(uint32_t) + (size_t(64) << 10);
-
+// H = 6..9 standalone pass B: grid-stride over (component, chunk) items; each
+// item's u16 rows are staged with cp.async and the CTA's next item is
+// prefetched as soon as B1 has consumed the current staging.
 template <int H, int MODE>
-__global__ void __launch_bounds__(512, 1) k_passb_staged(PassBArgs a) {
-  constexpr int THREADS = 512;
-  using S = ChunkShape<H, THREADS>;
-  extern __shared__ uint4 smem4[];  // [128 KiB int32 tile][64 KiB staging]
-  uint32_t* stg = reinterpret_cast<uint32_t*>(smem4) + kTileWords;
-  __shared__ int s_red[THREADS / 32];
+__global__ void __launch_bounds__(kStagedThreads, 2) k_passb_staged(PassBArgs a) {
+  using S = StagedShape<H>;
+  extern __shared__ uint4 smem4[];  // [32 KiB staging][64 KiB fp32-pair tile]
+  uint32_t* stg = reinterpret_cast<uint32_t*>(smem4);
+  float2* tile = reinterpret_cast<float2*>(stg + S::WORDS);
+  __shared__ int s_red[kStagedThreads / 32];
   const int64_t items = a.n_comp * S::PER_COMP;
   const int64_t comp_words = int64_t(1) << (a.n - 1);
   int64_t b = blockIdx.x;
-  if (b < items) stage_chunk<H, THREADS>(a.scratch + (b / S::PER_COMP) * comp_words,
-                                         b % S::PER_COMP, stg);
+  if (b < items) stage_chunk<H>(a.scratch + (b / S::PER_COMP) * comp_words, b % S::PER_COMP, stg);
   for (; b < items; b += gridDim.x) {
     stage_wait();
     const int64_t nxt = b + gridDim.x;
     auto prefetch = [&]() {
       if (nxt < items)
-        stage_chunk<H, THREADS>(a.scratch + (nxt / S::PER_COMP) * comp_words,
-                                nxt % S::PER_COMP, stg);
+        stage_chunk<H>(a.scratch + (nxt / S::PER_COMP) * comp_words, nxt % S::PER_COMP, stg);
     };
-    passb_smem_chunk<H, MODE>(a, b / S::PER_COMP, b % S::PER_COMP, stg,
-                              reinterpret_cast<int2*>(smem4), s_red, prefetch);
+    passb_staged_chunk<H, MODE>(a, b / S::PER_COMP, b % S::PER_COMP, stg, tile, s_red, prefetch);
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
