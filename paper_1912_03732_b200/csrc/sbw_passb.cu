@@ -59,8 +59,14 @@ template <int H, int MODE>
 int run_passb_regs(const PassBArgs& a, cudaStream_t st) {
   DeviceProps dp;
   if (int rc = device_props(&dp)) return rc;
+  // one resident wave: each CTA owns a contiguous item range
+  static int per_sm[64][10][2] = {};
+  int& occ = per_sm[dp.device & 63][H][MODE == MODE_NL ? 0 : 1];
+  if (occ == 0)
+    SBW_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_passb_regs<H, MODE>,
+                                                                 kPassBThreads, 0));
   const int64_t ctas = a.n_comp * ((int64_t(1) << 14) / kPassBThreads);
-  const int64_t cap = int64_t(dp.sm_count) * 8;
+  const int64_t cap = int64_t(dp.sm_count) * (occ > 0 ? occ : 1);
   k_passb_regs<H, MODE><<<int(ctas < cap ? ctas : cap), kPassBThreads, 0, st>>>(a);
   SBW_LAUNCH_CHECK("k_passb_regs");
   return SBW_OK;

@@ -1,15 +1,17 @@
 // Multi-pass path for n = 17..24 ("K3"), pass B.
 //
-// Pass A (k_tile_simd<15, MODE_EMIT>, one 1024-thread launch per batch of
-// components) leaves, for every component of the batch, 2^(n-15) blocks of
-// 2^15 partial transforms (x bits 0..14 done), each as the biased u16
-// s = (v + 2^15) / 2 in [0, 2^15].  Pass B runs the remaining H = n - 15
-// stages over x bits 15..n-1, i.e. across blocks, on v / 2 = s - 2^14 in
-// int32, and fuses max|W| into the top stage like the on-chip kernel.  The
-// reference does all n stages on one numpy array per mask (walsh.py:91-103);
-// stage order is free because the butterflies of different bits commute.
+// Pass A (k_tc_hybrid<kTcEmit> in sbw_tc.cu, or k_tile_simd<15, MODE_EMIT>
+// with SBW_TC=0; one launch per batch of components) leaves, for every
+// component of the batch, 2^(n-15) blocks of 2^15 partial transforms (x bits
+// 0..14 done), each as the biased u16 s = (v + 2^15) / 2 in [0, 2^15].  Pass
+// B runs the remaining H = n - 15 stages over x bits 15..n-1, i.e. across
+// blocks, on v / 2 = s - 2^14 in exact fp32, and fuses max|W| into the top
+// stage like the on-chip kernel.  The reference does all n stages on one
+// numpy array per mask (walsh.py:91-103); stage order is free because the
+// butterflies of different bits commute.
 //
-//   H <= 5: k_passb_regs   -- registers only, one thread per pair-column.
+//   H <= 5: k_passb_regs   -- registers only, one thread per pair-column,
+//           barrier-free.
 //   H >= 6: k_passb_staged -- cp.async-staged [2^H rows x 2^(13-H) pair-columns]
 //           chunks, two register passes through a 64 KiB fp32 tile, the next
 //           chunk prefetched while the current one computes.
@@ -31,11 +33,8 @@ struct PassBArgs {
   int64_t ld;
 };
 
-__device__ __forceinline__ int lo_half(uint32_t u) { return int(u & 0xFFFFu) - 16384; }
-__device__ __forceinline__ int hi_half(uint32_t u) { return int(u >> 16) - 16384; }
-
-// The same halves as exact fp32 integers: PRMT places the u16 under the
-// exponent of 2^23 (0x4B000000 | s == 2^23 + s as a float), one FADD removes
+// The u16 halves (v / 2 = s - 2^14) as exact fp32 integers: PRMT places the
+// u16 under the exponent of 2^23 (0x4B000000 | s == 2^23 + s as a float), one FADD removes
 // 2^23 + 2^14.  Pass B of max|W| runs its butterflies in fp32 on the FMA pipe
 // (4 warp-instr/clk/SM, twice the IADD3 rate): every intermediate is an
 // integer with |h| <= 2^(n-1) <= 2^23, which fp32 represents exactly, and the
@@ -61,23 +60,6 @@ __device__ __forceinline__ void fwht_regs_f(float (&e)[LEN]) {
       }
     }
   }
-}
-
-// Reduce a per-thread partial max over the CTA and publish it (all threads of
-// a CTA belong to the same component by construction).
-__device__ __forceinline__ void cta_publish_max(int mx, int* s_red, int32_t* slot,
-                                                unsigned long long* key, uint32_t v) {
-  mx = warp_max(mx);
-  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if ((threadIdx.x & 31) == 0) s_red[warp] = mx;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int m = 0;
-    for (int w = 0; w < nw; ++w) m = max(m, s_red[w]);
-    atomicMax(slot, m);
-    if (key) atomicMax(key, nl_key(m, v));
-  }
-  __syncthreads();
 }
 
 // ---- H = 6..9: staged chunks ---------------------------------------------
@@ -127,10 +109,11 @@ __device__ __forceinline__ void stage_wait() {
   __syncthreads();
 }
 
+// Returns this thread's max|W| over the chunk.
 template <int H, int MODE, typename AfterRead>
-__device__ __forceinline__ void passb_staged_chunk(const PassBArgs& a, int64_t comp, int64_t chunk,
-                                                   const uint32_t* stg, float2* tile, int* s_red,
-                                                   AfterRead after_read) {
+__device__ __forceinline__ int passb_staged_chunk(const PassBArgs& a, int64_t comp, int64_t chunk,
+                                                  const uint32_t* stg, float2* tile,
+                                                  AfterRead after_read) {
   using S = StagedShape<H>;
   constexpr int N1 = 1 << S::H1, N2 = 1 << S::H2;
 #pragma unroll 1
@@ -184,59 +167,79 @@ __device__ __forceinline__ void passb_staged_chunk(const PassBArgs& a, int64_t c
     }
   }
   if constexpr (MODE == MODE_NL) mx = 2 * __float2int_rn(mf);
-  cta_publish_max(mx, s_red, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
+  return mx;
+}
+
+// Per-warp publish of a component's running max (no CTA barrier).
+__device__ __forceinline__ void warp_publish_max(int mx, int32_t* slot, unsigned long long* key,
+                                                 uint32_t v) {
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(slot, mx);
+    if (key) atomicMax(key, nl_key(mx, v));
+  }
 }
 
 // ---- batched path for H <= 5 (n = 17..20) -----------------------------------
-// Pass A runs as standalone 1024-thread EMIT tile launches over a batch of
-// components; this kernel then runs the remaining H stages.  One thread owns
-// one pair-column (2^H rows, 2^(H+1) ints), 256-thread CTAs at high occupancy.
-// Launch boundaries invalidate L1, so plain (evict-first) loads are safe.
+// Pass A runs as standalone EMIT tile launches over a batch of components;
+// this kernel then runs the remaining H stages.  One thread owns one
+// pair-column (2^H rows, 2^(H+1) fp32 values, exact as in pass B staged),
+// 256-thread CTAs at high occupancy, each CTA one contiguous range of
+// (component, 256-column) items with no barrier: warps drift apart, so one
+// warp's loads overlap another's arithmetic.  Launch boundaries invalidate L1,
+// so plain (evict-first) loads are safe.
 constexpr int kPassBThreads = 256;
 
 template <int H, int MODE>
 __global__ void __launch_bounds__(kPassBThreads) k_passb_regs(PassBArgs a) {
   constexpr int NI = 1 << H;
-  __shared__ int s_red[kPassBThreads / 32];
-  const int64_t chunks = (int64_t(1) << 14) / kPassBThreads;  // per component
-  for (int64_t b = blockIdx.x; b < a.n_comp * chunks; b += gridDim.x) {
+  constexpr int64_t chunks = (int64_t(1) << 14) / kPassBThreads;  // per component
+  const int64_t items = a.n_comp * chunks;
+  const int64_t per_cta = (items + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per_cta;
+  const int64_t b1 = b0 + per_cta < items ? b0 + per_cta : items;
+  int run = 0;
+  for (int64_t b = b0; b < b1; ++b) {
     const int64_t comp = b / chunks;
     const int64_t col = (b % chunks) * kPassBThreads + threadIdx.x;
     const uint32_t* src = a.scratch + (comp << (a.n - 1)) + col;
     uint32_t u[NI];
 #pragma unroll
     for (int i = 0; i < NI; ++i) u[i] = __ldcs(src + (int64_t(i) << 14));
-    int e[2 * NI];
+    float e[2 * NI];
 #pragma unroll
     for (int i = 0; i < NI; ++i) {
-      e[2 * i] = lo_half(u[i]);
-      e[2 * i + 1] = hi_half(u[i]);
+      e[2 * i] = lo_half_f(u[i]);
+      e[2 * i + 1] = hi_half_f(u[i]);
     }
-    fwht_regs_until<2 * NI, 2, NI>(e);
-    int mx = 0;
+    fwht_regs_f<2 * NI, 2, NI>(e);
     if constexpr (MODE == MODE_NL) {
+      float mf = 0.f;
 #pragma unroll
-      for (int k = 0; k < NI; ++k) mx = max(mx, abs(e[k]) + abs(e[k + NI]));
-      mx *= 2;  // values are halved
+      for (int k = 0; k < NI; ++k) mf = fmaxf(mf, __fadd_rn(fabsf(e[k]), fabsf(e[k + NI])));
+      run = max(run, 2 * __float2int_rn(mf));  // values are halved
     } else {
+      int w[2 * NI];
 #pragma unroll
       for (int k = 0; k < NI; ++k) {
-        const int p = e[k], q = e[k + NI];
-        e[k] = 2 * (p + q);
-        e[k + NI] = 2 * (p - q);
-        mx = max(mx, max(abs(e[k]), abs(e[k + NI])));
+        const float p = e[k], q = e[k + NI];
+        w[k] = 2 * __float2int_rn(__fadd_rn(p, q));
+        w[k + NI] = 2 * __float2int_rn(__fsub_rn(p, q));
+        run = max(run, max(abs(w[k]), abs(w[k + NI])));
       }
       int32_t* dst = a.out + (a.out_row0 + comp) * a.ld + 2 * col;
 #pragma unroll
       for (int i = 0; i < NI; ++i)
-        *reinterpret_cast<int2*>(dst + (int64_t(i) << 15)) = make_int2(e[2 * i], e[2 * i + 1]);
+        __stcs(reinterpret_cast<int2*>(dst + (int64_t(i) << 15)), make_int2(w[2 * i], w[2 * i + 1]));
     }
-    cta_publish_max(mx, s_red, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
+    if (b + 1 >= b1 || (b + 1) / chunks != comp) {  // CTA-uniform
+      warp_publish_max(run, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
+      run = 0;
+    }
   }
 }
 
-// H = 6..9 standalone pass B: grid-stride over (component, chunk) items; each
-// item's u16 rows are staged with cp.async and the CTA's next item is
+// H = 6..9 standalone pass B over (component, chunk) items; each item's u16 rows are staged with cp.async and the CTA's next item is
 // prefetched as soon as B1 has consumed the current staging.
 template <int H, int MODE>
 __global__ void __launch_bounds__(kStagedThreads, 2) k_passb_staged(PassBArgs a) {
@@ -244,19 +247,27 @@ __global__ void __launch_bounds__(kStagedThreads, 2) k_passb_staged(PassBArgs a)
   extern __shared__ uint4 smem4[];  // [32 KiB staging][64 KiB fp32-pair tile]
   uint32_t* stg = reinterpret_cast<uint32_t*>(smem4);
   float2* tile = reinterpret_cast<float2*>(stg + S::WORDS);
-  __shared__ int s_red[kStagedThreads / 32];
+  // Each CTA owns one contiguous range of items, so it meets few component
+  // boundaries and publishes (per warp, no barrier) only at those.
   const int64_t items = a.n_comp * S::PER_COMP;
+  const int64_t per_cta = (items + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per_cta;
+  const int64_t b1 = b0 + per_cta < items ? b0 + per_cta : items;
   const int64_t comp_words = int64_t(1) << (a.n - 1);
-  int64_t b = blockIdx.x;
-  if (b < items) stage_chunk<H>(a.scratch + (b / S::PER_COMP) * comp_words, b % S::PER_COMP, stg);
-  for (; b < items; b += gridDim.x) {
-    stage_wait();
-    const int64_t nxt = b + gridDim.x;
+  if (b0 < b1) stage_chunk<H>(a.scratch + (b0 / S::PER_COMP) * comp_words, b0 % S::PER_COMP, stg);
+  int run = 0;  // running max over this CTA's chunks of the current component
+  for (int64_t b = b0; b < b1; ++b) {
+    stage_wait();  // also orders the previous chunk's B2 tile reads before this B1
+    const int64_t comp = b / S::PER_COMP, nxt = b + 1;
     auto prefetch = [&]() {
-      if (nxt < items)
+      if (nxt < b1)
         stage_chunk<H>(a.scratch + (nxt / S::PER_COMP) * comp_words, nxt % S::PER_COMP, stg);
     };
-    passb_staged_chunk<H, MODE>(a, b / S::PER_COMP, b % S::PER_COMP, stg, tile, s_red, prefetch);
+    run = max(run, passb_staged_chunk<H, MODE>(a, comp, b % S::PER_COMP, stg, tile, prefetch));
+    if (nxt >= b1 || nxt / S::PER_COMP != comp) {  // CTA-uniform
+      warp_publish_max(run, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
+      run = 0;
+    }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
