@@ -39,6 +39,11 @@ int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_co
 
 // Multi-pass path (n >= 17): planes, then pass A (emit) + pass B per L2-sized batch.
 size_t k3_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi);
+// K3 pass B on the tensor cores (n = 22..24, NL only), sbw_passb_tc.cu;
+// SBW_PASSB_TC=0 keeps the fp32 k_passb_staged kernel.
+struct PassBArgs;
+bool passb_tc_enabled();
+int launch_passb_tc(const PassBArgs& a, cudaStream_t st);
 int launch_k3(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32_t v_hi,
               int32_t* max_abs, unsigned long long* key, int32_t* out, int64_t ld, void* scratch,
               size_t scratch_bytes, cudaStream_t st);

@@ -144,7 +144,8 @@ int launch_k3_batched(const uint32_t* planes, int n, int m, uint32_t v_lo, uint3
     a.out = out;
     a.ld = ld;
     const int rc = out ? dispatch_passb_regs<MODE_SPEC>(n - 15, a, ks->b)
-                       : dispatch_passb_regs<MODE_NL>(n - 15, a, ks->b);
+                       : (n >= 22 && passb_tc_enabled()) ? launch_passb_tc(a, ks->b)
+                                                         : dispatch_passb_regs<MODE_NL>(n - 15, a, ks->b);
     if (rc) return rc;
     SBW_CUDA_CHECK(cudaEventRecord(ks->done_b[buf], ks->b));
   }

@@ -33,18 +33,24 @@ struct PassBArgs {
   int64_t ld;
 };
 
-// The u16 halves (v / 2 = s - 2^14) as exact fp32 integers: PRMT places the
-// u16 under the exponent of 2^23 (0x4B000000 | s == 2^23 + s as a float), one FADD removes
-// 2^23 + 2^14.  Pass B of max|W| runs its butterflies in fp32 on the FMA pipe
-// (4 warp-instr/clk/SM, twice the IADD3 rate): every intermediate is an
-// integer with |h| <= 2^(n-1) <= 2^23, which fp32 represents exactly, and the
-// sum of two such values is rounded only above 2^24, so the arithmetic is
-// bit-exact (K3).
-__device__ __forceinline__ float lo_half_f(uint32_t u) {
-  return __int_as_float(int(__byte_perm(u, 0x4B000000u, 0x7610))) - 8404992.0f;
-}
-__device__ __forceinline__ float hi_half_f(uint32_t u) {
-  return __int_as_float(int(__byte_perm(u, 0x4B000000u, 0x7632))) - 8404992.0f;
+// Pass B of max|W| runs its butterflies in fp32 on the FMA pipe (FADD at 4
+// warp-instr/clk/SM, twice the IADD3 rate).  Every intermediate is an integer
+// with |h| <= 2^(n-1) <= 2^23, which fp32 represents exactly, and the sum of
+// two such values is rounded only above 2^24, so the arithmetic is bit-exact
+// (K3).  The u16 s = h + 2^14 enters by PRMT under the exponent of
+// 2^23 (0x4B000000 | s is the float 2^23 + s), and the first row stage absorbs
+// the bias: with A = 2^23 + s_a, B = 2^23 + s_b, h_a - h_b = A - B and
+// h_a + h_b = (A - (2^24 + 2^15)) + B, every partial an integer below 2^24 --
+// three FADDs per lane pair.  Rows ua (even) / ub (odd) -> e[0..3].
+__device__ __forceinline__ void load_rows_stage1(uint32_t ua, uint32_t ub, float* e) {
+  const float al = __int_as_float(int(__byte_perm(ua, 0x4B000000u, 0x7610)));
+  const float ah = __int_as_float(int(__byte_perm(ua, 0x4B000000u, 0x7632)));
+  const float bl = __int_as_float(int(__byte_perm(ub, 0x4B000000u, 0x7610)));
+  const float bh = __int_as_float(int(__byte_perm(ub, 0x4B000000u, 0x7632)));
+  e[0] = __fadd_rn(__fsub_rn(al, 16809984.0f), bl);
+  e[1] = __fadd_rn(__fsub_rn(ah, 16809984.0f), bh);
+  e[2] = __fsub_rn(al, bl);
+  e[3] = __fsub_rn(ah, bh);
 }
 
 template <int LEN, int S0, int SEND>
@@ -121,12 +127,10 @@ __device__ __forceinline__ int passb_staged_chunk(const PassBArgs& a, int64_t co
     const int c = task & (S::CW - 1), rb = task >> S::LCW;
     float e[2 * N1];
 #pragma unroll
-    for (int i = 0; i < N1; ++i) {
-      const uint32_t u = stg[(rb + (i << S::H2)) * S::CW + c];
-      e[2 * i] = lo_half_f(u);
-      e[2 * i + 1] = hi_half_f(u);
-    }
-    fwht_regs_f<2 * N1, 2, 2 * N1>(e);
+    for (int i = 0; i < N1; i += 2)
+      load_rows_stage1(stg[(rb + (i << S::H2)) * S::CW + c], stg[(rb + ((i + 1) << S::H2)) * S::CW + c],
+                       e + 2 * i);
+    fwht_regs_f<2 * N1, 4, 2 * N1>(e);
 #pragma unroll
     for (int i = 0; i < N1; ++i)
       tile[(rb + (i << S::H2)) * S::CW + c] = make_float2(e[2 * i], e[2 * i + 1]);
@@ -208,11 +212,8 @@ __global__ void __launch_bounds__(kPassBThreads) k_passb_regs(PassBArgs a) {
     for (int i = 0; i < NI; ++i) u[i] = __ldcs(src + (int64_t(i) << 14));
     float e[2 * NI];
 #pragma unroll
-    for (int i = 0; i < NI; ++i) {
-      e[2 * i] = lo_half_f(u[i]);
-      e[2 * i + 1] = hi_half_f(u[i]);
-    }
-    fwht_regs_f<2 * NI, 2, NI>(e);
+    for (int i = 0; i < NI; i += 2) load_rows_stage1(u[i], u[i + 1], e + 2 * i);
+    fwht_regs_f<2 * NI, 4, NI>(e);
     if constexpr (MODE == MODE_NL) {
       float mf = 0.f;
 #pragma unroll

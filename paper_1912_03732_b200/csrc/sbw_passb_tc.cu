@@ -1,0 +1,275 @@
+// K3 pass B on the tensor cores: n = 22..24 (H = n - 15 = 7..9), NL only.
+//
+// Pass A leaves, per component, 2^H rows (x bits 15..n-1) of 2^15 biased u16
+// s = h + 2^14 (h = W_15 / 2, sbw_passb.cuh).  The 7 row stages over x bits
+// 15..21 are one int8 GEMM per 128-row block g:
+//
+//   D_g[r'][c] = sum_r H_128[r'][r] * B_g[r][c],   B_g = the u16 rows of block
+//                g read as a u8 matrix (column 2e = low byte of element e,
+//                column 2e+1 = high byte),
+//
+// so H_128 (s8 +/-1, the A operand) times the raw scratch bytes (u8, the B
+// operand, MN-major exactly as they lie in HBM) gives W_g = D_g[2e] +
+// 256 D_g[2e+1] = H_128 s, exact in s32 (|D| <= 128 * 255).  The bias 2^14 of
+// s adds 2^14 * 128 = 2^21 to row r' = 0 only (H_128 * 1 = 128 e_0).  The
+// remaining H - 7 stages (across the G = 2^(H-7) blocks) and the max|W| fold
+// run on the ALU from TMEM: ~4 instructions per element instead of ~13 for
+// the fp32 pass (k_passb_staged), so the kernel is bound by the HBM read.
+//
+// Data path: TMA (2D tensor map over the batch scratch, SWIZZLE_64B boxes of
+// 64 B x <= 256 rows) -> 4..8-stage shared-memory ring -> tcgen05.mma
+// kind::i8 (M128 N64 K32, B MN-major SW64) -> double-buffered TMEM ->
+// tcgen05.ld by 8 epilogue warps.  One item = one component x 32 elements
+// (64 bytes) of every row.  The reference runs all n stages per mask in numpy
+// (walsh.py:91-103); stage order is free because butterflies commute.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
+#include "sbw_internal.cuh"
+#include "sbw_launch.h"
+#include "sbw_passb.cuh"
+#include "sbw_tc.cuh"
+
+namespace sbw {
+namespace {
+
+constexpr int kPbThreads = 64 + 256;  // warp 0 TMA producer, warp 1 MMA issuer, 8 epilogue warps
+constexpr int kPbAOff = 0;            // H_128, s8, K-major no-swizzle (16 KiB)
+constexpr int kPbBOff = 16384;        // stage ring, 1024-aligned
+constexpr int kPbRingBytes = 4 * 32768;
+constexpr size_t kPbSmem = size_t(kPbBOff) + kPbRingBytes + 1024;  // + alignment slack
+
+__device__ __forceinline__ void mbar_arrive_pb(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(tc::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+// MN-major SWIZZLE_64B descriptor: 8 K-rows x 64 B atoms (512 B, 512-aligned),
+// 16-byte chunk c of K-row i at chunk c ^ ((i >> 1) & 3); SBO = distance
+// between 8-row atoms along K; one atom spans the whole N = 64 extent, so LBO
+// is unused.
+__device__ __forceinline__ uint64_t sdesc_mn_sw64(uint32_t saddr, uint32_t sbo) {
+  return uint64_t((saddr & 0x3FFFFu) >> 4) | (uint64_t(1) << 16) | (uint64_t((sbo >> 4) & 0x3FFFu) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(4) << 61);
+}
+__device__ __forceinline__ void wait_ld_tied32(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+                 "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+                 "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]),
+                 "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]),
+                 "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+
+template <int H>
+struct PbShape {
+  static constexpr int G = 1 << (H - 7);                    // 128-row blocks
+  static constexpr int ROWS = 1 << H;
+  static constexpr int ITEM_BYTES = ROWS * 64;              // 32 elements of every row
+  static constexpr int BOX_ROWS = ROWS < 256 ? ROWS : 256;  // TMA box height
+  static constexpr int STAGES = kPbRingBytes / ITEM_BYTES > 8 ? 8 : kPbRingBytes / ITEM_BYTES;
+  static constexpr int TCOLS = G * 64;                      // TMEM columns per buffer
+  static constexpr int TALLOC = 2 * TCOLS;                  // 128 / 256 / 512
+  static constexpr int64_t PER_COMP = int64_t(1) << 10;     // items per component
+};
+
+template <int H>
+__global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constant__ CUtensorMap tmap, PassBArgs a) {
+  using S = PbShape<H>;
+  constexpr uint32_t kIdesc = tc::idesc_i8(128, 64, true, false) | (1u << 16);  // B MN-major
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[S::STAGES], empty[S::STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t items = a.n_comp * S::PER_COMP;
+  const int64_t per_cta = (items + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per_cta;
+  const int64_t b1 = b0 + per_cta < items ? b0 + per_cta : items;
+  const int n_my = b0 < b1 ? int(b1 - b0) : 0;
+
+  // A = H_128: core matrix (row group rg, 16-byte K chunk kc) at
+  // (rg * 8 + kc) * 128, row r & 7 at + 16 (r & 7)
+  for (int e = tid; e < 128 * 32; e += kPbThreads) {
+    const int r = e >> 5, k4 = (e & 31) * 4;
+    uint32_t w = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w |= ((__popc(r & (k4 + j)) & 1) ? 0xFFu : 0x01u) << (8 * j);
+    *reinterpret_cast<uint32_t*>(smem + kPbAOff + ((r >> 3) * 8 + (k4 >> 4)) * 128 + (r & 7) * 16 + (k4 & 15)) = w;
+  }
+  if (warp == 0) tc::tmem_alloc(&tmem_slot, S::TALLOC);
+  if (tid == 0) {
+    for (int s = 0; s < S::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], 256);
+    }
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (one thread) ----------------
+    if (lane == 0) {
+      for (int i = 0; i < n_my; ++i) {
+        const int s = i % S::STAGES;
+        if (i >= S::STAGES) tc::mbar_wait(&empty[s], uint32_t((i / S::STAGES - 1) & 1));
+        const int64_t b = b0 + i;
+        const int comp = int(b >> 10), q = int(b & 1023);
+        mbar_expect_tx(&full[s], S::ITEM_BYTES);
+#pragma unroll
+        for (int bx = 0; bx < S::ROWS / S::BOX_ROWS; ++bx)
+          tma_load_2d(smem + kPbBOff + s * S::ITEM_BYTES + bx * S::BOX_ROWS * 64, &tmap, q * 64,
+                      comp * S::ROWS + bx * S::BOX_ROWS, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t a_base = tc::smem_u32(smem + kPbAOff);
+    for (int i = 0; i < n_my; ++i) {
+      const int s = i % S::STAGES, buf = i & 1;
+      tc::mbar_wait(&full[s], uint32_t((i / S::STAGES) & 1));
+      if (i >= 2) tc::mbar_wait(&tempty[buf], uint32_t(((i >> 1) - 1) & 1));
+      tc::fence_after();
+      const uint32_t b_base = tc::smem_u32(smem + kPbBOff + s * S::ITEM_BYTES);
+#pragma unroll
+      for (int g = 0; g < S::G; ++g)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc::mma_i8_elect(tmem + buf * S::TCOLS + g * 64, tc::sdesc(a_base + k * 256, 128, 1024),
+                           sdesc_mn_sw64(b_base + (g * 128 + 32 * k) * 64, 512), kIdesc, k > 0 ? 1u : 0u);
+      tc::mma_commit_elect(&empty[s]);
+      tc::mma_commit_elect(&tfull[buf]);
+      __syncwarp();
+    }
+  } else {
+    // ---------------- epilogue: 8 warps, lane quarter warp & 3, column half ----------------
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int rr = quarter * 32 + lane;  // output row r' = TMEM lane
+    // row r' = 0 carries 2^21 per block from the bias of s
+    const int corr = rr == 0 ? -(S::G == 1 ? (1 << 21) : (1 << 22)) : 0;
+    const uint32_t t_lane = uint32_t(quarter * 32) << 16;
+    int run = 0;
+    for (int i = 0; i < n_my; ++i) {
+      const int buf = i & 1;
+      tc::mbar_wait(&tfull[buf], uint32_t((i >> 1) & 1));
+      tc::fence_after();
+      uint32_t d[S::G][32];
+#pragma unroll
+      for (int g = 0; g < S::G; ++g) tc::tmem_ld_x32(tmem + t_lane + buf * S::TCOLS + g * 64 + half * 32, d[g]);
+#pragma unroll
+      for (int g = 0; g < S::G; ++g) wait_ld_tied32(d[g]);
+      tc::fence_before();
+      mbar_arrive_pb(&tempty[buf]);
+      int m = 0;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        int w[S::G];
+#pragma unroll
+        for (int g = 0; g < S::G; ++g) w[g] = int(d[g][2 * e + 1]) * 256 + int(d[g][2 * e]);
+        if constexpr (S::G == 1) {
+          m = max(m, abs(w[0] + corr));
+        } else if constexpr (S::G == 2) {
+          m = __vimax3_s32(m, abs(w[0] + w[1] + corr), abs(w[0] - w[1]));
+        } else {
+          const int s01 = w[0] + w[1] + corr, d01 = w[0] - w[1];
+          const int s23 = w[2] + w[3] + corr, d23 = w[2] - w[3];
+          m = __vimax3_s32(m, abs(s01) + abs(s23), abs(d01) + abs(d23));
+        }
+      }
+      run = max(run, 2 * m);  // values are W / 2
+      const int64_t b = b0 + i, comp = b >> 10;
+      if (i + 1 >= n_my || ((b + 1) >> 10) != comp) {
+        warp_publish_max(run, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
+        run = 0;
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    __syncwarp();
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, S::TALLOC);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+template <int H>
+int run_passb_tc(const PassBArgs& a, cudaStream_t st) {
+  using S = PbShape<H>;
+  DeviceProps dp;
+  if (int rc = device_props(&dp)) return rc;
+  auto enc = encode_fn();
+  if (!enc) return set_error(SBW_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {cuuint64_t(1) << 16, cuuint64_t(a.n_comp) << H};  // bytes per row, rows
+  const cuuint64_t strides[1] = {cuuint64_t(1) << 16};
+  const cuuint32_t box[2] = {64, cuuint32_t(S::BOX_ROWS)};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint32_t*>(a.scratch), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(SBW_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  static unsigned long long attr_done = 0;
+  if (!(attr_done >> (dp.device & 63) & 1ull)) {
+    SBW_CUDA_CHECK(cudaFuncSetAttribute(k_passb_tc<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPbSmem)));
+    attr_done |= 1ull << (dp.device & 63);
+  }
+  const int64_t items = a.n_comp * S::PER_COMP;
+  const int grid = int(items < dp.sm_count ? items : dp.sm_count);
+  k_passb_tc<H><<<grid, kPbThreads, kPbSmem, st>>>(map, a);
+  SBW_LAUNCH_CHECK("k_passb_tc");
+  return SBW_OK;
+}
+
+}  // namespace
+
+bool passb_tc_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SBW_PASSB_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+int launch_passb_tc(const PassBArgs& a, cudaStream_t st) {
+  switch (a.n - 15) {
+    case 7: return run_passb_tc<7>(a, st);
+    case 8: return run_passb_tc<8>(a, st);
+    case 9: return run_passb_tc<9>(a, st);
+    default: return set_error(SBW_EINVAL, "tensor-core pass B needs n in 22..24");
+  }
+}
+
+}  // namespace sbw
