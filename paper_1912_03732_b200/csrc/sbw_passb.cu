@@ -19,10 +19,24 @@ namespace {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-// ---- batched two-kernel path for n = 17..20 ---------------------------------
-// Two scratch buffers of `bb` components (~1 GiB each): pass A of batch b+1
-// runs on one stream beside pass B of batch b on another.
-constexpr size_t kBatchBytes = size_t(1) << 30;  // per buffer (measured: bigger batches win)
+// ---- batched two-kernel path for n = 17..24 ---------------------------------
+// Two scratch buffers of `bb` components (~4 GiB each): pass A of batch b+1
+// runs on one stream beside pass B of batch b on another.  Each batch pays a
+// fixed ~20-30 us (kernel prologues, pipeline fill, launch gaps), so bigger
+// batches win: 24x16 full NL 1000 / 938 / 906 / 896 ms at 0.5 / 1 / 2 / 4 GiB,
+// 20x20 860 / 843 / 836 / 830 ms (SBW_K3_BATCH sweep).
+constexpr size_t kBatchBytes = size_t(4) << 30;  // per buffer
+
+// Smallest n whose NL pass B runs on the tensor cores (SBW_PASSB_TC_MIN_N
+// overrides).  Below n = 21 the GEMM is block-diagonal (H_(2^H) (x) I_P) and
+// does P times the useful MACs: at 20x20 the kernel alone is 4 % faster than
+// k_passb_regs (689 vs 717 us per 4 GiB batch, both HBM-bound) but the full
+// run is 5 % slower (870 vs 830 ms; the tensor work lowers the clock under
+// the power cap), so n <= 20 keeps the fp32 register kernel.
+const int kPassBTcMinN = [] {
+  const char* e = getenv("SBW_PASSB_TC_MIN_N");
+  return e ? atoi(e) : 21;
+}();
 
 int64_t batch_components(int n, int64_t total) {
   static const char* env = getenv("SBW_K3_BATCH");  // tuning aid: components per batch
@@ -144,7 +158,7 @@ int launch_k3_batched(const uint32_t* planes, int n, int m, uint32_t v_lo, uint3
     a.out = out;
     a.ld = ld;
     const int rc = out ? dispatch_passb_regs<MODE_SPEC>(n - 15, a, ks->b)
-                       : (n >= 22 && passb_tc_enabled()) ? launch_passb_tc(a, ks->b)
+                       : (n >= kPassBTcMinN && passb_tc_enabled()) ? launch_passb_tc(a, ks->b)
                                                          : dispatch_passb_regs<MODE_NL>(n - 15, a, ks->b);
     if (rc) return rc;
     SBW_CUDA_CHECK(cudaEventRecord(ks->done_b[buf], ks->b));

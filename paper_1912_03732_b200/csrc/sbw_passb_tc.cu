@@ -1,30 +1,33 @@
-// K3 pass B on the tensor cores: n = 22..24 (H = n - 15 = 7..9), NL only.
+// K3 pass B on the tensor cores: n = 17..24 (H = n - 15 = 2..9), NL only.
 //
 // Pass A leaves, per component, 2^H rows (x bits 15..n-1) of 2^15 biased u16
-// s = h + 2^14 (h = W_15 / 2, sbw_passb.cuh).  The 7 row stages over x bits
-// 15..21 are one int8 GEMM per 128-row block g:
+// s = h + 2^14 (h = W_15 / 2, sbw_passb.cuh).  Up to 7 row stages are one
+// int8 GEMM per 128-row block g:
 //
-//   D_g[r'][c] = sum_r H_128[r'][r] * B_g[r][c],   B_g = the u16 rows of block
-//                g read as a u8 matrix (column 2e = low byte of element e,
+//   D_g[r'][c] = sum_r A[r'][r] * B_g[r][c],   B_g = the u16 rows of block g
+//                read as a u8 matrix (column 2e = low byte of element e,
 //                column 2e+1 = high byte),
 //
-// so H_128 (s8 +/-1, the A operand) times the raw scratch bytes (u8, the B
-// operand, MN-major exactly as they lie in HBM) gives W_g = D_g[2e] +
-// 256 D_g[2e+1] = H_128 s, exact in s32 (|D| <= 128 * 255).  The bias 2^14 of
-// s adds 2^14 * 128 = 2^21 to row r' = 0 only (H_128 * 1 = 128 e_0).  The
-// remaining H - 7 stages (across the G = 2^(H-7) blocks) and the max|W| fold
-// run on the ALU from TMEM: ~4 instructions per element instead of ~13 for
-// the fp32 pass (k_passb_staged), so the kernel is bound by the HBM read.
+// so A (s8 +/-1: H_128, or I_P (x) H_(2^H) for H < 7, see PbShape) times the
+// raw scratch bytes (u8, the B operand, MN-major exactly as they lie in HBM)
+// gives W_g = D_g[2e] + 256 D_g[2e+1] = A s, exact in s32 (|D| <= 128 * 255).
+// The bias 2^14 of s adds 2^14 * 2^h to row u = 0 of every 2^h block only
+// (H_(2^h) * 1 = 2^h e_0).  The remaining H - 7 stages (across the
+// G = 2^(H-7) blocks) and the max|W| fold run on the ALU from TMEM: ~4
+// instructions per element instead of ~13 for the fp32 pass
+// (k_passb_staged), so the kernel is bound by the HBM read.
 //
-// Data path: TMA (2D tensor map over the batch scratch, SWIZZLE_64B boxes of
-// 64 B x <= 256 rows) -> 4..8-stage shared-memory ring -> tcgen05.mma
+// Data path: TMA (3D tensor map [rows][chunks][64 B] over the batch scratch,
+// SWIZZLE_64B boxes of 64 B x P chunks x <= 256 rows) -> 4-stage ring -> tcgen05.mma
 // kind::i8 (M128 N64 K32, B MN-major SW64) -> double-buffered TMEM ->
-// tcgen05.ld by 8 epilogue warps.  One item = one component x 32 elements
-// (64 bytes) of every row.  The reference runs all n stages per mask in numpy
-// (walsh.py:91-103); stage order is free because butterflies commute.
+// tcgen05.ld by 8 epilogue warps.  One item = one component x 32 KiB: 32 P CG
+// elements (P CG adjacent 64-byte chunks) of every row.  The reference runs all n
+// stages per mask in numpy (walsh.py:91-103); stage order is free because
+// butterflies commute.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <climits>
 #include <cstdlib>
 
 #include "sbw_internal.cuh"
@@ -48,11 +51,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-      "[%4];" ::"r"(tc::smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(tc::smem_u32(bar))
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(tc::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(tc::smem_u32(bar))
       : "memory");
 }
 // MN-major SWIZZLE_64B descriptor: 8 K-rows x 64 B atoms (512 B, 512-aligned),
@@ -74,16 +77,33 @@ __device__ __forceinline__ void wait_ld_tied32(uint32_t (&r)[32]) {
                : "memory");
 }
 
+// H >= 7: G = 2^(H-7) blocks of 128 rows, A = H_128, the last H - 7 stages on
+// the ALU.  H <= 6: all H stages in the GEMM; P = 128 / 2^H adjacent 64-byte
+// column chunks of one component are interleaved along K (K index = row P + p,
+// exactly how one TMA box {64 B, P chunks, 2^H rows} lands) and A =
+// H_(2^H) (x) I_P, so output row r' = u P + p is coefficient u of chunk p.
+//
+// An item is CG = 4 / G column groups (32 P elements each) so that every item
+// moves 32 KiB: small items pay the per-item handshakes (mbarrier waits, TMEM
+// loads) too often to keep up with HBM.
 template <int H>
 struct PbShape {
-  static constexpr int G = 1 << (H - 7);                    // 128-row blocks
+  static constexpr int h = H < 7 ? H : 7;                   // stages in the GEMM
+  static constexpr int G = 1 << (H - h);                    // 128-row blocks
+  static constexpr int LP = 7 - h, P = 1 << LP;             // chunks interleaved along K
+  static constexpr int CG = 4 / G;                          // column groups per item
+  static constexpr int LCG = CG == 4 ? 2 : (CG == 2 ? 1 : 0);
   static constexpr int ROWS = 1 << H;
-  static constexpr int ITEM_BYTES = ROWS * 64;              // 32 elements of every row
-  static constexpr int BOX_ROWS = ROWS < 256 ? ROWS : 256;  // TMA box height
-  static constexpr int STAGES = kPbRingBytes / ITEM_BYTES > 8 ? 8 : kPbRingBytes / ITEM_BYTES;
-  static constexpr int TCOLS = G * 64;                      // TMEM columns per buffer
-  static constexpr int TALLOC = 2 * TCOLS;                  // 128 / 256 / 512
-  static constexpr int64_t PER_COMP = int64_t(1) << 10;     // items per component
+  static constexpr int SUB_BYTES = G * 128 * 64;            // one column group
+  static constexpr int ITEM_BYTES = CG * SUB_BYTES;         // 32 KiB
+  static constexpr int BOX_ROWS = ROWS < 256 ? ROWS : 256;  // TMA box {64 B, P, BOX_ROWS}
+  static constexpr int BOXES = ROWS / BOX_ROWS;             // per column group
+  static constexpr int STAGES = kPbRingBytes / ITEM_BYTES;  // 4
+  static constexpr int TCOLS = CG * G * 64;                 // TMEM columns per buffer (256)
+  static constexpr int TBUF = 512 / TCOLS;                  // 2
+  static constexpr int TALLOC = 512;
+  static constexpr int LPC = 10 - LP - LCG;                 // log2 items per component
+  static constexpr int64_t PER_COMP = int64_t(1) << LPC;
 };
 
 template <int H>
@@ -92,7 +112,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constan
   constexpr uint32_t kIdesc = tc::idesc_i8(128, 64, true, false) | (1u << 16);  // B MN-major
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[S::STAGES], empty[S::STAGES], tfull[2], tempty[2];
+  __shared__ uint64_t full[S::STAGES], empty[S::STAGES], tfull[S::TBUF], tempty[S::TBUF];
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t items = a.n_comp * S::PER_COMP;
@@ -101,13 +121,17 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constan
   const int64_t b1 = b0 + per_cta < items ? b0 + per_cta : items;
   const int n_my = b0 < b1 ? int(b1 - b0) : 0;
 
-  // A = H_128: core matrix (row group rg, 16-byte K chunk kc) at
+  // A = H_(2^h) (x) I_P: core matrix (row group rg, 16-byte K chunk kc) at
   // (rg * 8 + kc) * 128, row r & 7 at + 16 (r & 7)
   for (int e = tid; e < 128 * 32; e += kPbThreads) {
     const int r = e >> 5, k4 = (e & 31) * 4;
     uint32_t w = 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) w |= ((__popc(r & (k4 + j)) & 1) ? 0xFFu : 0x01u) << (8 * j);
+    for (int j = 0; j < 4; ++j) {
+      const int k = k4 + j;
+      const uint32_t v = ((r ^ k) & (S::P - 1)) ? 0u : ((__popc((r >> S::LP) & (k >> S::LP)) & 1) ? 0xFFu : 0x01u);
+      w |= v << (8 * j);
+    }
     *reinterpret_cast<uint32_t*>(smem + kPbAOff + ((r >> 3) * 8 + (k4 >> 4)) * 128 + (r & 7) * 16 + (k4 & 15)) = w;
   }
   if (warp == 0) tc::tmem_alloc(&tmem_slot, S::TALLOC);
@@ -116,7 +140,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constan
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < S::TBUF; ++b) {
       tc::mbar_init(&tfull[b], 1);
       tc::mbar_init(&tempty[b], 256);
     }
@@ -134,71 +158,117 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constan
         const int s = i % S::STAGES;
         if (i >= S::STAGES) tc::mbar_wait(&empty[s], uint32_t((i / S::STAGES - 1) & 1));
         const int64_t b = b0 + i;
-        const int comp = int(b >> 10), q = int(b & 1023);
+        const int comp = int(b >> S::LPC), q = int(b & (S::PER_COMP - 1));
         mbar_expect_tx(&full[s], S::ITEM_BYTES);
 #pragma unroll
-        for (int bx = 0; bx < S::ROWS / S::BOX_ROWS; ++bx)
-          tma_load_2d(smem + kPbBOff + s * S::ITEM_BYTES + bx * S::BOX_ROWS * 64, &tmap, q * 64,
-                      comp * S::ROWS + bx * S::BOX_ROWS, &full[s]);
+        for (int c = 0; c < S::CG; ++c)
+#pragma unroll
+          for (int bx = 0; bx < S::BOXES; ++bx)
+            tma_load_3d(smem + kPbBOff + s * S::ITEM_BYTES + c * S::SUB_BYTES + bx * S::BOX_ROWS * 64, &tmap, 0,
+                        (q * S::CG + c) * S::P, comp * S::ROWS + bx * S::BOX_ROWS, &full[s]);
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     const uint32_t a_base = tc::smem_u32(smem + kPbAOff);
     for (int i = 0; i < n_my; ++i) {
-      const int s = i % S::STAGES, buf = i & 1;
+      const int s = i % S::STAGES, buf = i % S::TBUF;
       tc::mbar_wait(&full[s], uint32_t((i / S::STAGES) & 1));
-      if (i >= 2) tc::mbar_wait(&tempty[buf], uint32_t(((i >> 1) - 1) & 1));
+      if (i >= S::TBUF) tc::mbar_wait(&tempty[buf], uint32_t((i / S::TBUF - 1) & 1));
       tc::fence_after();
       const uint32_t b_base = tc::smem_u32(smem + kPbBOff + s * S::ITEM_BYTES);
 #pragma unroll
-      for (int g = 0; g < S::G; ++g)
+      for (int c = 0; c < S::CG; ++c)
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          tc::mma_i8_elect(tmem + buf * S::TCOLS + g * 64, tc::sdesc(a_base + k * 256, 128, 1024),
-                           sdesc_mn_sw64(b_base + (g * 128 + 32 * k) * 64, 512), kIdesc, k > 0 ? 1u : 0u);
+        for (int g = 0; g < S::G; ++g)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tc::mma_i8_elect(tmem + buf * S::TCOLS + (c * S::G + g) * 64, tc::sdesc(a_base + k * 256, 128, 1024),
+                             sdesc_mn_sw64(b_base + c * S::SUB_BYTES + (g * 128 + 32 * k) * 64, 512), kIdesc,
+                             k > 0 ? 1u : 0u);
       tc::mma_commit_elect(&empty[s]);
       tc::mma_commit_elect(&tfull[buf]);
       __syncwarp();
     }
   } else {
-    // ---------------- epilogue: 8 warps, lane quarter warp & 3, column half ----------------
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    // ---------------- epilogue: 8 warps, lane quarter warp & 3 ----------------
+    // Both warpgroups read every item: CG >= 2 -> column groups split between
+    // them; CG = 1 (G = 4) -> one column half each.
+    const int quarter = warp & 3, wg = (warp - 2) >> 2;
     const int rr = quarter * 32 + lane;  // output row r' = TMEM lane
-    // row r' = 0 carries 2^21 per block from the bias of s
-    const int corr = rr == 0 ? -(S::G == 1 ? (1 << 21) : (1 << 22)) : 0;
+    // row u = 0 of every 2^h block carries 2^14 * 2^h from the bias of s
+    // (twice that after the first ALU stage when G >= 2)
+    const int corr = rr < S::P ? -(S::G == 1 ? (1 << (14 + S::h)) : (1 << 22)) : 0;
     const uint32_t t_lane = uint32_t(quarter * 32) << 16;
     int run = 0;
     for (int i = 0; i < n_my; ++i) {
-      const int buf = i & 1;
-      tc::mbar_wait(&tfull[buf], uint32_t((i >> 1) & 1));
+      const int buf = i % S::TBUF;
+      const uint32_t tb = tmem + t_lane + buf * S::TCOLS;
+      tc::mbar_wait(&tfull[buf], uint32_t((i / S::TBUF) & 1));
       tc::fence_after();
-      uint32_t d[S::G][32];
-#pragma unroll
-      for (int g = 0; g < S::G; ++g) tc::tmem_ld_x32(tmem + t_lane + buf * S::TCOLS + g * 64 + half * 32, d[g]);
-#pragma unroll
-      for (int g = 0; g < S::G; ++g) wait_ld_tied32(d[g]);
-      tc::fence_before();
-      mbar_arrive_pb(&tempty[buf]);
       int m = 0;
+      if constexpr (S::G == 1) {
+        // CG = 4: two column groups per warpgroup, 32 elements each
+        int mx = INT_MIN, mn = INT_MAX;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        int w[S::G];
+        for (int cc = 0; cc < 2; ++cc) {
+          uint32_t d[64];
+          tc::tmem_ld_x64(tb + (2 * wg + cc) * 64, d);
+          tc::wait_ld_tied(d);
+          if (cc == 1) {
+            tc::fence_before();
+            mbar_arrive_pb(&tempty[buf]);
+          }
 #pragma unroll
-        for (int g = 0; g < S::G; ++g) w[g] = int(d[g][2 * e + 1]) * 256 + int(d[g][2 * e]);
-        if constexpr (S::G == 1) {
-          m = max(m, abs(w[0] + corr));
-        } else if constexpr (S::G == 2) {
-          m = __vimax3_s32(m, abs(w[0] + w[1] + corr), abs(w[0] - w[1]));
-        } else {
+          for (int e = 0; e < 32; e += 2) {
+            const int w0 = int(d[2 * e + 1]) * 256 + int(d[2 * e]);
+            const int w1 = int(d[2 * e + 3]) * 256 + int(d[2 * e + 2]);
+            mx = __vimax3_s32(mx, w0, w1);
+            mn = __vimin3_s32(mn, w0, w1);
+          }
+        }
+        m = max(mx + corr, -(mn + corr));
+      } else if constexpr (S::G == 2) {
+        // CG = 2: one column group per warpgroup, both blocks, then the top stage
+        uint32_t d0[64], d1[64];
+        tc::tmem_ld_x64(tb + (wg * 2) * 64, d0);
+        tc::tmem_ld_x64(tb + (wg * 2 + 1) * 64, d1);
+        tc::wait_ld_tied(d0);
+        tc::wait_ld_tied(d1);
+        tc::fence_before();
+        mbar_arrive_pb(&tempty[buf]);
+        int mx = INT_MIN, mn = INT_MAX;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int w0 = int(d0[2 * e + 1]) * 256 + int(d0[2 * e]);
+          const int w1 = int(d1[2 * e + 1]) * 256 + int(d1[2 * e]);
+          mx = __vimax3_s32(mx, w0 + w1 + corr, w0 - w1);
+          mn = __vimin3_s32(mn, w0 + w1 + corr, w0 - w1);
+        }
+        m = max(mx, -mn);
+      } else {
+        // CG = 1, G = 4: one column half per warpgroup
+        uint32_t d[S::G][32];
+#pragma unroll
+        for (int g = 0; g < S::G; ++g) tc::tmem_ld_x32(tb + g * 64 + wg * 32, d[g]);
+#pragma unroll
+        for (int g = 0; g < S::G; ++g) wait_ld_tied32(d[g]);
+        tc::fence_before();
+        mbar_arrive_pb(&tempty[buf]);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          int w[S::G];
+#pragma unroll
+          for (int g = 0; g < S::G; ++g) w[g] = int(d[g][2 * e + 1]) * 256 + int(d[g][2 * e]);
+          // stage over block bit 0, then the top stage fused with the fold
           const int s01 = w[0] + w[1] + corr, d01 = w[0] - w[1];
           const int s23 = w[2] + w[3] + corr, d23 = w[2] - w[3];
           m = __vimax3_s32(m, abs(s01) + abs(s23), abs(d01) + abs(d23));
         }
       }
       run = max(run, 2 * m);  // values are W / 2
-      const int64_t b = b0 + i, comp = b >> 10;
-      if (i + 1 >= n_my || ((b + 1) >> 10) != comp) {
+      const int64_t b = b0 + i, comp = b >> S::LPC;
+      if (i + 1 >= n_my || ((b + 1) >> S::LPC) != comp) {
         warp_publish_max(run, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
         run = 0;
       }
@@ -233,11 +303,12 @@ int run_passb_tc(const PassBArgs& a, cudaStream_t st) {
   auto enc = encode_fn();
   if (!enc) return set_error(SBW_ECUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap map;
-  const cuuint64_t dims[2] = {cuuint64_t(1) << 16, cuuint64_t(a.n_comp) << H};  // bytes per row, rows
-  const cuuint64_t strides[1] = {cuuint64_t(1) << 16};
-  const cuuint32_t box[2] = {64, cuuint32_t(S::BOX_ROWS)};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint32_t*>(a.scratch), dims, strides, box,
+  // [rows][1024 chunks][64 B]: box {64 B, P chunks, BOX_ROWS rows}
+  const cuuint64_t dims[3] = {64, 1024, cuuint64_t(a.n_comp) << H};
+  const cuuint64_t strides[2] = {64, cuuint64_t(1) << 16};
+  const cuuint32_t box[3] = {64, cuuint32_t(S::P), cuuint32_t(S::BOX_ROWS)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint32_t*>(a.scratch), dims, strides, box,
                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(SBW_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
@@ -265,10 +336,15 @@ bool passb_tc_enabled() {
 
 int launch_passb_tc(const PassBArgs& a, cudaStream_t st) {
   switch (a.n - 15) {
+    case 2: return run_passb_tc<2>(a, st);
+    case 3: return run_passb_tc<3>(a, st);
+    case 4: return run_passb_tc<4>(a, st);
+    case 5: return run_passb_tc<5>(a, st);
+    case 6: return run_passb_tc<6>(a, st);
     case 7: return run_passb_tc<7>(a, st);
     case 8: return run_passb_tc<8>(a, st);
     case 9: return run_passb_tc<9>(a, st);
-    default: return set_error(SBW_EINVAL, "tensor-core pass B needs n in 22..24");
+    default: return set_error(SBW_EINVAL, "tensor-core pass B needs n in 17..24");
   }
 }
 

@@ -6,7 +6,8 @@ import sys, json, torch, numpy as np
 sys.path.insert(0, ".")
 import paper_1912_03732_b200 as sw
 res = {}
-for (n, m, lo, hi) in [(22, 6, 1, 64), (23, 5, 1, 32), (24, 4, 1, 16), (24, 16, 1000, 1064)]:
+for (n, m, lo, hi) in [(17, 8, 1, 256), (18, 6, 1, 64), (19, 6, 1, 64), (20, 8, 1, 256), (21, 6, 1, 64),
+                       (22, 6, 1, 64), (23, 5, 1, 32), (24, 4, 1, 16), (24, 16, 1000, 1064)]:
     s = sw.generate_sbox(n, m, 0, bijective=False)
     mx, key = sw.component_max_abs_device(s, lo, hi)
     torch.cuda.synchronize()
