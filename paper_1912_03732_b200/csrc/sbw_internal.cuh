@@ -99,4 +99,84 @@ __device__ __forceinline__ int warp_max(int x) {
   return x;
 }
 
+// --- L2 ring hand-off between concurrently running pass A / pass B (K3) ---
+// Counters live in global memory; producers release with a gpu-scope fence
+// before a relaxed atomicAdd, consumers poll with ld.acquire.gpu.  A wait
+// that exceeds ~4 s (the two kernels were not co-resident) raises *err and
+// gives up instead of hanging the device; the host turns *err into poisoned
+// results (odd gap -> AssertionError in the NL conversion).
+//
+// Ring layout: batch k = components [k Bc, (k + 1) Bc) of the ring run lives
+// in slot k mod R (R slots of Bc components).  Pass A CTA j = r * T + bp owns
+// 2^16-block pair bp and components [r L, (r + 1) L) of every batch
+// (Bc = q L, q = NA / T); each of its 8 transform warps arrives on ready[k]
+// after its last item of batch k.  Pass B CTA j owns items
+// [I j / NB, I (j + 1) / NB) of every batch (I = Bc x items per component)
+// and arrives on freed[k] once its last TMA load of batch k has landed.
+struct RingArgs {
+  int on;              // 0: batch mode (no ring)
+  int R, L, q, log_t;  // slots, components per pass-A CTA per batch, CTAs per block pair, log2 block pairs
+  int64_t batches;     // full batches in the ring run
+  int bc;              // components per batch (q L)
+  uint32_t na, nb;     // pass A / pass B CTAs
+  uint32_t* ready;     // [batches]: pass-A transform-warp arrivals (target 8 na)
+  uint32_t* freed;     // [batches]: pass-B CTA arrivals (target nb)
+  uint32_t* err;       // co-residency timeout flag
+  unsigned long long* wait_ns;  // [2] optional (SBW_K3_TRACE): ns spent waiting in pass A / pass B
+  int nowait;          // timing experiments only (SBW_K3_RING_NOWAIT): skip every wait (results invalid)
+};
+
+// Mask at natural position q of [v_lo, v_hi): Gray order inside every aligned
+// block of 256 masks that lies in the range (consecutive positions differ in
+// one mask bit, so generation is one plane XOR), natural order elsewhere.
+__device__ __forceinline__ uint32_t mask_at(int64_t q, uint32_t v_lo, uint32_t v_hi) {
+  const int64_t b = q & ~int64_t(255);
+  if (b >= int64_t(v_lo) && b + 256 <= int64_t(v_hi)) {
+    const uint32_t k = uint32_t(q) & 255u;
+    return uint32_t(b) | (k ^ (k >> 1));
+  }
+  return uint32_t(q);
+}
+
+// Ring position -> mask.  Pass-A CTA row r walks positions [r K L, (r + 1) K L)
+// (K = batches) in order, so its consecutive components are consecutive in
+// Gray order; slot r L + l of batch k holds position r K L + k L + l.
+__device__ __forceinline__ uint32_t ring_mask(const RingArgs& r, uint32_t v_first, int64_t pos) {
+  return mask_at(int64_t(v_first) + pos, v_first, uint32_t(int64_t(v_first) + r.batches * r.bc));
+}
+__device__ __forceinline__ int64_t ring_pos(const RingArgs& r, int64_t k, int64_t slot_comp) {
+  const int64_t row = slot_comp / r.L;
+  return row * r.batches * r.L + k * r.L + (slot_comp - row * r.L);
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void ring_wait_geq(const uint32_t* p, uint32_t target, uint32_t* err,
+                                              unsigned long long* wait_ns = nullptr) {
+  if (ld_acquire_gpu(p) >= target) return;
+  const uint64_t t0 = globaltimer_ns();
+  uint64_t t = t0;
+  while (ld_acquire_gpu(p) < target) {
+    if (ld_acquire_gpu(err) != 0u) break;
+    t = globaltimer_ns();
+    if (t - t0 > 4000000000ull) {
+      atomicExch(err, 1u);
+      break;
+    }
+  }
+  if (wait_ns) atomicAdd(wait_ns, static_cast<unsigned long long>(t - t0));
+}
+__device__ __forceinline__ void ring_signal(uint32_t* p) {
+  __threadfence();
+  atomicAdd(p, 1u);
+}
+
 }  // namespace sbw

@@ -37,6 +37,12 @@ int launch_tc16_spec(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32
 int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_comp, uint32_t* emit,
                    cudaStream_t st);
 
+// The same pass A streaming into the L2 ring of a concurrently running
+// k_passb_tc (RingArgs in sbw_internal.cuh); grid = ring.na CTAs.
+struct RingArgs;
+int launch_tc_emit_ring(const uint32_t* planes, int n, uint32_t v_first, const RingArgs& ring, uint32_t* emit,
+                        cudaStream_t st);
+
 // Multi-pass path (n >= 17): planes, then pass A (emit) + pass B per L2-sized batch.
 size_t k3_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi);
 // K3 pass B on the tensor cores (n = 22..24, NL only), sbw_passb_tc.cu;

@@ -31,6 +31,7 @@ struct PassBArgs {
   unsigned long long* key;
   int32_t* out;              // materialised rows (may be null)
   int64_t ld;
+  RingArgs ring;             // k_passb_tc only: L2 ring mode (scratch = the ring slots)
 };
 
 // Pass B of max|W| runs its butterflies in fp32 on the FMA pipe (FADD at 4

@@ -115,11 +115,27 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constan
   __shared__ uint64_t full[S::STAGES], empty[S::STAGES], tfull[S::TBUF], tempty[S::TBUF];
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t items = a.n_comp * S::PER_COMP;
-  const int64_t per_cta = (items + gridDim.x - 1) / gridDim.x;
-  const int64_t b0 = blockIdx.x * per_cta;
-  const int64_t b1 = b0 + per_cta < items ? b0 + per_cta : items;
-  const int n_my = b0 < b1 ? int(b1 - b0) : 0;
+  const bool ring = a.ring.on != 0;
+  int64_t b0 = 0, n_pb = 1, ib_off = 0, I = 0;
+  int n_my = 0;
+  if (ring) {  // this CTA's share [I j / NB, I (j + 1) / NB) of every batch
+    I = int64_t(a.ring.bc) * S::PER_COMP;
+    ib_off = I * blockIdx.x / gridDim.x;
+    n_pb = I * (blockIdx.x + 1) / gridDim.x - ib_off;
+    n_my = n_pb > 0 ? int(a.ring.batches * n_pb) : 0;
+  } else {
+    const int64_t items = a.n_comp * S::PER_COMP;
+    const int64_t per_cta = (items + gridDim.x - 1) / gridDim.x;
+    b0 = blockIdx.x * per_cta;
+    const int64_t b1 = b0 + per_cta < items ? b0 + per_cta : items;
+    n_my = b0 < b1 ? int(b1 - b0) : 0;
+  }
+  // i-th item of this CTA -> item index (component-major) within the launch
+  auto item_b = [&](int i) -> int64_t {
+    if (!ring) return b0 + i;
+    const int64_t k = i / n_pb;
+    return k * I + ib_off + (i - k * n_pb);
+  };
 
   // A = H_(2^h) (x) I_P: core matrix (row group rg, 16-byte K chunk kc) at
   // (rg * 8 + kc) * 128, row r & 7 at + 16 (r & 7)
@@ -157,8 +173,19 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constan
       for (int i = 0; i < n_my; ++i) {
         const int s = i % S::STAGES;
         if (i >= S::STAGES) tc::mbar_wait(&empty[s], uint32_t((i / S::STAGES - 1) & 1));
-        const int64_t b = b0 + i;
-        const int comp = int(b >> S::LPC), q = int(b & (S::PER_COMP - 1));
+        const int64_t b = item_b(i);
+        int comp = int(b >> S::LPC);
+        const int q = int(b & (S::PER_COMP - 1));
+        if (ring) {
+          // batch k sits in slot k mod R; its first item waits for every
+          // pass-A warp's arrival, then orders the TMA reads after the acquire
+          const int64_t k = i / n_pb;
+          if (i - k * n_pb == 0 && !a.ring.nowait) {
+            ring_wait_geq(a.ring.ready + k, 8u * a.ring.na, a.ring.err, a.ring.wait_ns ? a.ring.wait_ns + 1 : nullptr);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
+          comp = int((k % a.ring.R) * a.ring.bc + (int64_t(comp) - k * a.ring.bc));
+        }
         mbar_expect_tx(&full[s], S::ITEM_BYTES);
 #pragma unroll
         for (int c = 0; c < S::CG; ++c)
@@ -174,6 +201,10 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constan
     for (int i = 0; i < n_my; ++i) {
       const int s = i % S::STAGES, buf = i % S::TBUF;
       tc::mbar_wait(&full[s], uint32_t((i / S::STAGES) & 1));
+      // ring: the last load of this CTA's share of a batch has landed -> the
+      // slot may be overwritten as far as this CTA is concerned
+      if (ring && lane == 0 && (i % n_pb) == n_pb - 1) ring_signal(a.ring.freed + i / n_pb);
+      __syncwarp();
       if (i >= S::TBUF) tc::mbar_wait(&tempty[buf], uint32_t((i / S::TBUF - 1) & 1));
       tc::fence_after();
       const uint32_t b_base = tc::smem_u32(smem + kPbBOff + s * S::ITEM_BYTES);
@@ -267,9 +298,15 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constan
         }
       }
       run = max(run, 2 * m);  // values are W / 2
-      const int64_t b = b0 + i, comp = b >> S::LPC;
-      if (i + 1 >= n_my || ((b + 1) >> S::LPC) != comp) {
-        warp_publish_max(run, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
+      const int64_t comp = item_b(i) >> S::LPC;
+      if (i + 1 >= n_my || (item_b(i + 1) >> S::LPC) != comp) {
+        if (ring) {  // batch k, slot component cb -> its ring position's mask
+          const int64_t k = comp / a.ring.bc;
+          const uint32_t v = ring_mask(a.ring, a.v_first, ring_pos(a.ring, k, comp - k * a.ring.bc));
+          warp_publish_max(run, a.max_abs + (v - a.v_first), a.key, v);
+        } else {
+          warp_publish_max(run, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
+        }
         run = 0;
       }
     }
@@ -318,7 +355,7 @@ int run_passb_tc(const PassBArgs& a, cudaStream_t st) {
     attr_done |= 1ull << (dp.device & 63);
   }
   const int64_t items = a.n_comp * S::PER_COMP;
-  const int grid = int(items < dp.sm_count ? items : dp.sm_count);
+  const int grid = a.ring.on ? int(a.ring.nb) : int(items < dp.sm_count ? items : dp.sm_count);
   k_passb_tc<H><<<grid, kPbThreads, kPbSmem, st>>>(map, a);
   SBW_LAUNCH_CHECK("k_passb_tc");
   return SBW_OK;

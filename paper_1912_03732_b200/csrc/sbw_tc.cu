@@ -100,14 +100,6 @@ __device__ __forceinline__ int a_value(int u, int p) {
   return 0;
 }
 
-__device__ __forceinline__ uint32_t mask_at(int64_t q, uint32_t v_lo, uint32_t v_hi) {
-  const int64_t b = q & ~int64_t(255);
-  if (b >= int64_t(v_lo) && b + 256 <= int64_t(v_hi)) {
-    const uint32_t k = uint32_t(q) & 255u;
-    return uint32_t(b) | (k ^ (k >> 1));
-  }
-  return uint32_t(q);
-}
 
 __device__ __forceinline__ void xor_plane(uint32_t (&g)[8], const uint4& a, const uint4& b) {
   g[0] ^= a.x; g[1] ^= a.y; g[2] ^= a.z; g[3] ^= a.w;
@@ -261,6 +253,8 @@ struct TcArgs {
   // SPEC (n = 16 materialised spectrum, mask-major): out[(v - v_lo) * ld + u]
   int32_t* out;
   int64_t ld;
+  // EMIT into the L2 ring shared with a concurrent pass B (sbw_internal.cuh)
+  RingArgs ring;
 };
 
 constexpr int kTcNL = 0, kTcEmit = 1, kTcSpec = 2;
@@ -279,6 +273,11 @@ __device__ __forceinline__ int64_t items_total(const TcArgs& a) {
 template <int MODE, int NB>
 __device__ __forceinline__ void item_at(const TcArgs& a, int64_t t, uint32_t& v, uint32_t& bp) {
   if constexpr (MODE == kTcEmit) {
+    if (a.ring.on) {  // CTA (r, bp): ring position r K L + t (slot r L + t mod L of batch t / L)
+      bp = blockIdx.x & ((1u << a.ring.log_t) - 1u);
+      v = ring_mask(a.ring, a.v_first, int64_t(blockIdx.x >> a.ring.log_t) * a.ring.batches * a.ring.L + t);
+      return;
+    }
     bp = uint32_t(t / a.n_comp);
     v = a.v_first + uint32_t(t - int64_t(bp) * a.n_comp);
   } else {
@@ -345,8 +344,9 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
   __shared__ __align__(16) uint32_t s_wmax[4][kSlots][kMathWarps];  // per-warp max|W| [item & 3][slot]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t total = items_total<MODE, NB>(a);
-  const int64_t t_lo = total * blockIdx.x / gridDim.x;
-  const int n_my = int(total * (blockIdx.x + 1) / gridDim.x - t_lo);
+  const bool ring = EMIT && a.ring.on;
+  const int64_t t_lo = ring ? 0 : total * blockIdx.x / gridDim.x;
+  const int n_my = ring ? int(a.ring.batches * a.ring.L) : int(total * (blockIdx.x + 1) / gridDim.x - t_lo);
 
   // constant operands (A and B's bias block): one coalesced copy of the
   // image k_tc_consts built once per device
@@ -565,39 +565,87 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         }
         gen_store();
       }
-      // c bits L..6 (register bits L-1..5, stages 8+L..14); register bit b is
-      // c bit b+1, stage 9+b, diff bias 2^(9+b) per lane
-#pragma unroll
-      for (int sb = (kLogRows > 0 ? kLogRows - 1 : 0); sb < NB - 10; ++sb)
-#pragma unroll
-        for (int k = 0; k < 128; ++k)
-          if ((k & (1 << sb)) == 0) {
-            const uint32_t x = R[k], y = R[k | (1 << sb)];
-            R[k] = x + y;
-            R[k | (1 << sb)] = x - y + (0x02000200u << sb);
-          }
-      if constexpr (EMIT) {
-        // 15 stages per 2^15 block (c bit 7 = the block's parity is left to
-        // pass B).  Lanes are s = W_15 / 2 + 2^14; the row u = 0 offset sits in
-        // the lo lane of R[0] / R[64] (-128 x 128 columns).  Block word layout
-        // (pass B only pairs equal positions across blocks):
-        //   word (j >> 2) * 1024 + 4 u + (j & 3)  <-  R[64 h + j]
-        if (!kC0Mma && u == 0) {
-          R[0] += 0x4000u;
-          R[64] += 0x4000u;
-        }
+      if constexpr (EMIT && kRows == 8) {
+        // 15 stages per 2^15 block (c bit 7 = the block's parity, register
+        // bit 6, is left to pass B); lanes are s = W_15 / 2 + 2^14.  The
+        // remaining ALU stages (register bits 2..5) run one 16-register
+        // network (fixed bits 0, 1, 6) at a time and each network is stored
+        // as soon as it is final, so the 128 KiB of stores per item spread
+        // over the stage arithmetic instead of queueing behind it.  Block word
+        // layout (pass B only pairs equal positions across blocks):
+        //   network (h, b = bits 0..1), group g = bits 4..5 ->
+        //   words (4 b + g) * 1024 + 4 u + (0..3) <- R[64 h + b + 4 (4 g + 0..3)]
         uint32_t vi, bpi;
         item_at<MODE, NB>(a, t_lo + i, vi, bpi);
-        uint32_t* dst = a.emit + (int64_t(vi - a.v_first) << (a.n_full - 1)) +
-                        (int64_t(2 * bpi) << 14) + 4 * u;
+        int64_t slot_comp = int64_t(vi - a.v_first);
+        int64_t rk = 0;
+        int rl = 0;
+        if (ring) {
+          // ring slot of this component; before the first store into batch
+          // k's slot, wait until pass B has loaded batch k - R out of it
+          rk = i / a.ring.L;
+          rl = int(i - rk * a.ring.L);
+          slot_comp = (rk % a.ring.R) * a.ring.bc + int64_t(blockIdx.x >> a.ring.log_t) * a.ring.L + rl;
+          if (rl == 0 && rk >= a.ring.R && !a.ring.nowait) {
+            if (lane == 0) ring_wait_geq(a.ring.freed + (rk - a.ring.R), a.ring.nb, a.ring.err, a.ring.wait_ns);
+            __syncwarp();
+          }
+        }
+        uint32_t* dst = a.emit + (slot_comp << (a.n_full - 1)) + (int64_t(2 * bpi) << 14) + 4 * u;
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+        for (int net = 0; net < 8; ++net) {
+          const int base = (net >> 2) * 64 + (net & 3);  // h = net >> 2, b = net & 3
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
-            *reinterpret_cast<uint4*>(dst + (h << 14) + q * 1024) =
-                make_uint4(R[64 * h + 4 * q], R[64 * h + 4 * q + 1], R[64 * h + 4 * q + 2],
-                           R[64 * h + 4 * q + 3]);
+          for (int sb = 2; sb < 6; ++sb)
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if ((j & (1 << (sb - 2))) == 0) {
+                const int k0 = base + 4 * j, k1 = base + 4 * (j | (1 << (sb - 2)));
+                const uint32_t x = R[k0], y = R[k1];
+                R[k0] = x + y;
+                R[k1] = x - y + (0x02000200u << sb);
+              }
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            *reinterpret_cast<uint4*>(dst + ((net >> 2) << 14) + (4 * (net & 3) + g) * 1024) =
+                make_uint4(R[base + 16 * g], R[base + 16 * g + 4], R[base + 16 * g + 8], R[base + 16 * g + 12]);
+        }
+        if (ring && rl == a.ring.L - 1) {  // this warp's part of batch rk is stored
+          __syncwarp();
+          if (lane == 0) ring_signal(a.ring.ready + rk);
+        }
       } else {
+        // c bits L..6 (register bits L-1..5, stages 8+L..14); register bit b is
+        // c bit b+1, stage 9+b, diff bias 2^(9+b) per lane
+#pragma unroll
+        for (int sb = (kLogRows > 0 ? kLogRows - 1 : 0); sb < NB - 10; ++sb)
+#pragma unroll
+          for (int k = 0; k < 128; ++k)
+            if ((k & (1 << sb)) == 0) {
+              const uint32_t x = R[k], y = R[k | (1 << sb)];
+              R[k] = x + y;
+              R[k | (1 << sb)] = x - y + (0x02000200u << sb);
+            }
+        if constexpr (EMIT) {
+          // (SBW_TC_ROWS < 8 experiment builds) natural block word layout:
+          //   word (j >> 2) * 1024 + 4 u + (j & 3)  <-  R[64 h + j]
+          static_assert(!EMIT || NB == 16, "EMIT covers one 2^16 tile");
+          if (!kC0Mma && u == 0) {
+            R[0] += 0x4000u;
+            R[64] += 0x4000u;
+          }
+          uint32_t vi, bpi;
+          item_at<MODE, NB>(a, t_lo + i, vi, bpi);
+          uint32_t* dst = a.emit + (int64_t(vi - a.v_first) << (a.n_full - 1)) + (int64_t(2 * bpi) << 14) + 4 * u;
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              *reinterpret_cast<uint4*>(dst + (h << 14) + q * 1024) =
+                  make_uint4(R[64 * h + 4 * q], R[64 * h + 4 * q + 1], R[64 * h + 4 * q + 2],
+                             R[64 * h + 4 * q + 3]);
+          continue;
+        }
         // top stage (c bit NB-9 = register bit NB-10) fused with the max/min
         // fold, per slot (register bits NB-9..6; carry argument of
         // tile_last_pass for NB = 16).  NB = 11 has no ALU stage left: the
@@ -754,7 +802,7 @@ int tc_consts(int dev, cudaStream_t st, const uint8_t** out) {
 }
 
 template <int MODE, int NB = 16>
-int run_tc_hybrid(const TcArgs& a, int64_t items, cudaStream_t st) {
+int run_tc_hybrid(const TcArgs& a, int64_t items, cudaStream_t st, int grid_override = 0) {
   if (items <= 0) return SBW_OK;
   DeviceProps dp;
   if (int rc = device_props(&dp)) return rc;
@@ -766,7 +814,7 @@ int run_tc_hybrid(const TcArgs& a, int64_t items, cudaStream_t st) {
   }
   TcArgs args = a;
   if (int rc = tc_consts(dp.device, st, &args.consts)) return rc;
-  const int grid = int(items < dp.sm_count ? items : dp.sm_count);
+  const int grid = grid_override > 0 ? grid_override : int(items < dp.sm_count ? items : dp.sm_count);
   k_tc_hybrid<MODE, NB><<<grid, kAllThreads, kTcSmem, st>>>(args);
   SBW_LAUNCH_CHECK(MODE == kTcEmit ? "k_tc_hybrid<emit>" : (MODE == kTcSpec ? "k_tc_hybrid<spec>" : "k_tc_hybrid<nl>"));
   return SBW_OK;
@@ -831,6 +879,20 @@ int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_co
   a.n_full = n;
   a.emit = emit;
   return run_tc_hybrid<kTcEmit>(a, a.n_items, st);
+}
+
+int launch_tc_emit_ring(const uint32_t* planes, int n, uint32_t v_first, const RingArgs& ring, uint32_t* emit,
+                        cudaStream_t st) {
+  TcArgs a{};
+  a.planes = planes;
+  a.plane_words = (int64_t(1) << n) >> 5;
+  a.v_first = v_first;
+  a.n_comp = ring.batches * ring.bc;
+  a.n_items = a.n_comp << (n - 16);
+  a.n_full = n;
+  a.emit = emit;
+  a.ring = ring;
+  return run_tc_hybrid<kTcEmit>(a, a.n_items, st, int(ring.na));
 }
 
 }  // namespace sbw

@@ -57,3 +57,32 @@ def test_random_against_oracle(n, m, seed, lo, hi):
     s = sw.generate_sbox(n, m, seed, bijective=False)
     mx, _ = sw.component_max_abs_device(s, lo, hi)
     assert np.array_equal(mx.cpu().numpy().astype(np.int64), orc.component_max_abs(s.table, n, lo, hi))
+
+
+# ---- the L2 ring (SBW_K3_RING=1): concurrent pass A / pass B ---------------
+# Off by default (measured slower, K3); kept exact.  The ring
+# reorders components (Gray order per pass-A CTA row, slot positions per
+# batch) and hands batches between two co-resident kernels, so every case
+# compares the whole maxima array and the key with the batched path and
+# samples masks against the oracle; ranges leave a tail for the batched path.
+@pytest.mark.parametrize("n,m,bij,lo,hi,na,L,R", [
+    (20, 20, False, 1, 3001, 64, 4, 3),      # 187 batches of 16 + a tail of 8
+    (17, 17, True, 5, 4100, 64, 2, 3),       # T = 2: 32 CTAs per block pair
+    (21, 12, False, 1, 4096, 64, 1, 2),      # T = 32: 2 CTAs per block pair, L = 1
+    (19, 16, False, 300, 9000, 96, 3, 4),    # L not a power of two, unaligned start
+])
+def test_ring_matches_batched(monkeypatch, n, m, bij, lo, hi, na, L, R):
+    s = sw.generate_sbox(n, m, seed=n + m, bijective=bij)
+    monkeypatch.setenv("SBW_K3_RING", "0")
+    want_mx, want_key = sw.component_max_abs_device(s, lo, hi)
+    monkeypatch.setenv("SBW_K3_RING", "1")
+    monkeypatch.setenv("SBW_K3_NA", str(na))
+    monkeypatch.setenv("SBW_K3_RING_L", str(L))
+    monkeypatch.setenv("SBW_K3_RING_R", str(R))
+    got_mx, got_key = sw.component_max_abs_device(s, lo, hi)
+    got = got_mx.cpu().numpy()
+    assert np.array_equal(got, want_mx.cpu().numpy())
+    assert int(got_key.item()) == int(want_key.item())
+    rng = np.random.default_rng(n)
+    for v in sorted(set(rng.integers(lo, hi, size=3).tolist()) | {lo, hi - 1}):
+        assert int(got[v - lo]) == int(orc.component_max_abs(s.table, n, v, v + 1)[0]), v
