@@ -13,7 +13,10 @@ every step is timed with its own CUDA events on the launching stream.
 
 Multi-GPU (torchrun): weak scaling -- every rank evaluates its own full
 16x16 box (seed = rank); no collective on the data path; time = max over
-ranks.  --impl reference times the reference's CPU algorithm (the oracle
+ranks.  --shard (the north_star's mode for 20x20 / 24x16): strong scaling --
+one box (seed 0), rank r evaluates the masks partition_columns(2^m-1, N)[r]
+(parallel.py:38-57) and each step ends with the path's one exchange, an
+all_reduce(MAX) of the 8-byte (max|W|, smallest v) key.  --impl reference times the reference's CPU algorithm (the oracle
 port of its per-mask stream loop, walsh.py:230-244) on all host cores over a
 bounded sample of masks and prints the same metric.
 """
@@ -215,10 +218,13 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
 
     n, m, bij = CONFIGS[args.config]
-    s = sw.generate_sbox(n, m, seed=rank, bijective=bij)
+    s = sw.generate_sbox(n, m, seed=0 if args.shard else rank, bijective=bij)
     v_lo, v_hi = 1, 1 << m
     if args.masks:
         v_hi = min(v_hi, 1 + args.masks)
+    total_masks = v_hi - v_lo
+    if args.shard:  # this rank's contiguous balanced mask range
+        v_lo, v_hi = sw.partition_columns(total_masks, world).ranges[rank]
     nmask = v_hi - v_lo
     tab = d.device_table(s, dev, cache=False)
     mx = torch.empty(nmask, dtype=torch.int32, device=dev)
@@ -261,6 +267,8 @@ def run_ours(args, rank, world, local_rank):
             kev[i][1].record(stream)
             d.check(lib.sbw_maxabs_to_nl(mx.data_ptr(), nmask, n, nl.data_ptr(), bad.data_ptr(),
                                          sh))
+            if args.shard and dist is not None:  # the path's exchange: global (max|W|, v) key
+                dist.all_reduce(key, op=dist.ReduceOp.MAX)
             evs[i][1].record(stream)
         torch.cuda.synchronize(dev)
     barrier()
@@ -277,7 +285,7 @@ def run_ours(args, rank, world, local_rank):
         raise AssertionError("odd spectrum gap in the benchmark run")
     res = sw.transforms.decode_key(key, n)
     check = {"nl": res[0], "argmin_v": res[1], "max_abs": res[2]}
-    if args.config == "16x16" and rank == 0 and not args.masks:
+    if args.config == "16x16" and rank == 0 and not args.masks and (args.shard or world == 1):
         assert (res[0], res[1]) == (31942, 44828), res
 
     # ---- e2e through the C ABI with host buffers (sbw_nl_host) ------------
@@ -297,9 +305,14 @@ def run_ours(args, rank, world, local_rank):
                                 out3.ctypes.data, local_rank))
     barrier()
     t0 = time.perf_counter()
+    gkey = torch.zeros(1, dtype=torch.int64, device=dev)
     for _ in range(args.steps):
         d.check(lib.sbw_nl_host(table_host.ctypes.data, n, m, v_lo, v_hi, h_nl.ctypes.data,
                                 out3.ctypes.data, local_rank))
+        if args.shard and dist is not None:  # combine the shards' (max|W|, argmin v)
+            gkey.fill_((int(out3[2]) << 32) | (0xFFFFFFFF - int(out3[1])))
+            dist.all_reduce(gkey, op=dist.ReduceOp.MAX)
+            int(gkey.item())
     e2e_s = time.perf_counter() - t0
     if dist is not None:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
@@ -404,7 +417,7 @@ def run_ours(args, rank, world, local_rank):
         if dist is not None:
             dist.destroy_process_group()
         return
-    total_coeff = coeffs(n, m, nmask) * world * args.steps
+    total_coeff = coeffs(n, m, total_masks if args.shard else nmask * world) * args.steps
     value = total_coeff / (step_ms * 1e-3)
     line = {
         "metric": f"Walsh coefficients/s, {args.config} S-box full fused nonlinearity "
@@ -417,19 +430,22 @@ def run_ours(args, rank, world, local_rank):
         "ms_per_step": step_ms / args.steps,
         "full_nl_ms": step_ms / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": (value / world) / (coeffs(16, 16) / (PAPER_16x16_NL_MS * 1e-3))
+        "scaling": "strong" if args.shard else "weak",
+        "vs_baseline": (value / (1 if args.shard else world)) / (coeffs(16, 16) / (PAPER_16x16_NL_MS * 1e-3))
         if args.config == "16x16" and not args.masks else None,
         "vs_baseline_ref": "PAPER.md:421 fused NL 16x16 = 83,015 ms on i7-8700K-class CPU (BASELINE.md)",
         "dtype": "int8 MMA (s32 acc) + packed int16" if tc_path else "int32 (packed int8/int16 lanes)",
         "data": "synthetic: generate_sbox(n, m, seed=rank) -- numpy PCG64 like the reference",
         "config": {"workload": f"{args.config} S-box (n={n}, m={m}, bijective={bij}), "
                                f"masks [{v_lo},{v_hi}), full NL per step",
-                   "parallelism": f"weak x{world} (one S-box per GPU)",
+                   "parallelism": (f"strong x{world} (masks sharded by partition_columns, "
+                                   "all_reduce(MAX) of the key per step)") if args.shard
+                                  else f"weak x{world} (one S-box per GPU)",
                    "l2": "flushed between timed steps (256 MiB write), per-step CUDA events"},
         "result": check,
         "roofline": roofline,
-        "e2e": {"value": coeffs(n, m, nmask) * world * args.steps / e2e_s, "unit": "coeff/s",
+        "e2e": {"value": coeffs(n, m, total_masks if args.shard else nmask * world) * args.steps / e2e_s,
+                "unit": "coeff/s",
                 "h2d_bytes_per_step": int(table_host.nbytes),  # uint32 table
                 "d2h_bytes_per_step": int(h_nl.nbytes + 8 * 4),
                 "path": "sbw_nl_host C ABI (host table in, host NL out, page-locked caller "
@@ -483,6 +499,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=list(CONFIGS), default="16x16")
     ap.add_argument("--masks", type=int, default=0, help="limit masks (debug)")
+    ap.add_argument("--shard", action="store_true",
+                    help="strong scaling: shard one box's masks over the ranks (20x20 / 24x16 mode)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()

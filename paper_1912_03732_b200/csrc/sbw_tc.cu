@@ -63,6 +63,12 @@ namespace {
 // .pack::16b loads deliver the biased lanes.  R = 1: plain bit rows, the
 // transform warps pack c0 with IMADs (the earlier form, kept for A/B).
 constexpr int kRows = SBW_TC_ROWS;
+// EMIT store order: 1 = per 16-register network as soon as it is final (5 %
+// faster pass A in the L2 ring, 1 % slower in the HBM-bound batched path),
+// 0 = all stores after the stages (default).
+#ifndef SBW_EMIT_NET
+#define SBW_EMIT_NET 0
+#endif
 static_assert(kRows == 1 || kRows == 2 || kRows == 8, "SBW_TC_ROWS must be 1, 2 or 8");
 constexpr int kLogRows = kRows == 8 ? 3 : (kRows == 2 ? 1 : 0);
 constexpr bool kC0Mma = kRows > 1;
@@ -565,7 +571,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         }
         gen_store();
       }
-      if constexpr (EMIT && kRows == 8) {
+      if constexpr (EMIT && kRows == 8 && SBW_EMIT_NET) {
         // 15 stages per 2^15 block (c bit 7 = the block's parity, register
         // bit 6, is left to pass B); lanes are s = W_15 / 2 + 2^14.  The
         // remaining ALU stages (register bits 2..5) run one 16-register
