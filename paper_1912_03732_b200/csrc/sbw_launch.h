@@ -34,8 +34,10 @@ int launch_tc16_spec(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32
 // 2^15 block, biased u16 out in a block-internal word order of its own
 // (pass B pairs equal word positions across blocks only, so any fixed order
 // works for NL; SPEC keeps launch_emit_tiles).
+// Components are taken in the Gray order mask_at(position, run_lo, run_hi)
+// of the whole run [run_lo, run_hi) (pass B publishes with the same map).
 int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_comp, uint32_t* emit,
-                   cudaStream_t st);
+                   uint32_t run_lo, uint32_t run_hi, cudaStream_t st);
 
 // The same pass A streaming into the L2 ring of a concurrently running
 // k_passb_tc (RingArgs in sbw_internal.cuh); grid = ring.na CTAs.

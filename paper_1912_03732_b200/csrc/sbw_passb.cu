@@ -207,6 +207,8 @@ int launch_k3_batched(const uint32_t* planes, int n, int m, uint32_t v_lo, uint3
     cudaEventRecord(e, s);
     ev.push_back(e);
   };
+  // NL with the tensor-core pass A: Gray-ordered components (PassBArgs::gray)
+  const bool gray = out == nullptr && tc_path_enabled();
   int64_t nb = 0;
   for (int64_t c0 = 0; c0 < total; c0 += bb, ++nb) {
     const int64_t nc = (total - c0) < bb ? (total - c0) : bb;
@@ -214,8 +216,7 @@ int launch_k3_batched(const uint32_t* planes, int n, int m, uint32_t v_lo, uint3
     const int buf = int(nb & 1);
     if (nb >= 2) SBW_CUDA_CHECK(cudaStreamWaitEvent(ks->a, ks->done_b[buf], 0));  // buffer free
     mark(ks->a);
-    if (int rc = (out == nullptr && tc_path_enabled())
-                     ? launch_tc_emit(planes, n, vf, nc, emit[buf], ks->a)
+    if (int rc = gray ? launch_tc_emit(planes, n, vf, nc, emit[buf], v_lo, v_hi, ks->a)
                      : launch_emit_tiles(planes, n, m, vf, nc, emit[buf], ks->a))
       return rc;
     mark(ks->a);
@@ -232,6 +233,9 @@ int launch_k3_batched(const uint32_t* planes, int n, int m, uint32_t v_lo, uint3
     a.key = key;
     a.out = out;
     a.ld = ld;
+    a.gray = gray ? 1 : 0;
+    a.run_lo = v_lo;
+    a.run_hi = v_hi;
     const int rc = out ? dispatch_passb_regs<MODE_SPEC>(n - 15, a, ks->b)
                        : (n >= kPassBTcMinN && passb_tc_enabled()) ? launch_passb_tc(a, ks->b)
                                                          : dispatch_passb_regs<MODE_NL>(n - 15, a, ks->b);

@@ -32,7 +32,17 @@ struct PassBArgs {
   int32_t* out;              // materialised rows (may be null)
   int64_t ld;
   RingArgs ring;             // k_passb_tc only: L2 ring mode (scratch = the ring slots)
+  // gray != 0 (NL after the tensor-core pass A): batch position p = v_first +
+  // comp holds mask mask_at(p, run_lo, run_hi) (Gray order inside aligned
+  // 256-blocks of the run, so pass A's generation is one plane XOR per
+  // component); max_abs is indexed by mask - run_lo.
+  int gray;
+  uint32_t run_lo, run_hi;
 };
+
+// Publish a component's max: natural order (mask v_first + comp, row
+// out_row0 + comp) or the Gray order of the tensor-core pass A.
+__device__ __forceinline__ void publish_comp(const PassBArgs& a, int64_t comp, int run);
 
 // Pass B of max|W| runs its butterflies in fp32 on the FMA pipe (FADD at 4
 // warp-instr/clk/SM, twice the IADD3 rate).  Every intermediate is an integer
@@ -185,6 +195,15 @@ __device__ __forceinline__ void warp_publish_max(int mx, int32_t* slot, unsigned
   }
 }
 
+__device__ __forceinline__ void publish_comp(const PassBArgs& a, int64_t comp, int run) {
+  if (a.gray) {
+    const uint32_t v = mask_at(int64_t(a.v_first) + comp, a.run_lo, a.run_hi);
+    warp_publish_max(run, a.max_abs + (v - a.run_lo), a.key, v);
+  } else {
+    warp_publish_max(run, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
+  }
+}
+
 // ---- batched path for H <= 5 (n = 17..20) -----------------------------------
 // Pass A runs as standalone EMIT tile launches over a batch of components;
 // this kernel then runs the remaining H stages.  One thread owns one
@@ -235,7 +254,7 @@ __global__ void __launch_bounds__(kPassBThreads) k_passb_regs(PassBArgs a) {
         __stcs(reinterpret_cast<int2*>(dst + (int64_t(i) << 15)), make_int2(w[2 * i], w[2 * i + 1]));
     }
     if (b + 1 >= b1 || (b + 1) / chunks != comp) {  // CTA-uniform
-      warp_publish_max(run, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
+      publish_comp(a, comp, run);
       run = 0;
     }
   }
@@ -267,7 +286,7 @@ __global__ void __launch_bounds__(kStagedThreads, 2) k_passb_staged(PassBArgs a)
     };
     run = max(run, passb_staged_chunk<H, MODE>(a, comp, b % S::PER_COMP, stg, tile, prefetch));
     if (nxt >= b1 || nxt / S::PER_COMP != comp) {  // CTA-uniform
-      warp_publish_max(run, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
+      publish_comp(a, comp, run);
       run = 0;
     }
   }

@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constan
           const uint32_t v = ring_mask(a.ring, a.v_first, ring_pos(a.ring, k, comp - k * a.ring.bc));
           warp_publish_max(run, a.max_abs + (v - a.v_first), a.key, v);
         } else {
-          warp_publish_max(run, a.max_abs + a.out_row0 + comp, a.key, a.v_first + uint32_t(comp));
+          publish_comp(a, comp, run);
         }
         run = 0;
       }

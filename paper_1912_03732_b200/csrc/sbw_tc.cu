@@ -256,6 +256,7 @@ struct TcArgs {
   int64_t n_comp, n_items;
   int n_full;
   uint32_t* emit;
+  uint32_t run_lo, run_hi;  // position v_first + j holds mask mask_at(., run_lo, run_hi)
   // SPEC (n = 16 materialised spectrum, mask-major): out[(v - v_lo) * ld + u]
   int32_t* out;
   int64_t ld;
@@ -285,7 +286,7 @@ __device__ __forceinline__ void item_at(const TcArgs& a, int64_t t, uint32_t& v,
       return;
     }
     bp = uint32_t(t / a.n_comp);
-    v = a.v_first + uint32_t(t - int64_t(bp) * a.n_comp);
+    v = mask_at(int64_t(a.v_first) + (t - int64_t(bp) * a.n_comp), a.run_lo, a.run_hi);
   } else {
     constexpr int LC = 16 - NB;
     const uint32_t b0 = a.v_lo >> LC, b1 = uint32_t(((int64_t(a.v_hi) - 1) >> LC) + 1);
@@ -486,6 +487,31 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     // (warp w may only touch lanes 32 * (w % 4) .. +31; here w % 4 == mw % 4)
     const int u = 128 * (mw >> 2) + 32 * (mw & 3) + lane;
     const uint32_t tbase = tmem + (uint32_t((mw & 3) * 32) << 16) + uint32_t(mw >> 2) * 256;
+    // EMIT: where this thread's words of item i go.  Batched: component slot
+    // = batch position.  Ring: slot r L + l of batch k's ring slot, after
+    // waiting (first item of a batch) until pass B has loaded batch k - R.
+    auto emit_dst = [&](int i) -> uint32_t* {
+      uint32_t vi, bpi;
+      item_at<MODE, NB>(a, t_lo + i, vi, bpi);
+      int64_t slot_comp = (t_lo + i) - int64_t(bpi) * a.n_comp;
+      if (ring) {
+        const int64_t rk = i / a.ring.L;
+        const int rl = int(i - rk * a.ring.L);
+        slot_comp = (rk % a.ring.R) * a.ring.bc + int64_t(blockIdx.x >> a.ring.log_t) * a.ring.L + rl;
+        if (rl == 0 && rk >= a.ring.R && !a.ring.nowait) {
+          if (lane == 0) ring_wait_geq(a.ring.freed + (rk - a.ring.R), a.ring.nb, a.ring.err, a.ring.wait_ns);
+          __syncwarp();
+        }
+      }
+      return a.emit + (slot_comp << (a.n_full - 1)) + (int64_t(2 * bpi) << 14) + 4 * u;
+    };
+    // Ring: this warp's part of batch k is stored after its last item of k.
+    auto emit_done = [&](int i) {
+      if (ring && (i + 1) % a.ring.L == 0) {
+        __syncwarp();
+        if (lane == 0) ring_signal(a.ring.ready + i / a.ring.L);
+      }
+    };
     for (int i = 0; i < n_my; ++i) {
       // prefetch the first plane of the item two steps ahead
       const bool gen = i + 2 < n_my;
@@ -581,23 +607,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         // layout (pass B only pairs equal positions across blocks):
         //   network (h, b = bits 0..1), group g = bits 4..5 ->
         //   words (4 b + g) * 1024 + 4 u + (0..3) <- R[64 h + b + 4 (4 g + 0..3)]
-        uint32_t vi, bpi;
-        item_at<MODE, NB>(a, t_lo + i, vi, bpi);
-        int64_t slot_comp = int64_t(vi - a.v_first);
-        int64_t rk = 0;
-        int rl = 0;
-        if (ring) {
-          // ring slot of this component; before the first store into batch
-          // k's slot, wait until pass B has loaded batch k - R out of it
-          rk = i / a.ring.L;
-          rl = int(i - rk * a.ring.L);
-          slot_comp = (rk % a.ring.R) * a.ring.bc + int64_t(blockIdx.x >> a.ring.log_t) * a.ring.L + rl;
-          if (rl == 0 && rk >= a.ring.R && !a.ring.nowait) {
-            if (lane == 0) ring_wait_geq(a.ring.freed + (rk - a.ring.R), a.ring.nb, a.ring.err, a.ring.wait_ns);
-            __syncwarp();
-          }
-        }
-        uint32_t* dst = a.emit + (slot_comp << (a.n_full - 1)) + (int64_t(2 * bpi) << 14) + 4 * u;
+        uint32_t* dst = emit_dst(i);
 #pragma unroll
         for (int net = 0; net < 8; ++net) {
           const int base = (net >> 2) * 64 + (net & 3);  // h = net >> 2, b = net & 3
@@ -616,10 +626,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
             *reinterpret_cast<uint4*>(dst + ((net >> 2) << 14) + (4 * (net & 3) + g) * 1024) =
                 make_uint4(R[base + 16 * g], R[base + 16 * g + 4], R[base + 16 * g + 8], R[base + 16 * g + 12]);
         }
-        if (ring && rl == a.ring.L - 1) {  // this warp's part of batch rk is stored
-          __syncwarp();
-          if (lane == 0) ring_signal(a.ring.ready + rk);
-        }
+        emit_done(i);
       } else {
         // c bits L..6 (register bits L-1..5, stages 8+L..14); register bit b is
         // c bit b+1, stage 9+b, diff bias 2^(9+b) per lane
@@ -633,16 +640,14 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
               R[k | (1 << sb)] = x - y + (0x02000200u << sb);
             }
         if constexpr (EMIT) {
-          // (SBW_TC_ROWS < 8 experiment builds) natural block word layout:
+          // natural block word layout (default, and SBW_TC_ROWS < 8 builds):
           //   word (j >> 2) * 1024 + 4 u + (j & 3)  <-  R[64 h + j]
           static_assert(!EMIT || NB == 16, "EMIT covers one 2^16 tile");
           if (!kC0Mma && u == 0) {
             R[0] += 0x4000u;
             R[64] += 0x4000u;
           }
-          uint32_t vi, bpi;
-          item_at<MODE, NB>(a, t_lo + i, vi, bpi);
-          uint32_t* dst = a.emit + (int64_t(vi - a.v_first) << (a.n_full - 1)) + (int64_t(2 * bpi) << 14) + 4 * u;
+          uint32_t* dst = emit_dst(i);
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -650,6 +655,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
               *reinterpret_cast<uint4*>(dst + (h << 14) + q * 1024) =
                   make_uint4(R[64 * h + 4 * q], R[64 * h + 4 * q + 1], R[64 * h + 4 * q + 2],
                              R[64 * h + 4 * q + 3]);
+          emit_done(i);
           continue;
         }
         // top stage (c bit NB-9 = register bit NB-10) fused with the max/min
@@ -875,8 +881,10 @@ int launch_tc16_spec(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32
 }
 
 int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_comp, uint32_t* emit,
-                   cudaStream_t st) {
+                   uint32_t run_lo, uint32_t run_hi, cudaStream_t st) {
   TcArgs a{};
+  a.run_lo = run_lo;
+  a.run_hi = run_hi;
   a.planes = planes;
   a.plane_words = (int64_t(1) << n) >> 5;
   a.v_first = v_first;
