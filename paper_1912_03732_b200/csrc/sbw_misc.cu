@@ -69,6 +69,87 @@ __global__ void __launch_bounds__(256) k_inplace_pass(int32_t* __restrict__ d, i
   }
 }
 
+// Low 12 bits of every column in one pass through shared memory: a CTA
+// loads a contiguous 4096-element tile with coalesced 16-byte loads, runs
+// the 12 stages as three register phases of 4 (bits {0,1,10,11}, {2..5},
+// {6..9}) with two swizzled shared-memory exchanges, and stores the tile
+// back coalesced (fusing the max|.| fold when these are the column's last
+// stages).  Replaces the first two strided 6-bit passes, whose b0 = 0 pass
+// reads 64 consecutive words per thread (uncoalesced).
+constexpr int kTileBits = 12, kTileThreads = 256;
+__device__ __forceinline__ int tile_swz(int p) { return p ^ (((p >> 6) & 7) << 2); }
+
+__device__ __forceinline__ void fwht16_u32(uint32_t (&e)[16]) {
+  // 4 stages over the index bits of e (bit b of the index <-> stride 1 << b)
+#pragma unroll
+  for (int s = 1; s < 16; s <<= 1)
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if ((i & s) == 0) {
+        const uint32_t a = e[i], b = e[i + s];
+        e[i] = a + b;
+        e[i + s] = a - b;
+      }
+}
+
+__global__ void __launch_bounds__(kTileThreads) k_inplace_tile12(int32_t* __restrict__ d, int k, int64_t count,
+                                                                 long long* max_abs) {
+  __shared__ __align__(16) uint32_t sm[1 << kTileBits];
+  __shared__ int s_red[kTileThreads / 32];
+  const int t = threadIdx.x;
+  const int64_t tiles_per_col = int64_t(1) << (k - kTileBits);
+  const int64_t tiles = count * tiles_per_col;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    uint32_t* g = reinterpret_cast<uint32_t*>(d) + (tile << kTileBits);
+    uint32_t e[16];
+    // phase 1: e[4 j + q] = tile[1024 j + 4 t + q] -> index bits {0, 1, 10, 11}
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint4 v = *reinterpret_cast<const uint4*>(g + 1024 * j + 4 * t);
+      e[4 * j] = v.x; e[4 * j + 1] = v.y; e[4 * j + 2] = v.z; e[4 * j + 3] = v.w;
+    }
+    fwht16_u32(e);
+    __syncthreads();  // previous tile's phase-3 reads of sm are done
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      *reinterpret_cast<uint4*>(sm + tile_swz(1024 * j + 4 * t)) =
+          make_uint4(e[4 * j], e[4 * j + 1], e[4 * j + 2], e[4 * j + 3]);
+    __syncthreads();
+    // phase 2: bits 2..5; thread base covers bits {0, 1, 6..11}
+    {
+      const int base = (t & 3) | ((t >> 2) << 6);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) e[i] = sm[tile_swz(base + 4 * i)];
+      fwht16_u32(e);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) sm[tile_swz(base + 4 * i)] = e[i];
+    }
+    __syncthreads();
+    // phase 3: bits 6..9; thread base covers bits {0..5, 10, 11}; straight to global
+    const int base = (t & 63) | ((t >> 6) << 10);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) e[i] = sm[tile_swz(base + 64 * i)];
+    fwht16_u32(e);
+    int mx = INT_MIN;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      g[base + 64 * i] = e[i];
+      mx = max(mx, wrap_abs(int(e[i])));
+    }
+    if (max_abs) {  // k == 12: this tile is a whole column
+      mx = __reduce_max_sync(0xffffffffu, unsigned(mx) ^ 0x80000000u) ^ 0x80000000u;
+      if ((t & 31) == 0) s_red[t >> 5] = mx;
+      __syncthreads();
+      if (t == 0) {
+        int m = s_red[0];
+#pragma unroll
+        for (int w = 1; w < kTileThreads / 32; ++w) m = max(m, s_red[w]);
+        max_abs[tile / tiles_per_col] = m;
+      }
+    }
+  }
+}
+
 __global__ void k_fill_i64(long long* p, int64_t count, long long v) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
        i += int64_t(gridDim.x) * blockDim.x)
@@ -122,6 +203,14 @@ int inplace_fwht(int32_t* d, int k, int64_t count, long long* max_abs, cudaStrea
     SBW_LAUNCH_CHECK("k_fill_i64");
   }
   int b0 = 0;
+  // k >= 12 (16-byte aligned columns): the low 12 bits in one shared-memory pass
+  if (k >= kTileBits && (reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+    const int64_t tiles = count << (k - kTileBits);
+    k_inplace_tile12<<<grid_for(tiles, 1, 8), kTileThreads, 0, st>>>(d, k, count,
+                                                                     k == kTileBits ? max_abs : nullptr);
+    SBW_LAUNCH_CHECK("k_inplace_tile12");
+    b0 = kTileBits;
+  }
   while (b0 < k) {
     const int nb = (k - b0) < 6 ? (k - b0) : 6;
     const bool last = b0 + nb == k;

@@ -209,12 +209,16 @@ int launch_k3_batched(const uint32_t* planes, int n, int m, uint32_t v_lo, uint3
   };
   // NL with the tensor-core pass A: Gray-ordered components (PassBArgs::gray)
   const bool gray = out == nullptr && tc_path_enabled();
+  // SBW_K3_SERIAL=1: pass A of batch b+1 waits for pass B of batch b (no
+  // overlap between the HBM-bound passes)
+  const bool serial = env_int("SBW_K3_SERIAL", 0) != 0;
   int64_t nb = 0;
   for (int64_t c0 = 0; c0 < total; c0 += bb, ++nb) {
     const int64_t nc = (total - c0) < bb ? (total - c0) : bb;
     const uint32_t vf = v_lo + uint32_t(c0);
     const int buf = int(nb & 1);
     if (nb >= 2) SBW_CUDA_CHECK(cudaStreamWaitEvent(ks->a, ks->done_b[buf], 0));  // buffer free
+    if (serial && nb >= 1) SBW_CUDA_CHECK(cudaStreamWaitEvent(ks->a, ks->done_b[buf ^ 1], 0));
     mark(ks->a);
     if (int rc = gray ? launch_tc_emit(planes, n, vf, nc, emit[buf], v_lo, v_hi, ks->a)
                      : launch_emit_tiles(planes, n, m, vf, nc, emit[buf], ks->a))

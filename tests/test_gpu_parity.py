@@ -358,6 +358,26 @@ def test_long_columns(k):
     assert np.array_equal(col, want) and mx == wmx
 
 
+@pytest.mark.parametrize("rows_n,k", [(3, 12), (5, 13), (2, 16), (1, 18)])
+def test_rows_in_place_tile_pass(rows_n, k):
+    """k >= 12 takes the shared-memory 12-bit tile pass (k_inplace_tile12) first;
+    values up to 2^30 exercise int32 wrap-around in every phase."""
+    rng = np.random.default_rng(100 + k)
+    rows = rng.integers(-(1 << 30), 1 << 30, size=(rows_n, 1 << k)).astype(np.int32)
+    rows[0, :] = rng.integers(-5, 6, size=1 << k)
+    want = np.stack([orc.fwht_column(r)[0] for r in rows])
+    wmx = [orc.fwht_column(r)[1] for r in rows]
+    got = rows.copy()
+    for i in range(rows_n):
+        _, mx = sw.fwht_column_in_place(got[i])
+        assert mx == wmx[i], (i, mx, wmx[i])
+    assert np.array_equal(got, want)
+    # all rows at once (one launch, per-row maxima)
+    got2 = rows.copy()
+    mx_rows = sw.transforms._inplace_rows(got2)
+    assert np.array_equal(got2, want) and mx_rows.tolist() == wmx
+
+
 def test_transform_rows_in_place_with_maxima():
     s = sw.generate_sbox(9, 6, seed=4)
     rows = orc.polarity_block(s.table, 1, 64)
