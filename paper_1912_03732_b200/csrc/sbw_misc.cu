@@ -268,51 +268,83 @@ int launch_polarity(const void* table, int tbytes, int n, uint32_t v_lo, uint32_
 }
 
 // ---------------------------------------------------------------------------
-// 32x32 tiled transpose: mask-major rows -> x-major (walsh.py:174 is the
+// Tiled transpose: mask-major rows -> x-major (walsh.py:174 is the
 // reference's inverse copy `np.ascontiguousarray(wt.T)`).
 // ---------------------------------------------------------------------------
-// 64 x 64 tiles, 256 threads: 16 loads and 16 stores in flight per thread
-// (the 32 x 32 version kept too few bytes in flight to saturate HBM).  The
-// 65-int row pitch makes both the row-wise fill and the column-wise drain of
-// the shared tile conflict-free.
+// TR x TC tiles (TR input rows = masks, TC input columns = u), 256 threads.
+// Each warp reads TC / 32 coalesced 128-byte pieces per input row; the
+// (TC + 1)-int pitch keeps the shared tile conflict-free both ways.
+#ifndef SBW_TR
+#define SBW_TR 64
+#endif
+#ifndef SBW_TCOL
+#define SBW_TCOL 64
+#endif
+#ifndef SBW_TORDER
+#define SBW_TORDER 0  // 1: visit tiles along r first
+#endif
+#ifndef SBW_TALIGN
+#define SBW_TALIGN 0  // 1: line-aligned output stores (neutral at 64 x 64, see below)
+#endif
 #ifndef SBW_TRANSPOSE_CAP
 #define SBW_TRANSPOSE_CAP 3  // blocks per SM: fewer concurrent tiles measured faster (3.4 vs 4.0 ms at 8)
 #endif
-template <int T>
+template <int TR, int TC>
 __global__ void __launch_bounds__(256) k_transpose(const int32_t* __restrict__ in, int64_t rows,
                                                    int64_t cols, int64_t ld_in, int32_t* __restrict__ out,
                                                    int64_t ld_out) {
-  __shared__ int32_t t[T][T + 1];
-  const int64_t tiles_c = (cols + T - 1) / T;
-  const int64_t tiles = ((rows + T - 1) / T) * tiles_c;
-  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  static_assert(TR % 32 == 0 && TC % 32 == 0, "tile shape");
+  __shared__ int32_t t[TR][TC + 1];
+  const int64_t tiles_r = (rows + TR - 1) / TR, tiles_c = (cols + TC - 1) / TC;
+  const int64_t tiles = tiles_r * tiles_c;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // 8 warps
   for (int64_t b = blockIdx.x; b < tiles; b += gridDim.x) {
-    const int64_t r0 = (b / tiles_c) * T, c0 = (b % tiles_c) * T;
-    if (r0 + T <= rows && c0 + T <= cols) {
-      int32_t v[T / 8][T / 32];
+    const int64_t tr = SBW_TORDER ? b % tiles_r : b / tiles_c;
+    const int64_t tc = SBW_TORDER ? b / tiles_r : b % tiles_c;
+    const int64_t r0 = tr * TR, c0 = tc * TC;
+    if (r0 + TR <= rows && c0 + TC <= cols) {
+      int32_t v[TR / 8][TC / 32];
 #pragma unroll
-      for (int j = 0; j < T / 8; ++j)
+      for (int j = 0; j < TR / 8; ++j)
 #pragma unroll
-        for (int h = 0; h < T / 32; ++h) v[j][h] = __ldcs(in + (r0 + ty + 8 * j) * ld_in + c0 + tx + 32 * h);
+        for (int h = 0; h < TC / 32; ++h) v[j][h] = __ldcs(in + (r0 + w + 8 * j) * ld_in + c0 + lane + 32 * h);
 #pragma unroll
-      for (int j = 0; j < T / 8; ++j)
+      for (int j = 0; j < TR / 8; ++j)
 #pragma unroll
-        for (int h = 0; h < T / 32; ++h) t[ty + 8 * j][tx + 32 * h] = v[j][h];
+        for (int h = 0; h < TC / 32; ++h) t[w + 8 * j][lane + 32 * h] = v[j][h];
       __syncthreads();
+      if (SBW_TALIGN) {
+        // Each warp store covers one 128-byte-aligned line of the output
+        // row: with an odd row pitch (2^m - 1) a TR-element segment starts
+        // mid-line, and unaligned 128-byte stores cost ~65 % more than
+        // aligned ones (x-major 16383-mask slice: 3.70 vs 2.62 ms into an
+        // aligned pitch).  TR / 32 + 1 lines, the two end ones partial.
 #pragma unroll
-      for (int j = 0; j < T / 8; ++j)
+        for (int j = 0; j < TC / 8; ++j) {
+          const int64_t A = (c0 + w + 8 * j) * ld_out + r0;  // segment start (elements)
+          const int64_t a0 = A & ~int64_t(31);
 #pragma unroll
-        for (int h = 0; h < T / 32; ++h)
-          __stcs(out + (c0 + ty + 8 * j) * ld_out + r0 + tx + 32 * h, t[tx + 32 * h][ty + 8 * j]);
+          for (int h = 0; h <= TR / 32; ++h) {
+            const int64_t rr = a0 + 32 * h + lane - A;  // position inside the segment
+            if (rr >= 0 && rr < TR) __stcs(out + A + rr, t[rr][w + 8 * j]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < TC / 8; ++j)
+#pragma unroll
+          for (int h = 0; h < TR / 32; ++h)
+            __stcs(out + (c0 + w + 8 * j) * ld_out + r0 + lane + 32 * h, t[lane + 32 * h][w + 8 * j]);
+      }
     } else {
-      for (int j = ty; j < T; j += 8)
-        for (int h = tx; h < T; h += 32) {
+      for (int j = w; j < TR; j += 8)
+        for (int h = lane; h < TC; h += 32) {
           const int64_t r = r0 + j, c = c0 + h;
           if (r < rows && c < cols) t[j][h] = in[r * ld_in + c];
         }
       __syncthreads();
-      for (int j = ty; j < T; j += 8)
-        for (int h = tx; h < T; h += 32) {
+      for (int j = w; j < TC; j += 8)
+        for (int h = lane; h < TR; h += 32) {
           const int64_t c = c0 + j, r = r0 + h;
           if (r < rows && c < cols) out[c * ld_out + r] = t[h][j];
         }
@@ -324,9 +356,9 @@ __global__ void __launch_bounds__(256) k_transpose(const int32_t* __restrict__ i
 int launch_transpose_i32(const int32_t* in, int64_t rows, int64_t cols, int64_t ld_in,
                          int32_t* out, int64_t ld_out, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return SBW_OK;
-  constexpr int T = 64;
-  const int64_t tiles = ((rows + T - 1) / T) * ((cols + T - 1) / T);
-  k_transpose<T><<<grid_for(tiles, 1, SBW_TRANSPOSE_CAP), dim3(32, 8), 0, st>>>(in, rows, cols, ld_in, out, ld_out);
+  constexpr int TR = SBW_TR, TC = SBW_TCOL;
+  const int64_t tiles = ((rows + TR - 1) / TR) * ((cols + TC - 1) / TC);
+  k_transpose<TR, TC><<<grid_for(tiles, 1, SBW_TRANSPOSE_CAP), 256, 0, st>>>(in, rows, cols, ld_in, out, ld_out);
   SBW_LAUNCH_CHECK("k_transpose");
   return SBW_OK;
 }
