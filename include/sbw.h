@@ -170,6 +170,29 @@ int sbw_int32_peak(double* ops_per_s, double* ms, void* stream);
  */
 int sbw_int8_mma_peak(double* ops_per_s, double* ms, void* stream);
 
+/*
+ * Multi-GPU exchange over peer memory (NVLink), no collective library on the
+ * data path.  Replaces the all-reduce / all-gather of the per-worker results
+ * in fwht_parallel (parallel.py:118-126) when the workers are processes on
+ * different GPUs: the root allocates the result buffers with sbw_ipc_alloc,
+ * the other ranks map them with sbw_ipc_open, and every rank's sbw_nl writes
+ * its component maxima straight into the root's array (d_max_abs = the mapped
+ * pointer + (v_lo - 1)); sbw_key_merge then folds the rank's key into the
+ * root's with one system-scope atomicMax.
+ *   sbw_ipc_alloc: cudaMalloc(bytes) zeroed on the current device + its
+ *                  64-byte cudaIpcMemHandle in handle_out.
+ *   sbw_ipc_open:  map a handle from another process (any device with peer
+ *                  access to the owner, or the owner's device itself).
+ *   sbw_ipc_close / sbw_ipc_free: unmap / free.
+ */
+int sbw_ipc_alloc(size_t bytes, void** d_ptr_out, void* handle_out);
+int sbw_ipc_open(const void* handle, void** d_ptr_out);
+int sbw_ipc_close(void* d_ptr);
+int sbw_ipc_free(void* d_ptr);
+int sbw_key_merge(const unsigned long long* d_key, unsigned long long* d_dst_key, void* stream);
+/* Copy `bytes` between any two device (or mapped peer) addresses, async on `stream`. */
+int sbw_peer_copy(void* d_dst, const void* d_src, size_t bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

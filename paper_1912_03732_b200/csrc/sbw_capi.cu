@@ -380,4 +380,51 @@ int sbw_int8_mma_peak(double* ops_per_s, double* ms, void* stream) {
   return run_int8_mma_peak(ops_per_s, ms, as_stream(stream));
 }
 
+int sbw_ipc_alloc(size_t bytes, void** d_ptr_out, void* handle_out) {
+  if (!d_ptr_out || !handle_out || bytes == 0) return set_error(SBW_EINVAL, "sbw_ipc_alloc: bad arguments");
+  void* p = nullptr;
+  SBW_CUDA_CHECK(cudaMalloc(&p, bytes));
+  SBW_CUDA_CHECK(cudaMemset(p, 0, bytes));
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return cuda_error(e, "cudaIpcGetMemHandle");
+  }
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle_out, &h, sizeof(h));
+  *d_ptr_out = p;
+  return SBW_OK;
+}
+
+int sbw_ipc_open(const void* handle, void** d_ptr_out) {
+  if (!handle || !d_ptr_out) return set_error(SBW_EINVAL, "sbw_ipc_open: bad arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  SBW_CUDA_CHECK(cudaIpcOpenMemHandle(d_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return SBW_OK;
+}
+
+int sbw_ipc_close(void* d_ptr) {
+  SBW_CUDA_CHECK(cudaIpcCloseMemHandle(d_ptr));
+  return SBW_OK;
+}
+
+int sbw_ipc_free(void* d_ptr) {
+  SBW_CUDA_CHECK(cudaFree(d_ptr));
+  return SBW_OK;
+}
+
+int sbw_key_merge(const unsigned long long* d_key, unsigned long long* d_dst_key, void* stream) {
+  if (!d_key || !d_dst_key) return set_error(SBW_EINVAL, "sbw_key_merge: null key");
+  return launch_key_merge(d_key, d_dst_key, as_stream(stream));
+}
+
+int sbw_peer_copy(void* d_dst, const void* d_src, size_t bytes, void* stream) {
+  if (bytes == 0) return SBW_OK;
+  if (!d_dst || !d_src) return set_error(SBW_EINVAL, "sbw_peer_copy: null pointer");
+  SBW_CUDA_CHECK(cudaMemcpyAsync(d_dst, d_src, bytes, cudaMemcpyDefault, as_stream(stream)));
+  return SBW_OK;
+}
+
 }  // extern "C"

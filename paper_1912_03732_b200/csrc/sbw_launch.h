@@ -84,6 +84,8 @@ int launch_walsh_direct(const void* table, int tbytes, int n, const uint32_t* u,
                         const uint32_t* v, int64_t count, int32_t* out, cudaStream_t st);
 int launch_bruteforce(const void* table, int tbytes, int n, int m, int32_t* best,
                       cudaStream_t st);
+// *dst = max(*dst, *src) with a system-scope atomic (dst may be peer memory).
+int launch_key_merge(const unsigned long long* src, unsigned long long* dst, cudaStream_t st);
 int run_int32_peak(double* ops_per_s, double* ms_out, cudaStream_t st);
 int run_int8_mma_peak(double* ops_per_s, double* ms_out, cudaStream_t st);
 

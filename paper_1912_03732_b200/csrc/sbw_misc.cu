@@ -363,6 +363,18 @@ int launch_transpose_i32(const int32_t* in, int64_t rows, int64_t cols, int64_t 
   return SBW_OK;
 }
 
+// Fold a rank's (max|W|, smallest v) key into the root's over peer memory:
+// system scope, so atomics arriving from several GPUs serialise correctly.
+__global__ void k_key_merge(const unsigned long long* src, unsigned long long* dst) {
+  atomicMax_system(dst, *src);
+}
+
+int launch_key_merge(const unsigned long long* src, unsigned long long* dst, cudaStream_t st) {
+  k_key_merge<<<1, 1, 0, st>>>(src, dst);
+  SBW_LAUNCH_CHECK("k_key_merge");
+  return SBW_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Reducers.
 // ---------------------------------------------------------------------------

@@ -44,6 +44,12 @@ SIGNATURES = {
     "sbw_nl_host": (_i32, [_vp, _i32, _i32, _u32, _u32, _vp, _vp, _i32]),
     "sbw_int32_peak": (_i32, [_c.POINTER(_c.c_double), _c.POINTER(_c.c_double), _vp]),
     "sbw_int8_mma_peak": (_i32, [_c.POINTER(_c.c_double), _c.POINTER(_c.c_double), _vp]),
+    "sbw_ipc_alloc": (_i32, [_sz, _c.POINTER(_vp), _vp]),
+    "sbw_ipc_open": (_i32, [_vp, _c.POINTER(_vp)]),
+    "sbw_ipc_close": (_i32, [_vp]),
+    "sbw_ipc_free": (_i32, [_vp]),
+    "sbw_key_merge": (_i32, [_vp, _vp, _vp]),
+    "sbw_peer_copy": (_i32, [_vp, _vp, _sz, _vp]),
 }
 
 

@@ -112,8 +112,65 @@ def _gpu_shard(s: SBox, lo: int, hi: int):
     return maxabs_to_nl(mx, s.n), int(key.item())
 
 
-def evaluate_distributed(s: SBox, group=None, compute=None,
-                         return_values: bool = True) -> tuple[NonlinearityResult, ColumnMaxima | None]:
+def _evaluate_p2p(s: SBox, group, lo: int, hi: int, total: int,
+                  return_values: bool) -> tuple[int, np.ndarray | None]:
+    """Peer-memory exchange (sbw_ipc_* / sbw_key_merge, include/sbw.h).
+
+    Rank 0 owns int32 max|W|[2^m - 1] + the uint64 key in IPC-exportable
+    device memory; every rank maps them, its sbw_nl stores its component
+    maxima straight into rank 0's array (over NVLink when the ranks sit on
+    different GPUs) and one system-scope atomicMax folds its key into rank
+    0's.  The process group only carries the 64-byte handles and two
+    barriers.  Returns (key, per-component NL int64 or None), read back by
+    every rank from rank 0's memory.
+    """
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    lib = _dev.load_library()
+    dev = _dev.require_device()
+    torch.cuda.set_device(dev)
+    rank = dist.get_rank(group)
+    nbytes = 8 + 4 * total  # the uint64 key (8-byte aligned), then int32 max|W| per component
+    handle = ctypes.create_string_buffer(64)
+    base = ctypes.c_void_p()
+    if rank == 0:
+        _dev.check(lib.sbw_ipc_alloc(nbytes, ctypes.byref(base), handle))
+    obj = [handle.raw if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    if rank != 0:
+        _dev.check(lib.sbw_ipc_open(ctypes.create_string_buffer(obj[0], 64), ctypes.byref(base)))
+    root = int(base.value)
+    try:
+        stream = _dev.stream_handle(dev)
+        if hi > lo:
+            tab = _dev.device_table(s, dev)
+            key = torch.zeros(1, dtype=torch.int64, device=dev)
+            sb = lib.sbw_nl_scratch_bytes(s.n, s.m, lo, hi)
+            scratch = torch.empty(max(1, sb), dtype=torch.uint8, device=dev)
+            _dev.check(lib.sbw_nl(_dev.ptr(tab), _dev.table_bytes(s.m), s.n, s.m, lo, hi,
+                                  root + 8 + 4 * (lo - 1), _dev.ptr(key), _dev.ptr(scratch), sb, stream))
+            _dev.check(lib.sbw_key_merge(_dev.ptr(key), root, stream))
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)  # every shard is in rank 0's memory
+        out = torch.empty(2 + total, dtype=torch.int32, device=dev)
+        _dev.check(lib.sbw_peer_copy(_dev.ptr(out), root, nbytes if return_values else 8, stream))
+        torch.cuda.synchronize(dev)
+        k = int(out[:2].view(torch.int64).item())
+        values = maxabs_to_nl(out[2:], s.n) if return_values else None
+        dist.barrier(group=group)  # nobody reads rank 0's buffer any more
+    finally:
+        if rank == 0:
+            lib.sbw_ipc_free(base)
+        else:
+            lib.sbw_ipc_close(base)
+    return k, values
+
+
+def evaluate_distributed(s: SBox, group=None, compute=None, return_values: bool = True,
+                         transport: str = "collective") -> tuple[NonlinearityResult, ColumnMaxima | None]:
     """Whole-S-box NL with the masks sharded over the ranks of `group`.
 
     Rank r owns partition_columns(2^m - 1, world)[r] (the reference's static
@@ -122,6 +179,10 @@ def evaluate_distributed(s: SBox, group=None, compute=None,
     the padded per-component NL shards.  `compute(s, lo, hi) -> (nl_int64,
     key)` defaults to the GPU; tests inject the CPU oracle to exercise the
     exchange on gloo.
+
+    transport="p2p" (one process per GPU, CUDA devices required): no
+    collective on the data path -- the shards' maxima and keys are written
+    into rank 0's device memory through CUDA IPC mappings (_evaluate_p2p).
     """
     import torch
     import torch.distributed as dist
@@ -132,6 +193,18 @@ def evaluate_distributed(s: SBox, group=None, compute=None,
     part = partition_columns(total, world)
     ranges = list(part.ranges) + [(total + 1, total + 1)] * (world - len(part.ranges))
     lo, hi = ranges[rank]
+    if transport == "p2p":
+        if compute is not None:
+            raise ValueError("transport='p2p' runs the shards on the GPU; compute= is not supported")
+        k, values = _evaluate_p2p(s, group, lo, hi, total, return_values)
+        mxw = k >> 32
+        gap = (1 << s.n) - mxw
+        if gap & 1:
+            raise AssertionError("spectrum maximum has wrong parity")
+        result = NonlinearityResult(gap >> 1, 0xFFFFFFFF - (k & 0xFFFFFFFF), "distributed")
+        return result, (ColumnMaxima(s.n, s.m, values) if return_values else None)
+    if transport != "collective":
+        raise ValueError(f"transport must be 'collective' or 'p2p', got {transport!r}")
     compute = compute or _gpu_shard
     if hi > lo:
         nl, key = compute(s, lo, hi)
