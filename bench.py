@@ -324,9 +324,9 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- roofline of the dominant kernel (fused NL) ----------------------
     peak = live_peak(lib, d, "sbw_int32_peak")
-    # sbw_nl takes the tensor-core kernel for n = 11..16 (n < 16: 2^(16-n)
+    # sbw_nl takes the tensor-core kernel for n = 12..16 (n < 16: 2^(16-n)
     # components per 2^16 tile; needs m >= 16 - n), unless SBW_TC=0
-    tc_path = 11 <= n <= 16 and m >= 16 - n and os.environ.get("SBW_TC", "1") != "0"
+    tc_path = 12 <= n <= 16 and m >= 16 - n and os.environ.get("SBW_TC", "1") != "0"
     prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_traffic.json")
     traffic = None
     if os.path.exists(prof):
@@ -335,9 +335,9 @@ def run_ours(args, rank, world, local_rank):
     if tc_path:
         # k_tc_hybrid<NL>: the r stages (x bits 0..7) run as an int8 GEMM on
         # the tensor cores; the c stages (x bits 8..15) run on the integer
-        # ALUs -- 3 of them as byte-lane butterflies on the bit rows of the
-        # GEMM's B operand (c bits 0..2, inside the generation), 5 as packed
-        # 16-bit stages after the GEMM (c bits 3..7, incl. the max fold).  The
+        # ALUs -- 4 of them as byte-lane butterflies on the bit rows of the
+        # GEMM's B operand (c bits 0..3, inside the generation), 4 as packed
+        # 16-bit stages after the GEMM (c bits 4..7, incl. the max fold).  The
         # integer half is the limiter (ALU pipe ~80 %), so it is the primary
         # roofline: 8 stages x 2^16 butterfly element-ops per component
         # against the packed-16x2 rate (2 x the live int32 lane-op peak; the
@@ -354,12 +354,12 @@ def run_ours(args, rank, world, local_rank):
         roofline = {
             "bound": "int32_alu",
             "kernel": f"k_tc_hybrid<NL, {n}> (tcgen05 int8 GEMM over x bits 0..7; x bits 8..{n - 1} on "
-                      "the integer ALUs: 3 byte-lane stages on the GEMM operand + packed int16 stages)",
+                      "the integer ALUs: 4 byte-lane stages on the GEMM operand + packed int16 stages)",
             "achieved": achieved / 1e12, "peak": 2 * peak / 1e12, "unit": "Tops/s",
             "frac": achieved / (2 * peak), "traffic": traffic,
             "ops_per_launch": alu_ops,
             "ops_definition": "integer half: (n-8) stages x 2^n butterfly element-ops per component "
-                              "(x bits 8..n-1: 3 byte-lane + n-11 int16-lane stages incl. the "
+                              "(x bits 8..n-1: 4 byte-lane + n-12 int16-lane stages incl. the "
                               "max fold); the r stages run as the int8 GEMM below",
             "kernel_ms": kern_ms,
             "peak_source": "measured live by sbw_int32_peak (int32 lane-ops/s) x 2 lanes for "

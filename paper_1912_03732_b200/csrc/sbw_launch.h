@@ -25,6 +25,7 @@ int launch_tc16_nl(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t
 bool tc_path_enabled();
 // Tensor-core NL for n = 11..15 (2^(16-n) components per 2^16 tile); needs
 // m >= 16 - n so every slot's mask is a valid mask.
+int tc_min_small_n();  // smallest n of launch_tc_nl_small (11, or 12 for 16-row generation builds)
 int launch_tc_nl_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
                        unsigned long long* key, cudaStream_t st);
 // Tensor-core n = 16 materialised spectrum, mask-major rows out[(v - v_lo) * ld + u].

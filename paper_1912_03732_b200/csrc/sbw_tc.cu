@@ -55,7 +55,7 @@ namespace sbw {
 namespace {
 
 #ifndef SBW_TC_ROWS
-#define SBW_TC_ROWS 8
+#define SBW_TC_ROWS 16
 #endif
 // SBW_TC_ROWS = R: the B operand rows come in groups of R = 2^L consecutive c
 // holding the R-point WHT of their bit rows (unsigned, offset R/2 on all but
@@ -66,16 +66,24 @@ constexpr int kRows = SBW_TC_ROWS;
 // EMIT store order: 1 = per 16-register network as soon as it is final (5 %
 // faster pass A in the L2 ring, 1 % slower in the HBM-bound batched path),
 // 0 = all stores after the stages (default).
+#ifndef SBW_R16_LATE
+#define SBW_R16_LATE 0  // 1: R = 16 stores B(i+2) after the item's stages (measured 2 % slower)
+#endif
+constexpr bool kLateB = SBW_TC_ROWS == 16 && SBW_R16_LATE;
 #ifndef SBW_EMIT_NET
 #define SBW_EMIT_NET 0
 #endif
-static_assert(kRows == 1 || kRows == 2 || kRows == 8, "SBW_TC_ROWS must be 1, 2 or 8");
-constexpr int kLogRows = kRows == 8 ? 3 : (kRows == 2 ? 1 : 0);
+static_assert(kRows == 1 || kRows == 2 || kRows == 8 || kRows == 16, "SBW_TC_ROWS must be 1, 2, 8 or 16");
+constexpr int kLogRows = kRows == 16 ? 4 : (kRows == 8 ? 3 : (kRows == 2 ? 1 : 0));
 constexpr bool kC0Mma = kRows > 1;
 // bias per D entry: 128 R on every row, 128 R more on row u = 0, as columns of
-// 127 (plus a remainder) against all-ones B columns
+// 127 (plus a remainder) against B columns of kBiasB (2 for R = 16, so both
+// bias column sets fit one 32-wide K block)
 constexpr int kBiasT = 128 * kRows;
-constexpr int kBiasCols = (kBiasT + 126) / 127;
+constexpr int kBiasB = kRows == 16 ? 2 : 1;
+constexpr int kBiasCols = (kBiasT / kBiasB + 126) / 127;
+// generation state: plane words per transform thread (R = 16: word ks of 16 rows)
+constexpr int kGW = kRows == 16 ? 16 : 8;
 constexpr int kMathWarps = 8;
 constexpr int kKA = kC0Mma ? 288 : 256;        // K of A: 256 (r) [+ 32 bias block]
 constexpr int kAHalf = 128 * kKA;              // one M = 128 half of A
@@ -100,20 +108,22 @@ __device__ __forceinline__ int r_of_p(int p) { return (p & ~31) | ((p & 3) << 3)
 __device__ __forceinline__ int a_value(int u, int p) {
   if (p < 256) return (__popc(u & r_of_p(p)) & 1) ? 1 : -1;
   const int k = p - 256;
-  const int col = k % kBiasCols, last = kBiasT - 127 * (kBiasCols - 1);
+  const int col = k % kBiasCols, last = kBiasT / kBiasB - 127 * (kBiasCols - 1);
   if (k < kBiasCols) return col < kBiasCols - 1 ? 127 : last;
   if (k < 2 * kBiasCols) return u == 0 ? (col < kBiasCols - 1 ? 127 : last) : 0;
   return 0;
 }
 
 
-__device__ __forceinline__ void xor_plane(uint32_t (&g)[8], const uint4& a, const uint4& b) {
-  g[0] ^= a.x; g[1] ^= a.y; g[2] ^= a.z; g[3] ^= a.w;
-  g[4] ^= b.x; g[5] ^= b.y; g[6] ^= b.z; g[7] ^= b.w;
+__device__ __forceinline__ void xor_plane(uint32_t (&g)[kGW], const uint4 (&p)[kGW / 4]) {
+#pragma unroll
+  for (int q = 0; q < kGW / 4; ++q) {
+    g[4 * q] ^= p[q].x; g[4 * q + 1] ^= p[q].y; g[4 * q + 2] ^= p[q].z; g[4 * q + 3] ^= p[q].w;
+  }
 }
 
 // Expand the 256 bits of row c into the u8 B operand (K-major core matrices).
-[[maybe_unused]] __device__ __forceinline__ void store_row(const uint32_t (&g)[8], uint8_t* bbuf, int c) {
+[[maybe_unused]] __device__ __forceinline__ void store_row(const uint32_t* g, uint8_t* bbuf, int c) {
   uint8_t* row = bbuf + (c >> 3) * 2048 + (c & 7) * 16;
   constexpr uint32_t M = 0x01010101u;
 #pragma unroll
@@ -133,7 +143,7 @@ __device__ __forceinline__ void xor_plane(uint32_t (&g)[8], const uint4& a, cons
 // at i * 128, logical chunk c at chunk c ^ i.  The two K halves of a row pair
 // write chunks 2w + kh first and 2w + 1 - kh second, so the 8 threads of a
 // store phase hit 8 different 16-byte bank groups.
-[[maybe_unused]] __device__ __forceinline__ void store_rows_sw128(const uint32_t (&g)[8], uint8_t* bbuf, int j, int kh) {
+[[maybe_unused]] __device__ __forceinline__ void store_rows_sw128(const uint32_t* g, uint8_t* bbuf, int j, int kh) {
   const int i0 = (2 * j) & 7;
   uint8_t* a0 = bbuf + (kh * 32 + (j >> 2)) * 1024 + i0 * 128;  // row 2j (sum)
   uint8_t* a1 = a0 + 128;                                          // row 2j+1 (diff)
@@ -165,7 +175,7 @@ __device__ __forceinline__ void xor_plane(uint32_t (&g)[8], const uint4& a, cons
 // every output is in [0, 8]); output e goes to row 8j + e.  Threads with
 // ks >= 4 store their second chunk first, so a store phase (8 threads, one
 // row e, ks = 0..7) covers all 8 chunk positions c ^ e: no bank conflicts.
-[[maybe_unused]] __device__ __forceinline__ void store_rows8_sw128(const uint32_t (&g)[8], uint8_t* bbuf, int j, int ks) {
+[[maybe_unused]] __device__ __forceinline__ void store_rows8_sw128(const uint32_t* g, uint8_t* bbuf, int j, int ks) {
   uint8_t* base = bbuf + ((ks >> 2) * 32 + j) * 1024;
   constexpr uint32_t M = 0x01010101u;
   const int s4 = 4 * (ks >> 2);
@@ -195,6 +205,43 @@ __device__ __forceinline__ void xor_plane(uint32_t (&g)[8], const uint4& a, cons
     for (int e = 0; e < 8; ++e)
       *reinterpret_cast<uint4*>(base + e * 128 + ((c ^ e) << 4)) = make_uint4(o[e][0], o[e][1], o[e][2], o[e][3]);
   }
+}
+
+// R = 16 generation: thread (j, ks, kq) owns plane word ks of the 16 rows
+// 16 j .. 16 j + 15 (g[e] = row 16 j + e) and the bit positions k = 4 kq ..
+// 4 kq + 3 of its bytes, i.e. one 16-byte chunk (2 (ks & 3) + kq of SW128
+// atom column ks >> 2) of every row.  Per k the 16 byte vectors run through
+// a biased 16-point WHT (every output in [0, 16]).  A store phase (8 threads:
+// ks = 0..3 or 4..7, kq = 0, 1) covers the 8 chunk positions of one atom
+// row: no bank conflicts.
+[[maybe_unused]] __device__ __forceinline__ void store_rows16_sw128(const uint32_t* g, uint8_t* bbuf, int j,
+                                                                    int ks, int kq) {
+  uint8_t* base = bbuf + ((ks >> 2) * 32 + 2 * j) * 1024;
+  constexpr uint32_t M = 0x01010101u;
+  uint32_t o[16][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int k = 4 * kq + q;
+    uint32_t b[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) b[e] = (g[e] >> k) & M;
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if ((e & (1 << t)) == 0) {
+          const uint32_t x = b[e], y = b[e | (1 << t)];
+          b[e] = x + y;
+          b[e | (1 << t)] = x - y + (M << t);  // per byte in [0, 2^(t+1)]: no borrow
+        }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) o[e][q] = b[e];
+  }
+  const int c = 2 * (ks & 3) + kq;  // logical chunk of this thread in every row
+#pragma unroll
+  for (int e = 0; e < 16; ++e)
+    *reinterpret_cast<uint4*>(base + (e >> 3) * 1024 + (e & 7) * 128 + ((c ^ (e & 7)) << 4)) =
+        make_uint4(o[e][0], o[e][1], o[e][2], o[e][3]);
 }
 
 __device__ __forceinline__ void publish(const uint32_t* wmax, uint32_t v, uint32_t v_lo,
@@ -298,7 +345,7 @@ __device__ __forceinline__ void item_at(const TcArgs& a, int64_t t, uint32_t& v,
 // Generation state of one transform thread: row c's 8 plane words for mask
 // vcur in block bpcur.
 struct GenState16 {
-  uint32_t g[8];
+  uint32_t g[kGW];
   uint32_t vcur, bpcur;
 };
 
@@ -323,7 +370,7 @@ __global__ void k_tc_consts(uint8_t* img) {
     static_assert(2 * kBiasCols <= 32, "bias block is one K block");
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 256 * 32; e += gridDim.x * blockDim.x) {
       const int n = e >> 5, k = e & 31;
-      img[kBbOff + ((n >> 3) * 2 + (k >> 4)) * 128 + (n & 7) * 16 + (k & 15)] = k < 2 * kBiasCols ? 1 : 0;
+      img[kBbOff + ((n >> 3) * 2 + (k >> 4)) * 128 + (n & 7) * 16 + (k & 15)] = k < 2 * kBiasCols ? kBiasB : 0;
     }
   }
 }
@@ -340,7 +387,7 @@ __device__ __forceinline__ void publish_item(const TcArgs& a, const uint32_t* wm
 template <int MODE, int NB = 16>
 __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
   constexpr bool EMIT = MODE == kTcEmit;
-  static_assert(NB == 16 || (MODE == kTcNL && NB >= 11 && kRows == 8), "n < 16: NL with 8-row groups");
+  static_assert(NB == 16 || (MODE == kTcNL && NB >= 8 + kLogRows && kRows >= 8), "n < 16: NL with 8/16-row groups");
   constexpr int kSlots = 1 << (16 - NB);  // components per 2^16 tile
   static_assert(MODE != kTcSpec || kC0Mma, "exact SPEC output needs the bias-block GEMM");
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -404,17 +451,21 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kMathRegs));
     const int mt = tid - 128, mw = mt >> 5;  // transform thread / warp index
     const int c = mt;                        // generation row (plain B rows)
-    const int gj = kRows == 8 ? mt >> 3 : mt >> 1;  // C0MMA: row group
-    const int gkh = kRows == 8 ? mt & 7 : mt & 1;   // C0MMA: plane word (R = 8) / K half (R = 2)
+    const int gj = kRows == 16 ? mt >> 4 : (kRows == 8 ? mt >> 3 : mt >> 1);  // C0MMA: row group
+    // C0MMA: plane word (R = 8, 16) / K half (R = 2); R = 16 also splits the
+    // bit positions of the bytes: gkq = k half
+    const int gkh = kRows == 16 ? (mt >> 1) & 7 : (kRows == 8 ? mt & 7 : mt & 1);
+    const int gkq = mt & 1;
     const uint32_t* __restrict__ planes = a.planes;
     const int64_t pw = EMIT ? a.plane_words : (int64_t(1) << NB) >> 5;
     // NB < 16: this thread's 8 rows belong to slot gslot; its rows within the
     // component start at row group gj mod 2^(NB - 11)
-    const uint32_t gslot = NB < 16 ? uint32_t(gj >> (NB - 11)) : 0u;
-    const int gjc = NB < 16 ? (gj & ((1 << (NB - 11)) - 1)) : gj;
+    constexpr int kGrpLog = NB - 8 - kLogRows;  // log2 row groups per component (NB < 16)
+    const uint32_t gslot = NB < 16 ? uint32_t(gj >> kGrpLog) : 0u;
+    const int gjc = NB < 16 ? (gj & ((1 << kGrpLog) - 1)) : gj;
     GenState16 gs;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) gs.g[k] = 0;
+    for (int k = 0; k < kGW; ++k) gs.g[k] = 0;
     gs.vcur = 0;
     gs.bpcur = 0;
     // plane words of this thread's generation state in block bp: row c's 8
@@ -422,25 +473,26 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     // 2j+1 at bp * 2048 + 16 j + 4 kh (+ 8)
     auto row_off = [&](uint32_t bp) {
       return int64_t(bp) * 2048 +
-             (kRows == 8 ? 64 * gjc + gkh : (kRows == 2 ? 16 * gj + 4 * gkh : c * 8));
+             (kRows >= 8 ? 8 * kRows * gjc + gkh : (kRows == 2 ? 16 * gj + 4 * gkh : c * 8));
     };
-    auto load_pl = [&](int i, uint32_t bp, uint4& x, uint4& y) {
+    auto load_pl = [&](int i, uint32_t bp, uint4 (&x)[kGW / 4]) {
       const uint32_t* p = planes + int64_t(i) * pw + row_off(bp);
-      if constexpr (kRows == 8) {  // word gkh of rows 8 j + e: stride 8 words
-        x = make_uint4(__ldg(p), __ldg(p + 8), __ldg(p + 16), __ldg(p + 24));
-        y = make_uint4(__ldg(p + 32), __ldg(p + 40), __ldg(p + 48), __ldg(p + 56));
+      if constexpr (kRows >= 8) {  // word gkh of rows R j + e: stride 8 words
+#pragma unroll
+        for (int q = 0; q < kGW / 4; ++q)
+          x[q] = make_uint4(__ldg(p + 32 * q), __ldg(p + 32 * q + 8), __ldg(p + 32 * q + 16), __ldg(p + 32 * q + 24));
       } else {
-        x = __ldg(reinterpret_cast<const uint4*>(p));
-        y = __ldg(reinterpret_cast<const uint4*>(p) + (kC0Mma ? 2 : 1));
+        x[0] = __ldg(reinterpret_cast<const uint4*>(p));
+        x[1] = __ldg(reinterpret_cast<const uint4*>(p) + (kC0Mma ? 2 : 1));
       }
     };
     auto xor_all = [&](uint32_t d, uint32_t bp) {
       while (d) {
         const int i = __ffs(d) - 1;
         d &= d - 1;
-        uint4 x, y;
-        load_pl(i, bp, x, y);
-        xor_plane(gs.g, x, y);
+        uint4 x[kGW / 4];
+        load_pl(i, bp, x);
+        xor_plane(gs.g, x);
       }
     };
     // full recompute (first items): the planes of all set bits of d, 8 at a
@@ -448,19 +500,21 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     auto xor_full = [&](uint32_t d, uint32_t bp) {
 #pragma unroll 1
       for (int i0 = 0; i0 < 32 && (d >> i0); i0 += 8) {
-        uint4 x[8], y[8];
+        uint4 x[8][kGW / 4];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          x[q] = make_uint4(0, 0, 0, 0);
-          y[q] = x[q];
-          if ((d >> (i0 + q)) & 1u) load_pl(i0 + q, bp, x[q], y[q]);
+#pragma unroll
+          for (int h = 0; h < kGW / 4; ++h) x[q][h] = make_uint4(0, 0, 0, 0);
+          if ((d >> (i0 + q)) & 1u) load_pl(i0 + q, bp, x[q]);
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) xor_plane(gs.g, x[q], y[q]);
+        for (int q = 0; q < 8; ++q) xor_plane(gs.g, x[q]);
       }
     };
     auto store_b = [&](int buf) {
-      if constexpr (kRows == 8)
+      if constexpr (kRows == 16)
+        store_rows16_sw128(gs.g, smem + kBOff + buf * kBBytes, gj, gkh, gkq);
+      else if constexpr (kRows == 8)
         store_rows8_sw128(gs.g, smem + kBOff + buf * kBBytes, gj, gkh);
       else if constexpr (kRows == 2)
         store_rows_sw128(gs.g, smem + kBOff + buf * kBBytes, gj, gkh);
@@ -473,7 +527,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
       vn |= gslot;
       if (EMIT && bpn != gs.bpcur) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) gs.g[q] = 0;
+        for (int q = 0; q < kGW; ++q) gs.g[q] = 0;
         gs.vcur = 0;
         gs.bpcur = bpn;
       }
@@ -517,14 +571,16 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
       const bool gen = i + 2 < n_my;
       uint32_t vn = 0, bpn = 0, d = 0;
       bool reset = false;
-      uint4 pa = make_uint4(0, 0, 0, 0), pb = pa;
+      uint4 pa[kGW / 4];
+#pragma unroll
+      for (int h = 0; h < kGW / 4; ++h) pa[h] = make_uint4(0, 0, 0, 0);
       if (gen) {
         item_at<MODE, NB>(a, t_lo + i + 2, vn, bpn);
         vn |= gslot;
         reset = EMIT && bpn != gs.bpcur;
         d = reset ? vn : (gs.vcur ^ vn);
         if (d) {
-          load_pl(__ffs(d) - 1, bpn, pa, pb);
+          load_pl(__ffs(d) - 1, bpn, pa);
           d &= d - 1;
         }
       }
@@ -535,10 +591,10 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         if (gen) {
           if (reset) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) gs.g[q] = 0;
+            for (int q = 0; q < kGW; ++q) gs.g[q] = 0;
             gs.bpcur = bpn;
           }
-          xor_plane(gs.g, pa, pb);
+          xor_plane(gs.g, pa);
           if (d) xor_all(d, bpn);  // rare: more than one changed bit
           gs.vcur = vn;
         }
@@ -562,7 +618,10 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         tc::fence_before();
         mbar_arrive(&bar_tmem_empty);
         gen_update();
-        gen_store();
+        // R = 16: the 16-row generation needs 64 output registers, so B(i+2)
+        // is stored after this item's stages (R dead); MMA(i+2) still only
+        // waits for item i+1's TMEM read
+        if constexpr (!kLateB) gen_store();
       } else {
         // TMEM -> registers: two pairs of 64-column loads, two waits; TMEM is
         // released before any of the stages run.  R[j] holds c = 2j, 2j+1.
@@ -656,6 +715,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
                   make_uint4(R[64 * h + 4 * q], R[64 * h + 4 * q + 1], R[64 * h + 4 * q + 2],
                              R[64 * h + 4 * q + 3]);
           emit_done(i);
+          if constexpr (kLateB) gen_store();
           continue;
         }
         // top stage (c bit NB-9 = register bit NB-10) fused with the max/min
@@ -669,7 +729,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
 #pragma unroll
         for (int sl = 0; sl < kSlots; ++sl) {
           uint32_t mx = 0u, mn = 0xFFFFFFFFu;
-          if constexpr (NB >= 12) {
+          if constexpr (NB >= 9 + kLogRows) {  // an ALU top stage is left
 #pragma unroll
             for (int kk = 0; kk < kPerSlot / 2; ++kk) {
               const int k = sl * kPerSlot + (kk & ((1 << kTop) - 1)) + ((kk >> kTop) << (kTop + 1));
@@ -708,6 +768,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
           }
         }
       }
+      if constexpr (kLateB) gen_store();
     }
     tc::fence_before();
     mbar_arrive(&bar_done);
@@ -845,6 +906,8 @@ int launch_tc16_nl(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t
   return run_tc_hybrid<kTcNL>(a, int64_t(v_hi) - v_lo, st);
 }
 
+int tc_min_small_n() { return 8 + kLogRows; }
+
 int launch_tc_nl_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
                        unsigned long long* key, cudaStream_t st) {
   TcArgs a{};
@@ -857,7 +920,9 @@ int launch_tc_nl_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t v_
   const int lc = 16 - n;
   const int64_t items = ((int64_t(v_hi) - 1) >> lc) + 1 - (int64_t(v_lo) >> lc);
   switch (n) {
-    case 11: return run_tc_hybrid<kTcNL, 11>(a, items, st);
+    case 11:
+      if constexpr (kLogRows <= 3) return run_tc_hybrid<kTcNL, 11>(a, items, st);
+      return set_error(SBW_EINVAL, "16-row generation needs n >= 12");
     case 12: return run_tc_hybrid<kTcNL, 12>(a, items, st);
     case 13: return run_tc_hybrid<kTcNL, 13>(a, items, st);
     case 14: return run_tc_hybrid<kTcNL, 14>(a, items, st);

@@ -139,7 +139,7 @@ int launch_fused_onchip(const void* table, int tbytes, int n, int m, uint32_t v_
   }
   uint32_t* planes = static_cast<uint32_t*>(scratch);
   if (int rc = build_planes(table, tbytes, n, m, planes, st)) return rc;
-  if (n >= 11 && n <= 15 && out == nullptr && m >= 16 - n && tc_path_enabled())
+  if (n >= tc_min_small_n() && n <= 15 && out == nullptr && m >= 16 - n && tc_path_enabled())
     return launch_tc_nl_small(planes, n, v_lo, v_hi, max_abs, key, st);
   if (n == 16 && tc_path_enabled())
     return out == nullptr ? launch_tc16_nl(planes, v_lo, v_hi, max_abs, key, st)

@@ -132,8 +132,10 @@ def test_multipass_tensor_core_pass_a(n, m, seed, lo, hi):
                                        (13, 3, 1, 8), (13, 16, 1000, 1901), (12, 4, 1, 16), (12, 12, 1, 4096),
                                        (11, 5, 1, 32), (11, 11, 17, 2000), (11, 20, 123456, 124000)])
 def test_small_n_tensor_core_slots(n, m, lo, hi):
-    """n = 11..15 NL packs 2^(16-n) components per tile (slots); ranges that
-    start / end inside an item, the item holding v = 0, m = 16 - n exactly."""
+    """n = 12..15 NL packs 2^(16-n) components per tile (slots); ranges that
+    start / end inside an item, the item holding v = 0, m = 16 - n exactly.
+    (n = 11 runs on the tile kernel in the default 16-row-generation build and
+    on the tensor cores in an SBW_TC_ROWS=8 build; same expectations.)"""
     s = sw.generate_sbox(n, m, 40 + n, bijective=(n == m))
     got, (nl, v, mxw) = _maxima(s, lo, hi)
     want = orc.component_max_abs(s.table, n, lo, hi)
