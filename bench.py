@@ -453,7 +453,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:  # the CPU baseline is reported at N = 1 only
         line["cpu_baseline"] = cpu_baseline(args.config, target_s=args.cpu_seconds)
     print(json.dumps(line), flush=True)
     if dist is not None:
