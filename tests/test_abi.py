@@ -56,6 +56,13 @@ def test_abi_version_and_argument_validation():
         d.check(lib.sbw_nl(None, 2, 8, 8, 1, 2, None, None, None, 0, None))
     rc = lib.sbw_fwht_inplace(None, 31, 1, None, None)
     assert rc == d.SBW_EINVAL
+    # peer-memory exchange entry points validate before touching a device
+    ptr = ctypes.c_void_p()
+    assert lib.sbw_ipc_alloc(0, ctypes.byref(ptr), ctypes.create_string_buffer(64)) == d.SBW_EINVAL
+    assert lib.sbw_ipc_open(None, ctypes.byref(ptr)) == d.SBW_EINVAL
+    assert lib.sbw_key_merge(None, None, None) == d.SBW_EINVAL
+    assert lib.sbw_peer_copy(None, None, 8, None) == d.SBW_EINVAL
+    assert lib.sbw_peer_copy(None, None, 0, None) == d.SBW_OK
     with pytest.raises(ValueError, match="brute force capped"):
         buf = ctypes.create_string_buffer(64)
         d.check(lib.sbw_nl_bruteforce(ctypes.addressof(buf) + 16 - ctypes.addressof(buf) % 16,
