@@ -15,52 +15,88 @@ namespace sbw {
 // passes of up to 6 bits: element e = hi*2^(b0+NB) + i*2^b0 + lo.
 // ---------------------------------------------------------------------------
 template <int NB>
+__device__ __forceinline__ int inplace_task(int32_t* __restrict__ d, int k, int b0, int64_t t, int64_t per_col,
+                                            int64_t& col) {
+  constexpr int L = 1 << NB;
+  const int64_t lo_mask = (int64_t(1) << b0) - 1;
+  col = t / per_col;
+  const int64_t r = t - col * per_col;
+  const int64_t lo = r & lo_mask, hi = r >> b0;
+  int32_t* p = d + (col << k) + (hi << (b0 + NB)) + lo;
+  int e[L];
+#pragma unroll
+  for (int i = 0; i < L; ++i) e[i] = p[int64_t(i) << b0];
+  // wrap-around adds: do the arithmetic in uint32 (well-defined overflow)
+#pragma unroll
+  for (int s = 1; s < L; s <<= 1) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      if ((i & s) == 0) {
+        const uint32_t a = uint32_t(e[i]), b = uint32_t(e[i + s]);
+        e[i] = int(a + b);
+        e[i + s] = int(a - b);
+      }
+    }
+  }
+  int mx = INT_MIN;
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    p[int64_t(i) << b0] = e[i];
+    mx = max(mx, wrap_abs(e[i]));
+  }
+  return mx;
+}
+
+template <int NB>
 __global__ void __launch_bounds__(256) k_inplace_pass(int32_t* __restrict__ d, int k, int b0,
                                                       int64_t count, long long* max_abs) {
-  constexpr int L = 1 << NB;
   const int64_t per_col = int64_t(1) << (k - NB);
   const int64_t total = count * per_col;
-  const int64_t lo_mask = (int64_t(1) << b0) - 1;
+  const int lane = threadIdx.x & 31;
+  if (max_abs && (per_col & 31) == 0) {
+    // Last pass of long columns: every warp's 32 consecutive tasks share one
+    // column, so each CTA takes one contiguous task range and every thread
+    // keeps a running max, flushed (warp max + one atomic) only when its
+    // warp moves to the next column -- a handful of atomics per CTA instead
+    // of one per warp-task on a few hot addresses.
+    const int64_t per_cta = ((total + gridDim.x - 1) / gridDim.x + 31) & ~int64_t(31);
+    const int64_t t0 = blockIdx.x * per_cta, t1 = min(t0 + per_cta, total);
+    int64_t cur = -1;
+    int run = INT_MIN;
+    for (int64_t wb = t0 + (threadIdx.x & ~31u); wb < t1; wb += blockDim.x) {
+      int64_t col;
+      const int mx = inplace_task<NB>(d, k, b0, wb + lane, per_col, col);  // warp-uniform col
+      if (col != cur) {
+        if (cur >= 0) {
+          const int wm = __reduce_max_sync(0xffffffffu, unsigned(run) ^ 0x80000000u) ^ 0x80000000u;
+          if (lane == 0) atomicMax(max_abs + cur, (long long)wm);
+        }
+        cur = col;
+        run = INT_MIN;
+      }
+      run = max(run, mx);
+    }
+    if (cur >= 0) {
+      const int wm = __reduce_max_sync(0xffffffffu, unsigned(run) ^ 0x80000000u) ^ 0x80000000u;
+      if (lane == 0) atomicMax(max_abs + cur, (long long)wm);
+    }
+    return;
+  }
   // warp-uniform loop control so the warp-level reduction below is safe
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t wb = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); wb < total;
        wb += stride) {
-    const int64_t t = wb + (threadIdx.x & 31);
+    const int64_t t = wb + lane;
     const bool ok = t < total;
-    const int64_t col = ok ? t / per_col : 0;
-    int mx = INT_MIN;
-    if (ok) {
-      const int64_t r = t - col * per_col;
-      const int64_t lo = r & lo_mask, hi = r >> b0;
-      int32_t* p = d + (col << k) + (hi << (b0 + NB)) + lo;
-      int e[L];
-#pragma unroll
-      for (int i = 0; i < L; ++i) e[i] = p[int64_t(i) << b0];
-      // wrap-around adds: do the arithmetic in uint32 (well-defined overflow)
-#pragma unroll
-      for (int s = 1; s < L; s <<= 1) {
-#pragma unroll
-        for (int i = 0; i < L; ++i) {
-          if ((i & s) == 0) {
-            const uint32_t a = uint32_t(e[i]), b = uint32_t(e[i + s]);
-            e[i] = int(a + b);
-            e[i + s] = int(a - b);
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < L; ++i) {
-        p[int64_t(i) << b0] = e[i];
-        mx = max(mx, wrap_abs(e[i]));
-      }
-    }
+    int64_t col = 0;
+    const int mx = ok ? inplace_task<NB>(d, k, b0, t, per_col, col) : INT_MIN;
     if (max_abs) {
       const unsigned m = __ballot_sync(0xffffffffu, ok);
       if (ok) {
         const long long col0 = __shfl_sync(m, col, __ffs(m) - 1);
         if (__all_sync(m, col == col0)) {
           const int wm = __reduce_max_sync(m, unsigned(mx) ^ 0x80000000u) ^ 0x80000000u;
-          if ((threadIdx.x & 31) == __ffs(m) - 1) atomicMax(max_abs + col, (long long)wm);
+          if (lane == __ffs(m) - 1) atomicMax(max_abs + col, (long long)wm);
         } else {
           atomicMax(max_abs + col, (long long)mx);
         }
