@@ -457,7 +457,30 @@ __global__ void __launch_bounds__(256) k_row_maxabs(const int32_t* __restrict__ 
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     const int32_t* p = rows + r * ld;
     int hi = INT_MIN, lo = INT_MAX;
-    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+    int64_t c0 = 0;
+    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+      // 16-byte loads, four in flight per thread (the scan is HBM-bound)
+      const int4* q = reinterpret_cast<const int4*>(p);
+      const int64_t n4 = cols >> 2;
+      int64_t i = threadIdx.x;
+      for (; i + 3 * blockDim.x < n4; i += 4 * blockDim.x) {
+        int4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldcs(q + i + u * blockDim.x);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          hi = max(hi, max(max(v[u].x, v[u].y), max(v[u].z, v[u].w)));
+          lo = min(lo, min(min(v[u].x, v[u].y), min(v[u].z, v[u].w)));
+        }
+      }
+      for (; i < n4; i += blockDim.x) {
+        const int4 v = __ldcs(q + i);
+        hi = max(hi, max(max(v.x, v.y), max(v.z, v.w)));
+        lo = min(lo, min(min(v.x, v.y), min(v.z, v.w)));
+      }
+      c0 = n4 << 2;
+    }
+    for (int64_t c = c0 + threadIdx.x; c < cols; c += blockDim.x) {
       const int x = p[c];
       hi = max(hi, x);
       lo = min(lo, x);
