@@ -37,8 +37,11 @@ int launch_tc16_spec(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32
 // works for NL; SPEC keeps launch_emit_tiles).
 // Components are taken in the Gray order mask_at(position, run_lo, run_hi)
 // of the whole run [run_lo, run_hi) (pass B publishes with the same map).
+// emit16 = 1: 16 stages, wrapped u16 out (an affine tile raises *flag);
+// gate: run only if (*gate != 0) == gate_on (null: always).
 int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_comp, uint32_t* emit,
-                   uint32_t run_lo, uint32_t run_hi, cudaStream_t st);
+                   uint32_t run_lo, uint32_t run_hi, cudaStream_t st, int emit16 = 0, int* flag = nullptr,
+                   const int* gate = nullptr, int gate_on = 0);
 
 // The same pass A streaming into the L2 ring of a concurrently running
 // k_passb_tc (RingArgs in sbw_internal.cuh); grid = ring.na CTAs.

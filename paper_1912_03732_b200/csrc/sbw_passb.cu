@@ -109,6 +109,7 @@ int64_t batch_components(int n, int64_t total) {
 struct K3Streams {
   cudaStream_t a = nullptr, b = nullptr;
   cudaEvent_t fork = nullptr, done_a[2] = {nullptr, nullptr}, done_b[2] = {nullptr, nullptr};
+  int* flags = nullptr;  // [2]: per scratch buffer, "a tile of this batch wrapped at stage 16"
 };
 K3Streams g_k3[64];
 std::mutex g_k3_mu;
@@ -125,6 +126,7 @@ int k3_streams(int dev, K3Streams** out) {
       SBW_CUDA_CHECK(cudaEventCreateWithFlags(&s.done_a[i], cudaEventDisableTiming));
       SBW_CUDA_CHECK(cudaEventCreateWithFlags(&s.done_b[i], cudaEventDisableTiming));
     }
+    SBW_CUDA_CHECK(cudaMalloc(&s.flags, 2 * sizeof(int)));
   }
   *out = &s;
   return SBW_OK;
@@ -209,6 +211,16 @@ int launch_k3_batched(const uint32_t* planes, int n, int m, uint32_t v_lo, uint3
   };
   // NL with the tensor-core pass A: Gray-ordered components (PassBArgs::gray)
   const bool gray = out == nullptr && tc_path_enabled();
+  // 16 stages in pass A (n >= 18; pass B k_passb_regs for n <= 20, k_passb_tc
+  // above): pass B does one stage less.  A batch in which some tile wrapped
+  // at stage 16 (|W_16| = 2^16: the component is affine on that tile) is
+  // redone by gated 15-stage launches; the gates read a device flag, so no
+  // host synchronisation is needed.  Off by default (SBW_K3_EMIT16=1 enables
+  // it): bit-identical, but measured no faster -- 20x20 928 vs 927 ms, 24x16
+  // 978 vs 956 ms, 18x18 67 vs 57 ms -- the extra stage and wrap check cost
+  // pass A what pass B saves, plus two gated launches per batch.
+  const bool tc_b = n >= kPassBTcMinN && passb_tc_enabled();
+  const bool e16 = gray && n >= 18 && (tc_b || n <= 20) && env_int("SBW_K3_EMIT16", 0) != 0;
   // SBW_K3_SERIAL=1: pass A of batch b+1 waits for pass B of batch b (no
   // overlap between the HBM-bound passes)
   const bool serial = env_int("SBW_K3_SERIAL", 0) != 0;
@@ -220,7 +232,9 @@ int launch_k3_batched(const uint32_t* planes, int n, int m, uint32_t v_lo, uint3
     if (nb >= 2) SBW_CUDA_CHECK(cudaStreamWaitEvent(ks->a, ks->done_b[buf], 0));  // buffer free
     if (serial && nb >= 1) SBW_CUDA_CHECK(cudaStreamWaitEvent(ks->a, ks->done_b[buf ^ 1], 0));
     mark(ks->a);
-    if (int rc = gray ? launch_tc_emit(planes, n, vf, nc, emit[buf], v_lo, v_hi, ks->a)
+    int* flag = ks->flags + buf;
+    if (e16) SBW_CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int), ks->a));
+    if (int rc = gray ? launch_tc_emit(planes, n, vf, nc, emit[buf], v_lo, v_hi, ks->a, e16 ? 1 : 0, flag)
                      : launch_emit_tiles(planes, n, m, vf, nc, emit[buf], ks->a))
       return rc;
     mark(ks->a);
@@ -240,10 +254,22 @@ int launch_k3_batched(const uint32_t* planes, int n, int m, uint32_t v_lo, uint3
     a.gray = gray ? 1 : 0;
     a.run_lo = v_lo;
     a.run_hi = v_hi;
-    const int rc = out ? dispatch_passb_regs<MODE_SPEC>(n - 15, a, ks->b)
-                       : (n >= kPassBTcMinN && passb_tc_enabled()) ? launch_passb_tc(a, ks->b)
-                                                         : dispatch_passb_regs<MODE_NL>(n - 15, a, ks->b);
-    if (rc) return rc;
+    auto run_b = [&](const PassBArgs& x) {
+      return out ? dispatch_passb_regs<MODE_SPEC>(n - 15, x, ks->b)
+                 : tc_b ? launch_passb_tc(x, ks->b) : dispatch_passb_regs<MODE_NL>(n - 15 - x.e16, x, ks->b);
+    };
+    if (e16) {
+      PassBArgs a16 = a;  // the 16-stage batch, unless a tile wrapped
+      a16.e16 = 1;
+      a16.gate = flag;
+      a16.gate_on = 0;
+      if (int rc = run_b(a16)) return rc;
+      // fallback, only if a tile wrapped: the same batch with 15 stages
+      if (int rc = launch_tc_emit(planes, n, vf, nc, emit[buf], v_lo, v_hi, ks->b, 0, nullptr, flag, 1)) return rc;
+      a.gate = flag;
+      a.gate_on = 1;
+    }
+    if (int rc = run_b(a)) return rc;
     mark(ks->b);
     SBW_CUDA_CHECK(cudaEventRecord(ks->done_b[buf], ks->b));
   }

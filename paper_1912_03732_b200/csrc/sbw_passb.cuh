@@ -38,7 +38,18 @@ struct PassBArgs {
   // component); max_abs is indexed by mask - run_lo.
   int gray;
   uint32_t run_lo, run_hi;
+  // e16 = 1: the scratch holds pass A's 16-stage output (rows = x bits
+  // 16..n-1 of 2^16 biased u16 s = W_16 / 2 + 2^15, k_passb_regs /
+  // k_passb_tc only); 0: 15-stage (rows = x bits 15..n-1, 2^15 u16, bias 2^14)
+  int e16;
+  // run only if (*gate != 0) == gate_on (gate may be null)
+  const int* gate;
+  int gate_on;
 };
+
+__device__ __forceinline__ bool passb_gated_off(const PassBArgs& a) {
+  return a.gate && ((*a.gate != 0) != (a.gate_on != 0));
+}
 
 // Publish a component's max: natural order (mask v_first + comp, row
 // out_row0 + comp) or the Gray order of the tensor-core pass A.
@@ -53,13 +64,14 @@ __device__ __forceinline__ void publish_comp(const PassBArgs& a, int64_t comp, i
 // the bias: with A = 2^23 + s_a, B = 2^23 + s_b, h_a - h_b = A - B and
 // h_a + h_b = (A - (2^24 + 2^15)) + B, every partial an integer below 2^24 --
 // three FADDs per lane pair.  Rows ua (even) / ub (odd) -> e[0..3].
-__device__ __forceinline__ void load_rows_stage1(uint32_t ua, uint32_t ub, float* e) {
+// (e16: s = h + 2^15, so the pair's bias is 2^24 + 2^16.)
+__device__ __forceinline__ void load_rows_stage1(uint32_t ua, uint32_t ub, float* e, float bias2 = 16809984.0f) {
   const float al = __int_as_float(int(__byte_perm(ua, 0x4B000000u, 0x7610)));
   const float ah = __int_as_float(int(__byte_perm(ua, 0x4B000000u, 0x7632)));
   const float bl = __int_as_float(int(__byte_perm(ub, 0x4B000000u, 0x7610)));
   const float bh = __int_as_float(int(__byte_perm(ub, 0x4B000000u, 0x7632)));
-  e[0] = __fadd_rn(__fsub_rn(al, 16809984.0f), bl);
-  e[1] = __fadd_rn(__fsub_rn(ah, 16809984.0f), bh);
+  e[0] = __fadd_rn(__fsub_rn(al, bias2), bl);
+  e[1] = __fadd_rn(__fsub_rn(ah, bias2), bh);
   e[2] = __fsub_rn(al, bl);
   e[3] = __fsub_rn(ah, bh);
 }
@@ -217,7 +229,10 @@ constexpr int kPassBThreads = 256;
 template <int H, int MODE>
 __global__ void __launch_bounds__(kPassBThreads) k_passb_regs(PassBArgs a) {
   constexpr int NI = 1 << H;
-  constexpr int64_t chunks = (int64_t(1) << 14) / kPassBThreads;  // per component
+  if (passb_gated_off(a)) return;
+  const int row_log = 14 + a.e16;                                   // u32 words per row
+  const int64_t chunks = (int64_t(1) << row_log) / kPassBThreads;  // per component
+  const float bias2 = a.e16 ? 16842752.0f : 16809984.0f;           // 2^24 + 2^16 / 2^24 + 2^15
   const int64_t items = a.n_comp * chunks;
   const int64_t per_cta = (items + gridDim.x - 1) / gridDim.x;
   const int64_t b0 = blockIdx.x * per_cta;
@@ -229,10 +244,10 @@ __global__ void __launch_bounds__(kPassBThreads) k_passb_regs(PassBArgs a) {
     const uint32_t* src = a.scratch + (comp << (a.n - 1)) + col;
     uint32_t u[NI];
 #pragma unroll
-    for (int i = 0; i < NI; ++i) u[i] = __ldcs(src + (int64_t(i) << 14));
+    for (int i = 0; i < NI; ++i) u[i] = __ldcs(src + (int64_t(i) << row_log));
     float e[2 * NI];
 #pragma unroll
-    for (int i = 0; i < NI; i += 2) load_rows_stage1(u[i], u[i + 1], e + 2 * i);
+    for (int i = 0; i < NI; i += 2) load_rows_stage1(u[i], u[i + 1], e + 2 * i, bias2);
     fwht_regs_f<2 * NI, 4, NI>(e);
     if constexpr (MODE == MODE_NL) {
       float mf = 0.f;
@@ -265,6 +280,7 @@ __global__ void __launch_bounds__(kPassBThreads) k_passb_regs(PassBArgs a) {
 template <int H, int MODE>
 __global__ void __launch_bounds__(kStagedThreads, 2) k_passb_staged(PassBArgs a) {
   using S = StagedShape<H>;
+  if (passb_gated_off(a)) return;  // (15-stage layout only: e16 is never set here)
   extern __shared__ uint4 smem4[];  // [32 KiB staging][64 KiB fp32-pair tile]
   uint32_t* stg = reinterpret_cast<uint32_t*>(smem4);
   float2* tile = reinterpret_cast<float2*>(stg + S::WORDS);

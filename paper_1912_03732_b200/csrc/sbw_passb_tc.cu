@@ -115,6 +115,10 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constan
   __shared__ uint64_t full[S::STAGES], empty[S::STAGES], tfull[S::TBUF], tempty[S::TBUF];
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (passb_gated_off(a)) return;  // CTA-uniform, before any setup
+  // e16: rows are twice as wide (2^16 u16), so a component has twice the items
+  const int64_t per_comp = S::PER_COMP << a.e16;
+  const int lpc = S::LPC + a.e16;
   const bool ring = a.ring.on != 0;
   int64_t b0 = 0, n_pb = 1, ib_off = 0, I = 0;
   int n_my = 0;
@@ -124,7 +128,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constan
     n_pb = I * (blockIdx.x + 1) / gridDim.x - ib_off;
     n_my = n_pb > 0 ? int(a.ring.batches * n_pb) : 0;
   } else {
-    const int64_t items = a.n_comp * S::PER_COMP;
+    const int64_t items = a.n_comp * per_comp;
     const int64_t per_cta = (items + gridDim.x - 1) / gridDim.x;
     b0 = blockIdx.x * per_cta;
     const int64_t b1 = b0 + per_cta < items ? b0 + per_cta : items;
@@ -174,8 +178,8 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constan
         const int s = i % S::STAGES;
         if (i >= S::STAGES) tc::mbar_wait(&empty[s], uint32_t((i / S::STAGES - 1) & 1));
         const int64_t b = item_b(i);
-        int comp = int(b >> S::LPC);
-        const int q = int(b & (S::PER_COMP - 1));
+        int comp = int(b >> lpc);
+        const int q = int(b & (per_comp - 1));
         if (ring) {
           // batch k sits in slot k mod R; its first item waits for every
           // pass-A warp's arrival, then orders the TMA reads after the acquire
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constan
     const int rr = quarter * 32 + lane;  // output row r' = TMEM lane
     // row u = 0 of every 2^h block carries 2^14 * 2^h from the bias of s
     // (twice that after the first ALU stage when G >= 2)
-    const int corr = rr < S::P ? -(S::G == 1 ? (1 << (14 + S::h)) : (1 << 22)) : 0;
+    const int corr = rr < S::P ? -(S::G == 1 ? (1 << (14 + a.e16 + S::h)) : (1 << (22 + a.e16))) : 0;
     const uint32_t t_lane = uint32_t(quarter * 32) << 16;
     int run = 0;
     for (int i = 0; i < n_my; ++i) {
@@ -298,8 +302,8 @@ __global__ void __launch_bounds__(kPbThreads, 1) k_passb_tc(const __grid_constan
         }
       }
       run = max(run, 2 * m);  // values are W / 2
-      const int64_t comp = item_b(i) >> S::LPC;
-      if (i + 1 >= n_my || (item_b(i + 1) >> S::LPC) != comp) {
+      const int64_t comp = item_b(i) >> lpc;
+      if (i + 1 >= n_my || (item_b(i + 1) >> lpc) != comp) {
         if (ring) {  // batch k, slot component cb -> its ring position's mask
           const int64_t k = comp / a.ring.bc;
           const uint32_t v = ring_mask(a.ring, a.v_first, ring_pos(a.ring, k, comp - k * a.ring.bc));
@@ -340,9 +344,9 @@ int run_passb_tc(const PassBArgs& a, cudaStream_t st) {
   auto enc = encode_fn();
   if (!enc) return set_error(SBW_ECUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap map;
-  // [rows][1024 chunks][64 B]: box {64 B, P chunks, BOX_ROWS rows}
-  const cuuint64_t dims[3] = {64, 1024, cuuint64_t(a.n_comp) << H};
-  const cuuint64_t strides[2] = {64, cuuint64_t(1) << 16};
+  // [rows][1024 (e16: 2048) chunks][64 B]: box {64 B, P chunks, BOX_ROWS rows}
+  const cuuint64_t dims[3] = {64, cuuint64_t(1024) << a.e16, cuuint64_t(a.n_comp) << H};
+  const cuuint64_t strides[2] = {64, cuuint64_t(1) << (16 + a.e16)};
   const cuuint32_t box[3] = {64, cuuint32_t(S::P), cuuint32_t(S::BOX_ROWS)};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint32_t*>(a.scratch), dims, strides, box,
@@ -354,7 +358,7 @@ int run_passb_tc(const PassBArgs& a, cudaStream_t st) {
     SBW_CUDA_CHECK(cudaFuncSetAttribute(k_passb_tc<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPbSmem)));
     attr_done |= 1ull << (dp.device & 63);
   }
-  const int64_t items = a.n_comp * S::PER_COMP;
+  const int64_t items = a.n_comp * (S::PER_COMP << a.e16);
   const int grid = a.ring.on ? int(a.ring.nb) : int(items < dp.sm_count ? items : dp.sm_count);
   k_passb_tc<H><<<grid, kPbThreads, kPbSmem, st>>>(map, a);
   SBW_LAUNCH_CHECK("k_passb_tc");
@@ -372,7 +376,7 @@ bool passb_tc_enabled() {
 }
 
 int launch_passb_tc(const PassBArgs& a, cudaStream_t st) {
-  switch (a.n - 15) {
+  switch (a.n - 15 - a.e16) {
     case 2: return run_passb_tc<2>(a, st);
     case 3: return run_passb_tc<3>(a, st);
     case 4: return run_passb_tc<4>(a, st);

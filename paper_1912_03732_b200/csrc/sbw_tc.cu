@@ -309,6 +309,15 @@ struct TcArgs {
   int64_t ld;
   // EMIT into the L2 ring shared with a concurrent pass B (sbw_internal.cuh)
   RingArgs ring;
+  // EMIT: emit16 = 1 runs the 16th stage (x bit 15) too and writes the
+  // wrapped u16 s = W_16 / 2 + 2^15 (h = 0: u bit 15 = 0, h = 1: = 1); a lane
+  // that wraps (|W_16| = 2^16, an affine tile) raises *flag, and the host's
+  // gated launches redo the batch with the 15-stage form (sbw_passb.cu).
+  int emit16;
+  int* flag;
+  // run only if (*gate != 0) == gate_on (gate may be null)
+  const int* gate;
+  int gate_on;
 };
 
 constexpr int kTcNL = 0, kTcEmit = 1, kTcSpec = 2;
@@ -397,6 +406,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(16) uint32_t s_wmax[4][kSlots][kMathWarps];  // per-warp max|W| [item & 3][slot]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (EMIT && a.gate && ((*a.gate != 0) != (a.gate_on != 0))) return;  // CTA-uniform, before any setup
   const int64_t total = items_total<MODE, NB>(a);
   const bool ring = EMIT && a.ring.on;
   const int64_t t_lo = ring ? 0 : total * blockIdx.x / gridDim.x;
@@ -707,6 +717,19 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
             R[64] += 0x4000u;
           }
           uint32_t* dst = emit_dst(i);
+          if (a.emit16) {
+            // stage 16 (register bit 6): S = x + y -> h = 0, D = x - y + 2^15 -> h = 1,
+            // lanes = W_16 / 2 + 2^15 mod 2^16; a lane at 0 is W_16 = +-2^16
+            uint32_t mn = 0xFFFFFFFFu;
+#pragma unroll
+            for (int k = 0; k < 64; ++k) {
+              const uint32_t x = R[k], y = R[k + 64];
+              R[k] = x + y;
+              R[k + 64] = x - y + 0x80008000u;
+              mn = __vimin3_u16x2(mn, R[k], R[k + 64]);
+            }
+            if (__any_sync(0xFFFFFFFFu, (mn & 0xFFFFu) == 0u || (mn >> 16) == 0u) && lane == 0) atomicOr(a.flag, 1);
+          }
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -946,10 +969,15 @@ int launch_tc16_spec(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32
 }
 
 int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_comp, uint32_t* emit,
-                   uint32_t run_lo, uint32_t run_hi, cudaStream_t st) {
+                   uint32_t run_lo, uint32_t run_hi, cudaStream_t st, int emit16, int* flag, const int* gate,
+                   int gate_on) {
   TcArgs a{};
   a.run_lo = run_lo;
   a.run_hi = run_hi;
+  a.emit16 = emit16;
+  a.flag = flag;
+  a.gate = gate;
+  a.gate_on = gate_on;
   a.planes = planes;
   a.plane_words = (int64_t(1) << n) >> 5;
   a.v_first = v_first;

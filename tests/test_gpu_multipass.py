@@ -86,3 +86,30 @@ def test_ring_matches_batched(monkeypatch, n, m, bij, lo, hi, na, L, R):
     rng = np.random.default_rng(n)
     for v in sorted(set(rng.integers(lo, hi, size=3).tolist()) | {lo, hi - 1}):
         assert int(got[v - lo]) == int(orc.component_max_abs(s.table, n, v, v + 1)[0]), v
+
+
+# ---- 16 stages in pass A (SBW_K3_EMIT16=1, off by default) --------------------
+# Pass A also runs stage 16 and writes the wrapped u16; a batch in which a tile
+# wrapped (|W_16| = 2^16: affine on the tile) is redone by gated 15-stage
+# launches.  Linear components wrap in every tile (all fallback); random ones
+# never do (all 16-stage); both must match the default path and the oracle.
+@pytest.mark.parametrize("n,m,seed,lo,hi", [(18, 18, 21, 1, 3000), (20, 12, 22, 1, 4096),
+                                             (21, 16, 23, 100, 400), (24, 16, 24, 1, 9)])
+def test_emit16_random_matches_default(monkeypatch, n, m, seed, lo, hi):
+    s = sw.generate_sbox(n, m, seed, bijective=False)
+    monkeypatch.setenv("SBW_K3_EMIT16", "0")
+    want, wkey = sw.component_max_abs_device(s, lo, hi)
+    monkeypatch.setenv("SBW_K3_EMIT16", "1")
+    got, gkey = sw.component_max_abs_device(s, lo, hi)
+    assert np.array_equal(got.cpu().numpy(), want.cpu().numpy()) and int(gkey.item()) == int(wkey.item())
+    v = lo + (hi - lo) // 2
+    assert int(got[v - lo].item()) == int(orc.component_max_abs(s.table, n, v, v + 1)[0])
+
+
+@pytest.mark.parametrize("n", [18, 20, 21, 24])
+def test_emit16_linear_components_fall_back(monkeypatch, n):
+    monkeypatch.setenv("SBW_K3_EMIT16", "1")
+    s = _linear_sbox(n)
+    mx, key = sw.component_max_abs_device(s)
+    assert np.all(mx.cpu().numpy() == 1 << n)
+    assert sw.transforms.decode_key(key, n)[:2] == (0, 1)
