@@ -244,6 +244,17 @@ __device__ __forceinline__ void xor_plane(uint32_t (&g)[kGW], const uint4 (&p)[k
         make_uint4(o[e][0], o[e][1], o[e][2], o[e][3]);
 }
 
+// Pass-A scratch store (SBW_EMIT_CS=1: streaming st.global.cs, evict-first)
+#ifndef SBW_EMIT_CS
+#define SBW_EMIT_CS 1  // 24x16: 945 vs 956 ms (plain stores); 20x20 unchanged
+#endif
+__device__ __forceinline__ void emit_store(uint4* p, uint4 v) {
+  if (SBW_EMIT_CS)
+    __stcs(p, v);
+  else
+    *p = v;
+}
+
 __device__ __forceinline__ void publish(const uint32_t* wmax, uint32_t v, uint32_t v_lo,
                                         int32_t* max_abs, unsigned long long* key) {
   const uint4 a = *reinterpret_cast<const uint4*>(wmax);
@@ -309,18 +320,18 @@ struct TcArgs {
   int64_t ld;
   // EMIT into the L2 ring shared with a concurrent pass B (sbw_internal.cuh)
   RingArgs ring;
-  // EMIT: emit16 = 1 runs the 16th stage (x bit 15) too and writes the
+  // MODE kTcEmit16 runs the 16th stage (x bit 15) too and writes the
   // wrapped u16 s = W_16 / 2 + 2^15 (h = 0: u bit 15 = 0, h = 1: = 1); a lane
   // that wraps (|W_16| = 2^16, an affine tile) raises *flag, and the host's
   // gated launches redo the batch with the 15-stage form (sbw_passb.cu).
-  int emit16;
-  int* flag;
+  int* flag;  // kTcEmit16
   // run only if (*gate != 0) == gate_on (gate may be null)
   const int* gate;
   int gate_on;
 };
 
-constexpr int kTcNL = 0, kTcEmit = 1, kTcSpec = 2;
+constexpr int kTcNL = 0, kTcEmit = 1, kTcSpec = 2, kTcEmit16 = 3;  // kTcEmit16: EMIT + stage 16
+__host__ __device__ constexpr bool is_emit(int mode) { return mode == kTcEmit || mode == kTcEmit16; }
 
 // NL items for an n = NB <= 16 box: one 2^16 tile holds C = 2^(16 - NB)
 // components (slots); item t covers masks (base << log2 C) | slot, with base
@@ -329,13 +340,13 @@ constexpr int kTcNL = 0, kTcEmit = 1, kTcSpec = 2;
 template <int MODE, int NB>
 __device__ __forceinline__ int64_t items_total(const TcArgs& a) {
   constexpr int LC = 16 - NB;
-  if constexpr (MODE == kTcEmit) return a.n_items;
+  if constexpr (is_emit(MODE)) return a.n_items;
   return ((int64_t(a.v_hi) - 1) >> LC) + 1 - (int64_t(a.v_lo) >> LC);
 }
 // item t of the launch -> (mask v of slot 0, 2^16-block index bp)
 template <int MODE, int NB>
 __device__ __forceinline__ void item_at(const TcArgs& a, int64_t t, uint32_t& v, uint32_t& bp) {
-  if constexpr (MODE == kTcEmit) {
+  if constexpr (is_emit(MODE)) {
     if (a.ring.on) {  // CTA (r, bp): ring position r K L + t (slot r L + t mod L of batch t / L)
       bp = blockIdx.x & ((1u << a.ring.log_t) - 1u);
       v = ring_mask(a.ring, a.v_first, int64_t(blockIdx.x >> a.ring.log_t) * a.ring.batches * a.ring.L + t);
@@ -395,7 +406,7 @@ __device__ __forceinline__ void publish_item(const TcArgs& a, const uint32_t* wm
 
 template <int MODE, int NB = 16>
 __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
-  constexpr bool EMIT = MODE == kTcEmit;
+  constexpr bool EMIT = is_emit(MODE);
   static_assert(NB == 16 || (MODE == kTcNL && NB >= 8 + kLogRows && kRows >= 8), "n < 16: NL with 8/16-row groups");
   constexpr int kSlots = 1 << (16 - NB);  // components per 2^16 tile
   static_assert(MODE != kTcSpec || kC0Mma, "exact SPEC output needs the bias-block GEMM");
@@ -717,7 +728,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
             R[64] += 0x4000u;
           }
           uint32_t* dst = emit_dst(i);
-          if (a.emit16) {
+          if constexpr (MODE == kTcEmit16) {
             // stage 16 (register bit 6): S = x + y -> h = 0, D = x - y + 2^15 -> h = 1,
             // lanes = W_16 / 2 + 2^15 mod 2^16; a lane at 0 is W_16 = +-2^16
             uint32_t mn = 0xFFFFFFFFu;
@@ -734,9 +745,9 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
           for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int q = 0; q < 16; ++q)
-              *reinterpret_cast<uint4*>(dst + (h << 14) + q * 1024) =
-                  make_uint4(R[64 * h + 4 * q], R[64 * h + 4 * q + 1], R[64 * h + 4 * q + 2],
-                             R[64 * h + 4 * q + 3]);
+              emit_store(reinterpret_cast<uint4*>(dst + (h << 14) + q * 1024),
+                         make_uint4(R[64 * h + 4 * q], R[64 * h + 4 * q + 1], R[64 * h + 4 * q + 2],
+                                    R[64 * h + 4 * q + 3]));
           emit_done(i);
           if constexpr (kLateB) gen_store();
           continue;
@@ -912,7 +923,7 @@ int run_tc_hybrid(const TcArgs& a, int64_t items, cudaStream_t st, int grid_over
   if (int rc = tc_consts(dp.device, st, &args.consts)) return rc;
   const int grid = grid_override > 0 ? grid_override : int(items < dp.sm_count ? items : dp.sm_count);
   k_tc_hybrid<MODE, NB><<<grid, kAllThreads, kTcSmem, st>>>(args);
-  SBW_LAUNCH_CHECK(MODE == kTcEmit ? "k_tc_hybrid<emit>" : (MODE == kTcSpec ? "k_tc_hybrid<spec>" : "k_tc_hybrid<nl>"));
+  SBW_LAUNCH_CHECK(is_emit(MODE) ? "k_tc_hybrid<emit>" : (MODE == kTcSpec ? "k_tc_hybrid<spec>" : "k_tc_hybrid<nl>"));
   return SBW_OK;
 }
 }  // namespace
@@ -974,7 +985,7 @@ int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_co
   TcArgs a{};
   a.run_lo = run_lo;
   a.run_hi = run_hi;
-  a.emit16 = emit16;
+
   a.flag = flag;
   a.gate = gate;
   a.gate_on = gate_on;
@@ -985,7 +996,7 @@ int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_co
   a.n_items = n_comp << (n - 16);
   a.n_full = n;
   a.emit = emit;
-  return run_tc_hybrid<kTcEmit>(a, a.n_items, st);
+  return emit16 ? run_tc_hybrid<kTcEmit16>(a, a.n_items, st) : run_tc_hybrid<kTcEmit>(a, a.n_items, st);
 }
 
 int launch_tc_emit_ring(const uint32_t* planes, int n, uint32_t v_first, const RingArgs& ring, uint32_t* emit,
