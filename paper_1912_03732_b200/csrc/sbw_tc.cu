@@ -296,8 +296,16 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // the two transform warpgroups get 232 (3 warps per SM sub-partition:
 // 32 + 232 + 232 = 496 of the 512 registers per lane of a sub-partition;
 // an exact 512 fit hung setmaxnreg.inc on B200).
-constexpr int kIssuerRegs = 32;
-constexpr int kMathRegs = 232;
+#ifndef SBW_ISSUER_REGS
+#define SBW_ISSUER_REGS 32
+#endif
+#ifndef SBW_MATH_REGS
+#define SBW_MATH_REGS 232
+#endif
+constexpr int kIssuerRegs = SBW_ISSUER_REGS;
+constexpr int kMathRegs = SBW_MATH_REGS;
+static_assert(kIssuerRegs + 2 * kMathRegs <= 512 && kIssuerRegs % 8 == 0 && kMathRegs % 8 == 0,
+              "setmaxnreg split of a sub-partition's 512 registers per lane");
 constexpr int kAllThreads = 128 + kMathWarps * 32;  // warpgroup 0: issuer (+3 idle warps)
 
 struct TcArgs {
