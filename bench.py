@@ -204,6 +204,11 @@ def run_ours(args, rank, world, local_rank):
     import paper_1912_03732_b200 as sw
     from paper_1912_03732_b200 import device as d
 
+    # SBW_BENCH_BACKEND=gloo (plumbing check only): several ranks may share a
+    # GPU, which NCCL refuses; the timing of such a run means nothing.
+    backend = os.environ.get("SBW_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local_rank = local_rank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     lib = d.load_library()
@@ -211,7 +216,10 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if dist is not None:
