@@ -69,21 +69,22 @@ constexpr int kRows = SBW_TC_ROWS;
 #ifndef SBW_R16_LATE
 #define SBW_R16_LATE 0  // 1: R = 16 stores B(i+2) after the item's stages (measured 2 % slower)
 #endif
-constexpr bool kLateB = SBW_TC_ROWS == 16 && SBW_R16_LATE;
+constexpr bool kLateB = (SBW_TC_ROWS == 16 && SBW_R16_LATE) || SBW_TC_ROWS == 32;  // R = 32 cannot hold both
 #ifndef SBW_EMIT_NET
 #define SBW_EMIT_NET 0
 #endif
-static_assert(kRows == 1 || kRows == 2 || kRows == 8 || kRows == 16, "SBW_TC_ROWS must be 1, 2, 8 or 16");
-constexpr int kLogRows = kRows == 16 ? 4 : (kRows == 8 ? 3 : (kRows == 2 ? 1 : 0));
+static_assert(kRows == 1 || kRows == 2 || kRows == 8 || kRows == 16 || kRows == 32,
+              "SBW_TC_ROWS must be 1, 2, 8, 16 or 32");
+constexpr int kLogRows = kRows == 32 ? 5 : (kRows == 16 ? 4 : (kRows == 8 ? 3 : (kRows == 2 ? 1 : 0)));
 constexpr bool kC0Mma = kRows > 1;
 // bias per D entry: 128 R on every row, 128 R more on row u = 0, as columns of
 // 127 (plus a remainder) against B columns of kBiasB (2 for R = 16, so both
 // bias column sets fit one 32-wide K block)
 constexpr int kBiasT = 128 * kRows;
-constexpr int kBiasB = kRows == 16 ? 2 : 1;
+constexpr int kBiasB = kRows >= 16 ? kRows / 8 : 1;
 constexpr int kBiasCols = (kBiasT / kBiasB + 126) / 127;
 // generation state: plane words per transform thread (R = 16: word ks of 16 rows)
-constexpr int kGW = kRows == 16 ? 16 : 8;
+constexpr int kGW = kRows >= 16 ? kRows : 8;
 constexpr int kMathWarps = 8;
 constexpr int kKA = kC0Mma ? 288 : 256;        // K of A: 256 (r) [+ 32 bias block]
 constexpr int kAHalf = 128 * kKA;              // one M = 128 half of A
@@ -253,6 +254,39 @@ __device__ __forceinline__ void emit_store(uint4* p, uint4 v) {
     __stcs(p, v);
   else
     *p = v;
+}
+
+// R = 32 generation: thread (j, ks, kq) owns plane word ks of the 32 rows
+// 32 j .. 32 j + 31 and the bit positions k = 2 kq, 2 kq + 1: 8 bytes (half a
+// 16-byte SW128 chunk) of every row.  Biased 32-point WHT, outputs in [0, 32].
+[[maybe_unused]] __device__ __forceinline__ void store_rows32_sw128(const uint32_t* g, uint8_t* bbuf, int j,
+                                                                    int ks, int kq) {
+  uint8_t* base = bbuf + ((ks >> 2) * 32 + 4 * j) * 1024;
+  constexpr uint32_t M = 0x01010101u;
+  uint32_t o[32][2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int k = 2 * kq + q;
+    uint32_t b[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) b[e] = (g[e] >> k) & M;
+#pragma unroll
+    for (int t = 0; t < 5; ++t)
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if ((e & (1 << t)) == 0) {
+          const uint32_t x = b[e], y = b[e | (1 << t)];
+          b[e] = x + y;
+          b[e | (1 << t)] = x - y + (M << t);  // per byte in [0, 2^(t+1)]: no borrow
+        }
+#pragma unroll
+    for (int e = 0; e < 32; ++e) o[e][q] = b[e];
+  }
+  const int c = 2 * (ks & 3) + (kq >> 1);  // logical chunk; this thread's 8 bytes at half kq & 1
+#pragma unroll
+  for (int e = 0; e < 32; ++e)
+    *reinterpret_cast<uint2*>(base + (e >> 3) * 1024 + (e & 7) * 128 + ((c ^ (e & 7)) << 4) + 8 * (kq & 1)) =
+        make_uint2(o[e][0], o[e][1]);
 }
 
 __device__ __forceinline__ void publish(const uint32_t* wmax, uint32_t v, uint32_t v_lo,
@@ -480,11 +514,11 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kMathRegs));
     const int mt = tid - 128, mw = mt >> 5;  // transform thread / warp index
     const int c = mt;                        // generation row (plain B rows)
-    const int gj = kRows == 16 ? mt >> 4 : (kRows == 8 ? mt >> 3 : mt >> 1);  // C0MMA: row group
+    const int gj = kRows == 32 ? mt >> 5 : (kRows == 16 ? mt >> 4 : (kRows == 8 ? mt >> 3 : mt >> 1));  // C0MMA: row group
     // C0MMA: plane word (R = 8, 16) / K half (R = 2); R = 16 also splits the
     // bit positions of the bytes: gkq = k half
-    const int gkh = kRows == 16 ? (mt >> 1) & 7 : (kRows == 8 ? mt & 7 : mt & 1);
-    const int gkq = mt & 1;
+    const int gkh = kRows == 32 ? (mt >> 2) & 7 : (kRows == 16 ? (mt >> 1) & 7 : (kRows == 8 ? mt & 7 : mt & 1));
+    const int gkq = kRows == 32 ? mt & 3 : mt & 1;
     const uint32_t* __restrict__ planes = a.planes;
     const int64_t pw = EMIT ? a.plane_words : (int64_t(1) << NB) >> 5;
     // NB < 16: this thread's 8 rows belong to slot gslot; its rows within the
@@ -527,21 +561,24 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     // full recompute (first items): the planes of all set bits of d, 8 at a
     // time with every load in flight, instead of one serialized load per bit
     auto xor_full = [&](uint32_t d, uint32_t bp) {
+      constexpr int kXB = kGW >= 32 ? 2 : 8;  // planes per batch (R = 32: 32 words each)
 #pragma unroll 1
-      for (int i0 = 0; i0 < 32 && (d >> i0); i0 += 8) {
-        uint4 x[8][kGW / 4];
+      for (int i0 = 0; i0 < 32 && (d >> i0); i0 += kXB) {
+        uint4 x[kXB][kGW / 4];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < kXB; ++q) {
 #pragma unroll
           for (int h = 0; h < kGW / 4; ++h) x[q][h] = make_uint4(0, 0, 0, 0);
           if ((d >> (i0 + q)) & 1u) load_pl(i0 + q, bp, x[q]);
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) xor_plane(gs.g, x[q]);
+        for (int q = 0; q < kXB; ++q) xor_plane(gs.g, x[q]);
       }
     };
     auto store_b = [&](int buf) {
-      if constexpr (kRows == 16)
+      if constexpr (kRows == 32)
+        store_rows32_sw128(gs.g, smem + kBOff + buf * kBBytes, gj, gkh, gkq);
+      else if constexpr (kRows == 16)
         store_rows16_sw128(gs.g, smem + kBOff + buf * kBBytes, gj, gkh, gkq);
       else if constexpr (kRows == 8)
         store_rows8_sw128(gs.g, smem + kBOff + buf * kBBytes, gj, gkh);
@@ -640,13 +677,14 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         // biased s = W_(8+L) / 2 + 2^(7+L) straight from the GEMM
         uint32_t(&R0)[64] = *reinterpret_cast<uint32_t(*)[64]>(&R[0]);
         uint32_t(&R1)[64] = *reinterpret_cast<uint32_t(*)[64]>(&R[64]);
+        if constexpr (kLateB) gen_update();  // before R is live (register pressure)
         tc::tmem_ld_x64_p16(tbase, R0);
         tc::tmem_ld_x64_p16(tbase + 128, R1);
         tc::wait_ld_tied(R0);
         tc::wait_ld_tied(R1);
         tc::fence_before();
         mbar_arrive(&bar_tmem_empty);
-        gen_update();
+        if constexpr (!kLateB) gen_update();
         // R = 16: the 16-row generation needs 64 output registers, so B(i+2)
         // is stored after this item's stages (R dead); MMA(i+2) still only
         // waits for item i+1's TMEM read
@@ -962,13 +1000,16 @@ int launch_tc_nl_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t v_
   const int lc = 16 - n;
   const int64_t items = ((int64_t(v_hi) - 1) >> lc) + 1 - (int64_t(v_lo) >> lc);
   switch (n) {
-    case 11:
-      if constexpr (kLogRows <= 3) return run_tc_hybrid<kTcNL, 11>(a, items, st);
-      return set_error(SBW_EINVAL, "16-row generation needs n >= 12");
-    case 12: return run_tc_hybrid<kTcNL, 12>(a, items, st);
-    case 13: return run_tc_hybrid<kTcNL, 13>(a, items, st);
-    case 14: return run_tc_hybrid<kTcNL, 14>(a, items, st);
-    case 15: return run_tc_hybrid<kTcNL, 15>(a, items, st);
+#define SBW_TC_SMALL_CASE(N)                                         \
+    case N:                                                          \
+      if constexpr (8 + kLogRows <= N) return run_tc_hybrid<kTcNL, N>(a, items, st); \
+      return set_error(SBW_EINVAL, "row-group generation needs n >= %d", 8 + kLogRows);
+    SBW_TC_SMALL_CASE(11)
+    SBW_TC_SMALL_CASE(12)
+    SBW_TC_SMALL_CASE(13)
+    SBW_TC_SMALL_CASE(14)
+    SBW_TC_SMALL_CASE(15)
+#undef SBW_TC_SMALL_CASE
     default: return set_error(SBW_EINVAL, "tensor-core NL for n < 16 needs n in 11..15");
   }
 }
