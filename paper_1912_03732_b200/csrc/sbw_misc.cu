@@ -2,6 +2,7 @@
 // truth tables, the layout transpose, the reducers, the direct-sum and
 // affine-distance checkers and the INT32 peak microbenchmark.
 #include <climits>
+#include <cstdlib>
 
 #include "sbw_internal.cuh"
 #include "sbw_launch.h"
@@ -389,9 +390,101 @@ __global__ void __launch_bounds__(256) k_transpose(const int32_t* __restrict__ i
   }
 }
 
+// Dense x-major output (ld_out == rows): aligned 64-element chunks of the
+// flat output (default; SBW_TRANSPOSE_FLAT=0 keeps the tiled kernel).  Output row c's chunks
+// start at r = phi(c) = -c L mod 64; a CTA owns 64 consecutive output rows and
+// slides a 2 x 64-row input window over r, writing one whole aligned chunk
+// per output row per step.  A chunk past the end of row c continues in row
+// c + 1 at r' < 64: from the kept first window, or global memory for the
+// block's last row.
+constexpr int kFlatW = 64;
+constexpr size_t kFlatSmem = size_t(3) * kFlatW * (kFlatW + 1) * sizeof(int32_t);
+__global__ void __launch_bounds__(256) k_transpose_flat(const int32_t* __restrict__ in, int64_t rows,
+                                                        int64_t cols, int64_t ld_in, int32_t* __restrict__ out) {
+  extern __shared__ int32_t sm_flat[];
+  constexpr int P = kFlatW + 1;
+  int32_t* ring0 = sm_flat;
+  int32_t* first = sm_flat + 2 * kFlatW * P;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t nwin = (rows + kFlatW - 1) / kFlatW;
+  constexpr int kPer = kFlatW * kFlatW / 256;
+  int32_t pf[kPer];
+  // element e = t + 256 i of a window -> (rr, cc) = (e >> 6, e & 63): 32-bit
+  // offsets inside the window, one 64-bit base per window
+  const int cc_t = t & 63, rr_t = t >> 6;  // e >> 6 = rr_t + 4 i
+  auto fetch = [&](int64_t w, int64_t c0) {
+    const int32_t* base = in + (w * kFlatW) * ld_in + c0 + cc_t;
+    const int rlim = int(rows - w * kFlatW < kFlatW ? rows - w * kFlatW : kFlatW);
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int rr = rr_t + 4 * i;
+      pf[i] = rr < rlim ? __ldcs(base + int64_t(rr) * ld_in) : 0;
+    }
+  };
+  auto deposit = [&](int32_t* dst) {
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) dst[(rr_t + 4 * i) * P + cc_t] = pf[i];
+  };
+  const int rmod = int(rows % kFlatW);
+  for (int64_t cb = blockIdx.x; cb * kFlatW < cols; cb += gridDim.x) {
+    const int64_t c0 = cb * kFlatW;
+    fetch(0, c0);
+    deposit(first);
+    deposit(ring0);
+    if (nwin > 1) fetch(1, c0);
+    for (int64_t w = 0; w < nwin; ++w) {
+      if (w + 1 < nwin) {
+        deposit(ring0 + ((w + 1) & 1) * kFlatW * P);
+        if (w + 2 < nwin) fetch(w + 2, c0);
+      }
+      __syncthreads();
+      const int64_t rw = w * kFlatW;          // first input row of the window
+      const int rleft = int(rows - rw);        // rows left from the window start (> 0)
+      const int slot0 = int(w & 1);
+#pragma unroll 2
+      for (int j = 0; j < 8; ++j) {
+        const int cl = warp * 8 + j;           // output row inside the block
+        const int64_t c = c0 + cl;
+        // phi(c) = -c rows mod 64, from (c mod 64) (rows mod 64): 32-bit
+        const int phi = (kFlatW - int((uint32_t(c) & 63u) * uint32_t(rmod) & 63u)) & 63;
+        if (phi >= rleft) continue;            // no chunk of row c starts in this window
+        int32_t* orow = out + c * rows + rw;   // flat position of (c, rw)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int rl = phi + 32 * h + lane;  // row offset from rw, 0..127
+          int32_t v;
+          if (rl < rleft) {
+            v = ring0[(((rl >> 6) + slot0) & 1) * kFlatW * P + (rl & 63) * P + cl];
+          } else {  // continues in row c + 1 at r' = rl - rleft (< 64)
+            const int r2 = rl - rleft;
+            if (c + 1 >= cols) continue;
+            v = (cl + 1 < kFlatW) ? first[r2 * P + cl + 1] : __ldg(in + int64_t(r2) * ld_in + c + 1);
+          }
+          __stcs(orow + rl, v);
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 int launch_transpose_i32(const int32_t* in, int64_t rows, int64_t cols, int64_t ld_in,
                          int32_t* out, int64_t ld_out, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return SBW_OK;
+  const char* fe = getenv("SBW_TRANSPOSE_FLAT");  // "0": tiled kernel; "1<k>": k CTAs per SM
+  if (!(fe && fe[0] == '0') && ld_out == rows && rows >= kFlatW && cols % kFlatW == 0 &&
+      (reinterpret_cast<uintptr_t>(out) & 255) == 0) {
+    DeviceProps dp;
+    if (int rc = device_props(&dp)) return rc;
+    SBW_CUDA_CHECK(cudaFuncSetAttribute(k_transpose_flat, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(kFlatSmem)));
+    const int64_t blocks = cols / kFlatW;
+    const int cap = (fe && fe[0] && fe[1]) ? atoi(fe + 1) : 4;
+    const int grid = int(blocks < int64_t(dp.sm_count) * cap ? blocks : int64_t(dp.sm_count) * cap);
+    k_transpose_flat<<<grid, 256, kFlatSmem, st>>>(in, rows, cols, ld_in, out);
+    SBW_LAUNCH_CHECK("k_transpose_flat");
+    return SBW_OK;
+  }
   constexpr int TR = SBW_TR, TC = SBW_TCOL;
   const int64_t tiles = ((rows + TR - 1) / TR) * ((cols + TC - 1) / TC);
   k_transpose<TR, TC><<<grid_for(tiles, 1, SBW_TRANSPOSE_CAP), 256, 0, st>>>(in, rows, cols, ld_in, out, ld_out);
