@@ -407,25 +407,29 @@ __global__ void __launch_bounds__(256) k_transpose_flat(const int32_t* __restric
   int32_t* first = sm_flat + 2 * kFlatW * P;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t nwin = (rows + kFlatW - 1) / kFlatW;
-  constexpr int kPer = kFlatW * kFlatW / 256;
-  int32_t pf[kPer];
-  // element e = t + 256 i of a window -> (rr, cc) = (e >> 6, e & 63): 32-bit
-  // offsets inside the window, one 64-bit base per window
-  const int cc_t = t & 63, rr_t = t >> 6;  // e >> 6 = rr_t + 4 i
+  // fetch: 16-byte loads, thread t -> rows (t >> 4) + 16 i, columns 4 (t & 15) .. +3
+  int4 pf[4];
+  const int cq = (t & 15) * 4, rq = t >> 4;
   auto fetch = [&](int64_t w, int64_t c0) {
-    const int32_t* base = in + (w * kFlatW) * ld_in + c0 + cc_t;
+    const int32_t* base = in + (w * kFlatW) * ld_in + c0 + cq;
     const int rlim = int(rows - w * kFlatW < kFlatW ? rows - w * kFlatW : kFlatW);
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      const int rr = rr_t + 4 * i;
-      pf[i] = rr < rlim ? __ldcs(base + int64_t(rr) * ld_in) : 0;
+    for (int i = 0; i < 4; ++i) {
+      const int rr = rq + 16 * i;
+      pf[i] = rr < rlim ? __ldcs(reinterpret_cast<const int4*>(base + int64_t(rr) * ld_in)) : make_int4(0, 0, 0, 0);
     }
   };
   auto deposit = [&](int32_t* dst) {
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) dst[(rr_t + 4 * i) * P + cc_t] = pf[i];
+    for (int i = 0; i < 4; ++i) {
+      int32_t* d = dst + (rq + 16 * i) * P + cq;
+      d[0] = pf[i].x; d[1] = pf[i].y; d[2] = pf[i].z; d[3] = pf[i].w;
+    }
   };
   const int rmod = int(rows % kFlatW);
+  // emit: a warp instruction stores two aligned 64-element chunks (lanes
+  // 0-15 one output row, 16-31 the next), 16 bytes = 4 consecutive r per lane
+  const int half = lane >> 4, q4 = (lane & 15) * 4;
   for (int64_t cb = blockIdx.x; cb * kFlatW < cols; cb += gridDim.x) {
     const int64_t c0 = cb * kFlatW;
     fetch(0, c0);
@@ -438,29 +442,34 @@ __global__ void __launch_bounds__(256) k_transpose_flat(const int32_t* __restric
         if (w + 2 < nwin) fetch(w + 2, c0);
       }
       __syncthreads();
-      const int64_t rw = w * kFlatW;          // first input row of the window
-      const int rleft = int(rows - rw);        // rows left from the window start (> 0)
+      const int64_t rw = w * kFlatW;
+      const int rleft = int(rows - rw);
       const int slot0 = int(w & 1);
-#pragma unroll 2
-      for (int j = 0; j < 8; ++j) {
-        const int cl = warp * 8 + j;           // output row inside the block
-        const int64_t c = c0 + cl;
-        // phi(c) = -c rows mod 64, from (c mod 64) (rows mod 64): 32-bit
-        const int phi = (kFlatW - int((uint32_t(c) & 63u) * uint32_t(rmod) & 63u)) & 63;
-        if (phi >= rleft) continue;            // no chunk of row c starts in this window
-        int32_t* orow = out + c * rows + rw;   // flat position of (c, rw)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int rl = phi + 32 * h + lane;  // row offset from rw, 0..127
-          int32_t v;
+      for (int j = 0; j < 4; ++j) {
+        const int cl = warp * 8 + 2 * j + half;  // this half-warp's output row inside the block
+        const int64_t c = c0 + cl;
+        const int phi = (kFlatW - int((uint32_t(c) & 63u) * uint32_t(rmod) & 63u)) & 63;
+        if (phi >= rleft) continue;              // (half-warp uniform) no chunk starts here
+        int v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int rl = phi + q4 + k;           // 0..127 from rw
           if (rl < rleft) {
-            v = ring0[(((rl >> 6) + slot0) & 1) * kFlatW * P + (rl & 63) * P + cl];
+            v[k] = ring0[(((rl >> 6) + slot0) & 1) * kFlatW * P + (rl & 63) * P + cl];
           } else {  // continues in row c + 1 at r' = rl - rleft (< 64)
             const int r2 = rl - rleft;
-            if (c + 1 >= cols) continue;
-            v = (cl + 1 < kFlatW) ? first[r2 * P + cl + 1] : __ldg(in + int64_t(r2) * ld_in + c + 1);
+            v[k] = (c + 1 >= cols) ? 0
+                   : (cl + 1 < kFlatW) ? first[r2 * P + cl + 1] : __ldg(in + int64_t(r2) * ld_in + c + 1);
           }
-          __stcs(orow + rl, v);
+        }
+        int32_t* dst = out + c * rows + rw + phi + q4;  // 16-byte aligned (chunk starts are 256-byte aligned)
+        if (c + 1 < cols || phi + q4 + 3 < rleft) {
+          __stcs(reinterpret_cast<int4*>(dst), make_int4(v[0], v[1], v[2], v[3]));
+        } else {  // the last output row: stop at the end of the array
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (phi + q4 + k < rleft) dst[k] = v[k];
         }
       }
       __syncthreads();
@@ -472,8 +481,8 @@ int launch_transpose_i32(const int32_t* in, int64_t rows, int64_t cols, int64_t 
                          int32_t* out, int64_t ld_out, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return SBW_OK;
   const char* fe = getenv("SBW_TRANSPOSE_FLAT");  // "0": tiled kernel; "1<k>": k CTAs per SM
-  if (!(fe && fe[0] == '0') && ld_out == rows && rows >= kFlatW && cols % kFlatW == 0 &&
-      (reinterpret_cast<uintptr_t>(out) & 255) == 0) {
+  if (!(fe && fe[0] == '0') && ld_out == rows && rows >= kFlatW && cols % kFlatW == 0 && ld_in % 4 == 0 &&
+      (reinterpret_cast<uintptr_t>(out) & 255) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
     DeviceProps dp;
     if (int rc = device_props(&dp)) return rc;
     SBW_CUDA_CHECK(cudaFuncSetAttribute(k_transpose_flat, cudaFuncAttributeMaxDynamicSharedMemorySize,
