@@ -400,7 +400,8 @@ __global__ void __launch_bounds__(256) k_transpose(const int32_t* __restrict__ i
 constexpr int kFlatW = 64;
 constexpr size_t kFlatSmem = size_t(3) * kFlatW * (kFlatW + 1) * sizeof(int32_t);
 __global__ void __launch_bounds__(256) k_transpose_flat(const int32_t* __restrict__ in, int64_t rows,
-                                                        int64_t cols, int64_t ld_in, int32_t* __restrict__ out) {
+                                                        int64_t cols, int64_t ld_in, int32_t* __restrict__ out,
+                                                        int64_t seg_windows) {
   extern __shared__ int32_t sm_flat[];
   constexpr int P = kFlatW + 1;
   int32_t* ring0 = sm_flat;
@@ -430,16 +431,24 @@ __global__ void __launch_bounds__(256) k_transpose_flat(const int32_t* __restric
   // emit: a warp instruction stores two aligned 64-element chunks (lanes
   // 0-15 one output row, 16-31 the next), 16 bytes = 4 consecutive r per lane
   const int half = lane >> 4, q4 = (lane & 15) * 4;
-  for (int64_t cb = blockIdx.x; cb * kFlatW < cols; cb += gridDim.x) {
+  // work item = (64-column block, segment of seg_windows windows), so small
+  // spectra still fill the GPU; a segment reloads the first window for the
+  // chunks that continue into the next output row
+  const int64_t nseg = (nwin + seg_windows - 1) / seg_windows;
+  const int64_t items = (cols / kFlatW) * nseg;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t cb = it / nseg, w0 = (it % nseg) * seg_windows;
+    const int64_t w1 = w0 + seg_windows < nwin ? w0 + seg_windows : nwin;
     const int64_t c0 = cb * kFlatW;
     fetch(0, c0);
     deposit(first);
-    deposit(ring0);
-    if (nwin > 1) fetch(1, c0);
-    for (int64_t w = 0; w < nwin; ++w) {
+    if (w0 > 0) fetch(w0, c0);
+    deposit(ring0 + (w0 & 1) * kFlatW * P);
+    if (w0 + 1 < nwin) fetch(w0 + 1, c0);
+    for (int64_t w = w0; w < w1; ++w) {
       if (w + 1 < nwin) {
         deposit(ring0 + ((w + 1) & 1) * kFlatW * P);
-        if (w + 2 < nwin) fetch(w + 2, c0);
+        if (w + 2 < nwin && w + 1 < w1) fetch(w + 2, c0);
       }
       __syncthreads();
       const int64_t rw = w * kFlatW;
@@ -487,10 +496,15 @@ int launch_transpose_i32(const int32_t* in, int64_t rows, int64_t cols, int64_t 
     if (int rc = device_props(&dp)) return rc;
     SBW_CUDA_CHECK(cudaFuncSetAttribute(k_transpose_flat, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         int(kFlatSmem)));
-    const int64_t blocks = cols / kFlatW;
+    const int64_t blocks = cols / kFlatW, nwin = (rows + kFlatW - 1) / kFlatW;
     const int cap = (fe && fe[0] && fe[1]) ? atoi(fe + 1) : 4;
-    const int grid = int(blocks < int64_t(dp.sm_count) * cap ? blocks : int64_t(dp.sm_count) * cap);
-    k_transpose_flat<<<grid, 256, kFlatSmem, st>>>(in, rows, cols, ld_in, out);
+    const int64_t slots = int64_t(dp.sm_count) * cap;
+    // segments: enough work items for every CTA slot, each >= 4 windows
+    int64_t seg = (blocks * nwin + slots - 1) / slots;
+    if (seg < 4) seg = 4;
+    const int64_t items = blocks * ((nwin + seg - 1) / seg);
+    const int grid = int(items < slots ? items : slots);
+    k_transpose_flat<<<grid, 256, kFlatSmem, st>>>(in, rows, cols, ld_in, out, seg);
     SBW_LAUNCH_CHECK("k_transpose_flat");
     return SBW_OK;
   }
