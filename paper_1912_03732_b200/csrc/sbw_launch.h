@@ -28,6 +28,9 @@ bool tc_path_enabled();
 int tc_min_small_n();  // smallest n of launch_tc_nl_small (11, or 12 for 16-row generation builds)
 int launch_tc_nl_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
                        unsigned long long* key, cudaStream_t st);
+// Tensor-core n = tc_min_small_n()..15 materialised spectrum (m >= 16 - n), mask-major rows.
+int launch_tc_spec_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
+                         int32_t* out, int64_t ld, cudaStream_t st);
 // Tensor-core n = 16 materialised spectrum, mask-major rows out[(v - v_lo) * ld + u].
 int launch_tc16_spec(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
                      int32_t* out, int64_t ld, cudaStream_t st);

@@ -449,7 +449,8 @@ __device__ __forceinline__ void publish_item(const TcArgs& a, const uint32_t* wm
 template <int MODE, int NB = 16>
 __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
   constexpr bool EMIT = is_emit(MODE);
-  static_assert(NB == 16 || (MODE == kTcNL && NB >= 8 + kLogRows && kRows >= 8), "n < 16: NL with 8/16-row groups");
+  static_assert(NB == 16 || ((MODE == kTcNL || MODE == kTcSpec) && NB >= 8 + kLogRows && kRows >= 8),
+                "n < 16: NL / SPEC with 8/16-row groups");
   constexpr int kSlots = 1 << (16 - NB);  // components per 2^16 tile
   static_assert(MODE != kTcSpec || kC0Mma, "exact SPEC output needs the bias-block GEMM");
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -829,7 +830,41 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
           const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<NB>(mx, mn)));
           if (lane == 0) s_wmax[i & 3][sl][mw] = m;
         }
-        if constexpr (MODE == kTcSpec) {
+        if constexpr (MODE == kTcSpec && NB < 16) {
+          // n < 16: per slot (component v = vi | slot) the exact W of every
+          // lane, W = 2 s - 2^NB for the biased s; no lane can wrap (|W| <=
+          // 2^NB <= 2^15).  u = u_c * 256 + u_r, u_c from the register index
+          // and lane inside the slot (natural order); 32 consecutive u_r per
+          // warp store.
+          uint32_t vi, bpi;
+          item_at<MODE, NB>(a, t_lo + i, vi, bpi);
+          constexpr int kPerSlot = 1 << (NB - 9);  // registers per slot
+#pragma unroll
+          for (int sl = 0; sl < kSlots; ++sl) {
+            const uint32_t v = vi | uint32_t(sl);
+            if (v < a.v_lo || v >= a.v_hi) continue;
+            int32_t* row = a.out + int64_t(v - a.v_lo) * a.ld + u;
+            if constexpr (NB >= 9 + kLogRows) {  // the top stage pairs k, k + kPerSlot / 2
+#pragma unroll
+              for (int kk = 0; kk < kPerSlot / 2; ++kk) {
+                const uint32_t x = R[sl * kPerSlot + kk], y = R[sl * kPerSlot + kk + kPerSlot / 2];
+                const int x0 = int(x & 0xFFFFu), x1 = int(x >> 16), y0 = int(y & 0xFFFFu), y1 = int(y >> 16);
+                __stcs(row + (2 * kk) * 256, 2 * (x0 + y0) - (1 << NB));
+                __stcs(row + (2 * kk + 1) * 256, 2 * (x1 + y1) - (1 << NB));
+                __stcs(row + (2 * kk + kPerSlot) * 256, 2 * (x0 - y0));
+                __stcs(row + (2 * kk + 1 + kPerSlot) * 256, 2 * (x1 - y1));
+              }
+            } else {  // the GEMM output is final
+#pragma unroll
+              for (int kk = 0; kk < kPerSlot; ++kk) {
+                const uint32_t x = R[sl * kPerSlot + kk];
+                __stcs(row + (2 * kk) * 256, 2 * int(x & 0xFFFFu) - (1 << NB));
+                __stcs(row + (2 * kk + 1) * 256, 2 * int(x >> 16) - (1 << NB));
+              }
+            }
+          }
+        }
+        if constexpr (MODE == kTcSpec && NB == 16) {
           // exact W of the top stage per lane (the packed S / D above may wrap
           // at |W| = 2^16), stored at u = u_c * 256 + u_r with
           // u_c = lane + 2 k (+ 128 for the diff) -- 32 consecutive u_r per
@@ -1011,6 +1046,33 @@ int launch_tc_nl_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t v_
     SBW_TC_SMALL_CASE(15)
 #undef SBW_TC_SMALL_CASE
     default: return set_error(SBW_EINVAL, "tensor-core NL for n < 16 needs n in 11..15");
+  }
+}
+
+int launch_tc_spec_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
+                         int32_t* out, int64_t ld, cudaStream_t st) {
+  TcArgs a{};
+  a.planes = planes;
+  a.plane_words = (int64_t(1) << n) >> 5;
+  a.v_lo = v_lo;
+  a.v_hi = v_hi;
+  a.max_abs = max_abs;
+  a.out = out;
+  a.ld = ld;
+  const int lc = 16 - n;
+  const int64_t items = ((int64_t(v_hi) - 1) >> lc) + 1 - (int64_t(v_lo) >> lc);
+  switch (n) {
+#define SBW_TC_SPEC_CASE(N)                                                             \
+    case N:                                                                             \
+      if constexpr (8 + kLogRows <= N) return run_tc_hybrid<kTcSpec, N>(a, items, st); \
+      return set_error(SBW_EINVAL, "row-group generation needs n >= %d", 8 + kLogRows);
+    SBW_TC_SPEC_CASE(11)
+    SBW_TC_SPEC_CASE(12)
+    SBW_TC_SPEC_CASE(13)
+    SBW_TC_SPEC_CASE(14)
+    SBW_TC_SPEC_CASE(15)
+#undef SBW_TC_SPEC_CASE
+    default: return set_error(SBW_EINVAL, "tensor-core spectrum for n < 16 needs n in 11..15");
   }
 }
 

@@ -139,8 +139,9 @@ int launch_fused_onchip(const void* table, int tbytes, int n, int m, uint32_t v_
   }
   uint32_t* planes = static_cast<uint32_t*>(scratch);
   if (int rc = build_planes(table, tbytes, n, m, planes, st)) return rc;
-  if (n >= tc_min_small_n() && n <= 15 && out == nullptr && m >= 16 - n && tc_path_enabled())
-    return launch_tc_nl_small(planes, n, v_lo, v_hi, max_abs, key, st);
+  if (n >= tc_min_small_n() && n <= 15 && m >= 16 - n && tc_path_enabled())
+    return out == nullptr ? launch_tc_nl_small(planes, n, v_lo, v_hi, max_abs, key, st)
+                          : launch_tc_spec_small(planes, n, v_lo, v_hi, max_abs, out, ld, st);
   if (n == 16 && tc_path_enabled())
     return out == nullptr ? launch_tc16_nl(planes, v_lo, v_hi, max_abs, key, st)
                           : launch_tc16_spec(planes, v_lo, v_hi, max_abs, out, ld, st);

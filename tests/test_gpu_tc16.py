@@ -142,3 +142,15 @@ def test_small_n_tensor_core_slots(n, m, lo, hi):
     assert np.array_equal(got, want)
     i = int(np.argmax(want))
     assert (v, mxw) == (lo + i, int(want[i]))
+
+
+@pytest.mark.parametrize("n,m,lo,hi", [(15, 15, 1, 700), (14, 14, 5, 1001), (13, 16, 1000, 1301),
+                                       (12, 12, 1, 4096), (12, 4, 1, 16), (15, 1, 1, 2), (14, 20, 70001, 70040)])
+def test_small_n_tensor_core_spectrum(n, m, lo, hi):
+    """n = 12..15 materialised spectra on the tensor-core kernel (k_tc_hybrid<SPEC, n>):
+    exact W per slot, ranges starting / ending inside an item, m = 16 - n exactly."""
+    s = sw.generate_sbox(n, m, 60 + n, bijective=(n == m))
+    rows, mx = sw.spectrum_device(s, lo, hi)
+    want = orc.spectrum(s.table, n, lo, hi)
+    assert np.array_equal(rows.cpu().numpy(), want)
+    assert np.array_equal(mx.cpu().numpy(), np.abs(want).max(axis=1))
