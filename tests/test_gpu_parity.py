@@ -598,3 +598,21 @@ def test_full_large_config_nl(name, want):
     checks = [res[1]] + [int(v) for v in np.random.default_rng(9).integers(1, 1 << s.m, 2)]
     for v in checks:
         assert full[v - 1] == orc.component_max_abs(s.table, s.n, v, v + 1)[0], v
+
+
+def test_evaluate_retain_skips_the_discarded_spectrum():
+    """evaluate(method fused/parallel, mode retain) never materialises the
+    spectrum it discards, but keeps the reference's retain-mode budget check
+    and charge (walsh.py:220-222, parallel.py:91-93) and the same result."""
+    s = sw.generate_sbox(12, 12, seed=5, bijective=True)
+    need = 4095 * 4096 * 4
+    for method in ("fused", "parallel"):
+        sw.spectrum_allocations.reset_peak()
+        r = sw.evaluate(s, method=method, mode="retain")
+        assert sw.spectrum_allocations.peak_bytes >= need and sw.spectrum_allocations.current_bytes == 0
+        _, cm = sw.fwht_fused(s, mode="retain")
+        assert (r.value, r.argmin_v) == (sw.nonlinearity_from_maxima(cm).value, sw.nonlinearity_from_maxima(cm).argmin_v)
+        with pytest.raises(sw.MemoryBudgetError):
+            sw.evaluate(s, method=method, mode="retain", max_bytes=need - 1)
+    with pytest.raises(ValueError):
+        sw.evaluate(s, method="parallel", workers=0)
