@@ -176,14 +176,14 @@ def maxabs_to_nl(max_abs, n: int) -> np.ndarray:
     torch = _dev.torch_mod()
     dev = max_abs.device
     count = max_abs.numel()
-    nl = torch.empty(max(1, count), dtype=torch.int64, device=dev)
-    bad = torch.empty(1, dtype=torch.int64, device=dev)
-    _dev.check(_dev.load_library().sbw_maxabs_to_nl(_dev.ptr(max_abs), count, n, _dev.ptr(nl),
-                                                    _dev.ptr(bad), _dev.stream_handle(dev)))
-    b = int(bad.item())
+    out = torch.empty(count + 1, dtype=torch.int64, device=dev)  # NL values, then the odd-gap flag
+    _dev.check(_dev.load_library().sbw_maxabs_to_nl(_dev.ptr(max_abs), count, n, _dev.ptr(out),
+                                                    _dev.ptr(out) + 8 * count, _dev.stream_handle(dev)))
+    host = out.cpu().numpy()  # one device -> host copy
+    b = int(host[count])
     if b != INT64_MAX:
         raise AssertionError(f"odd spectrum gap at component {b}: not a genuine Walsh column")
-    return nl[:count].cpu().numpy()
+    return host[:count]
 
 
 def decode_key(key, n: int) -> tuple[int, int, int]:
