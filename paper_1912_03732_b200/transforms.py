@@ -142,10 +142,12 @@ def spectrum_to_host(s: SBox, v_lo: int = 1, v_hi: int | None = None, layout: st
 
     def drain(slot, a, b):
         done[slot].synchronize()
+        # torch's CPU copy runs on all intra-op threads (numpy's assignment is
+        # one thread), which also spreads the first-touch page faults of `out`
         if layout == "mask":
-            out[a - v_lo:b - v_lo] = pins[slot][: b - a].numpy()
+            torch.from_numpy(out[a - v_lo:b - v_lo]).copy_(pins[slot][: b - a])
         else:
-            out[:, a - v_lo:b - v_lo] = pins[slot][:, : b - a].numpy()
+            torch.from_numpy(out[:, a - v_lo:b - v_lo]).copy_(pins[slot][:, : b - a])
 
     for i, a in enumerate(range(v_lo, v_hi, rows)):
         b = min(v_hi, a + rows)
