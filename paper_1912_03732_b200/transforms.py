@@ -254,7 +254,10 @@ def _inplace_rows(rows2d: np.ndarray) -> np.ndarray:
     mx = torch.empty(max(1, count), dtype=torch.int64, device=dev)
     _dev.check(_dev.load_library().sbw_fwht_inplace(_dev.ptr(d), k, count, _dev.ptr(mx),
                                                     _dev.stream_handle(dev)))
-    rows2d[...] = d.cpu().numpy()
+    if rows2d.flags.c_contiguous:
+        torch.from_numpy(rows2d).copy_(d)  # one device -> host copy straight into the caller's array
+    else:
+        rows2d[...] = d.cpu().numpy()
     return mx[:count].cpu().numpy()
 
 
