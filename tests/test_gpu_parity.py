@@ -616,3 +616,21 @@ def test_evaluate_retain_skips_the_discarded_spectrum():
             sw.evaluate(s, method=method, mode="retain", max_bytes=need - 1)
     with pytest.raises(ValueError):
         sw.evaluate(s, method="parallel", workers=0)
+
+
+def test_spectrum_scan_host_chunks_rebase_rows():
+    """A host spectrum larger than one scan chunk (256 MiB) is staged chunk by
+    chunk; the per-chunk keys are re-based to global rows: largest max|W| wins,
+    ties go to the smallest v (nonlinearity.py:36-48)."""
+    n = 16
+    nrows = 2047  # 2047 x 2^16 int32 = 537 MB: three chunks
+    rows = np.zeros((nrows, 1 << n), dtype=np.int32)
+    rows[:, 0] = 2
+    rows[1100, 5] = -1000   # the maximum, in the second chunk ...
+    rows[1150, 7] = 1000    # ... tied by a later row
+    rows[3, 9] = 998
+    r = sw.nonlinearity_from_spectrum(sw.WalshSpectrum(n, 11, rows))
+    assert (r.value, r.argmin_v) == (((1 << n) - 1000) // 2, 1101)
+    row_max, _ = sw.reducers.spectrum_row_maxabs(sw.WalshSpectrum(n, 11, rows))
+    want = np.abs(rows).max(axis=1)
+    assert np.array_equal(row_max.cpu().numpy(), want)
