@@ -106,7 +106,12 @@ def polarity_truth_table(s: SBox, max_bytes: int | None = None) -> PolarityTruth
     """Mask-major (2^m - 1) x 2^n polarity matrix (sbox.py:155-162)."""
     check_budget(((1 << s.m) - 1) * (1 << s.n) * 4, max_bytes)
     dev = _dev.require_device()
-    rows = _polarity_device(s, 1, 1 << s.m, _dev.LAYOUT_MASK_MAJOR, dev).cpu().numpy()
+    d = _polarity_device(s, 1, 1 << s.m, _dev.LAYOUT_MASK_MAJOR, dev)
+    if d.numel() * 4 > (256 << 20):
+        from .transforms import device_to_host_chunked
+        rows = device_to_host_chunked(d, np.empty(tuple(d.shape), dtype=np.int32))
+    else:
+        rows = d.cpu().numpy()
     return PolarityTruthTable(s.n, s.m, rows)
 
 

@@ -19,7 +19,8 @@ import numpy as np
 from . import device as _dev
 from .accounting import charged, check_budget, memory_estimate
 from .records import ColumnMaxima, ColumnPartition, NonlinearityResult, SBox, WalshSpectrum
-from .transforms import component_max_abs_device, decode_key, maxabs_to_nl, spectrum_device
+from .transforms import (component_max_abs_device, decode_key, device_to_host_chunked, maxabs_to_nl,
+                         spectrum_device)
 
 
 def partition_columns(total_columns: int, workers: int) -> ColumnPartition:
@@ -94,7 +95,7 @@ def fwht_parallel(s: SBox, workers: int | None = None, mode: str = "retain",
         for lo, hi, spec, mx in pending:  # completion barrier, in range order
             values[lo - 1:hi - 1] = maxabs_to_nl(mx, s.n)
             if spec is not None:
-                rows[lo - 1:hi - 1] = spec.cpu().numpy()
+                device_to_host_chunked(spec, rows[lo - 1:hi - 1])
         t2 = time.perf_counter()
     if timings is not None:
         timings["build_s"] = t1 - t0
