@@ -320,6 +320,8 @@ def transform_rows_in_place(rows: np.ndarray, maxima_out: np.ndarray | None = No
 
 
 def _host_rows(t) -> np.ndarray:
+    if t.dim() == 2 and t.is_contiguous() and t.numel() * t.element_size() > (256 << 20):
+        return device_to_host_chunked(t, np.empty(tuple(t.shape), dtype=np.int32))
     return t.cpu().numpy()
 
 
