@@ -174,6 +174,37 @@ def cpu_baseline(name, target_s=12.0, procs=None):
                       f"{wall:.1f} s wall"}
 
 
+def cpu_engine(name, target_s=4.0):
+    """The reference's SHIPPED engine shape: fwht_parallel
+    (parallel.py:64-133) = a ThreadPoolExecutor over partition_columns ranges,
+    each worker running the per-mask stream body (walsh.py:237-240), here the
+    oracle port of that body.  Timed with workers = os.cpu_count() and 1 over
+    a bounded mask sample; the GIL lets ~1 core run numpy's small per-stage
+    ufunc calls at a time, which is why the process harness above is faster."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import sbw_oracle as orc
+
+    n, m, bij = CONFIGS[name]
+    t = orc.gen_table(n, m, 0, bij)
+    k0 = 2 if n >= 20 else 8
+    t0 = time.perf_counter()
+    orc.stream_loop(t, n, 1, 1 + k0)
+    per_mask = (time.perf_counter() - t0) / k0
+    total = max(1, min((1 << m) - 1, int(target_s / per_mask / 2)))
+    out = {"sample": f"{name} seed 0, masks 1..{total}", "unit": "coeff/s",
+           "note": "reference engine shape: ThreadPoolExecutor(workers) over partition_columns "
+                   "ranges running the per-mask stream body (oracle port); GIL-bound"}
+    for workers in (os.cpu_count() or 1, 1):
+        part = orc.partition_columns(total, workers)
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=len(part)) as pool:
+            list(pool.map(lambda r: orc.stream_loop(t, n, r[0], r[1]), part))
+        out[f"workers_{workers}"] = coeffs(n, m, total) / (time.perf_counter() - t0)
+    out["cores"] = os.cpu_count() or 1
+    return out
+
+
 # ------------------------------------------------------------------- GPU ----
 def measured_hbm_peak():
     """HBM copy bandwidth in GB/s from the driver-written MEASURED_PEAKS.json,
@@ -291,7 +322,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- correctness of what was timed (against the committed goldens) ----
     if int(bad.item()) != (1 << 63) - 1:
         raise AssertionError("odd spectrum gap in the benchmark run")
-    res = sw.transforms.decode_key(key, n)
+    res = sw.walsh.decode_key(key, n)
     check = {"nl": res[0], "argmin_v": res[1], "max_abs": res[2]}
     if args.config == "16x16" and rank == 0 and not args.masks and (args.shard or world == 1):
         assert (res[0], res[1]) == (31942, 44828), res
@@ -442,7 +473,10 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": (value / (1 if args.shard else world)) / (coeffs(16, 16) / (PAPER_16x16_NL_MS * 1e-3))
         if args.config == "16x16" and not args.masks else None,
         "vs_baseline_ref": "PAPER.md:421 fused NL 16x16 = 83,015 ms on i7-8700K-class CPU (BASELINE.md)",
-        "dtype": "int8 MMA (s32 acc) + packed int16" if tc_path else "int32 (packed int8/int16 lanes)",
+        "dtype": ("int8 MMA (s32 acc) + packed int16" if tc_path else
+                  ("u16 scratch: int8 MMA pass A (s32 acc), pass B "
+                   + ("int8 MMA (s32 acc)" if n >= 21 else "fp32 (exact integers < 2^24)"))
+                  if n >= 17 else "packed int8/int16 lanes (int32 ALU)"),
         "data": "synthetic: generate_sbox(n, m, seed=rank) -- numpy PCG64 like the reference",
         "config": {"workload": f"{args.config} S-box (n={n}, m={m}, bijective={bij}), "
                                f"masks [{v_lo},{v_hi}), full NL per step",
@@ -463,6 +497,7 @@ def run_ours(args, rank, world, local_rank):
     }
     if not args.no_cpu and world == 1:  # the CPU baseline is reported at N = 1 only
         line["cpu_baseline"] = cpu_baseline(args.config, target_s=args.cpu_seconds)
+        line["cpu_baseline"]["engine"] = cpu_engine(args.config, target_s=args.cpu_seconds / 3)
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -492,11 +527,49 @@ def run_reference(args, rank, world):
         "config": {"workload": f"{args.config} S-box (n={n}, m={m}, bijective={bij})",
                    "note": "each step is a bounded mask sample; full-NL time extrapolated "
                            "linearly in the number of masks"},
-        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline": dict({k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                             engine=cpu_engine(args.config, target_s=args.cpu_seconds / 3)),
         "e2e": {"value": value, "unit": "coeff/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _free_port():
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(n):
+    """`python bench.py --gpus N` without torchrun: start N ranks of this
+    script (one per GPU, RANK/LOCAL_RANK/WORLD_SIZE/MASTER_* set as torchrun
+    would), stream their output, and exit with the worst exit code.  Rank 0
+    alone prints the JSON line.  If any rank fails the others are stopped
+    (a rank blocked in a collective would otherwise wait forever)."""
+    port = _free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                      env=env))
+    rc = 0
+    live = list(procs)
+    while live:
+        for p in list(live):
+            code = p.poll()
+            if code is None:
+                continue
+            live.remove(p)
+            if code != 0:
+                rc = rc or code
+                for q in live:
+                    q.terminate()
+        time.sleep(0.05)
+    return rc
 
 
 def main():
@@ -508,13 +581,20 @@ def main():
     ap.add_argument("--config", choices=list(CONFIGS), default="16x16")
     ap.add_argument("--masks", type=int, default=0, help="limit masks (debug)")
     ap.add_argument("--shard", action="store_true",
-                    help="strong scaling: shard one box's masks over the ranks (20x20 / 24x16 mode)")
+                    help="strong scaling: shard one box's masks over the ranks (the default for N > 1)")
+    ap.add_argument("--weak", action="store_true",
+                    help="N > 1: one whole box per rank (seed = rank) instead of sharding one box")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
+    if args.impl == "ours" and "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
+    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.impl == "reference" else 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    # N > 1: the north_star's mode -- one box, output masks sharded over the
+    # GPUs (partition_columns), one max-all-reduce of the key per step
+    args.shard = (args.shard or world > 1) and not args.weak
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

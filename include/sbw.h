@@ -48,6 +48,16 @@ extern "C" {
 #define SBW_LAYOUT_MASK_MAJOR 0 /* out[(v - v_lo) * ld + u]  (WalshSpectrum.rows, walsh.py:32-44) */
 #define SBW_LAYOUT_X_MAJOR 1    /* out[u * ld + (v - v_lo)]  (build_polarity_xmajor, walsh.py:117-131) */
 
+/* Element types of sbw_fwht_inplace_strided (numpy dtypes of the column). */
+#define SBW_ELEM_I8 1
+#define SBW_ELEM_U8 2
+#define SBW_ELEM_I16 3
+#define SBW_ELEM_U16 4
+#define SBW_ELEM_I32 5
+#define SBW_ELEM_U32 6
+#define SBW_ELEM_I64 7
+#define SBW_ELEM_U64 8
+
 typedef struct sbw_device_info {
   int device;
   int sm_count;
@@ -73,8 +83,15 @@ uint64_t sbw_launch_count(void);
  *   d_max_abs[v - v_lo] <- max_u |W(u,v)|               (int32, device)
  *   *d_key              <- atomicMax(key) over the range (device, may be NULL;
  *                          caller initialises it, e.g. to 0)
- * n, m in 1..24.  `scratch`/`scratch_bytes` is a device workspace required
- * only for n >= 17 (size from sbw_nl_scratch_bytes); pass NULL/0 otherwise.
+ * n, m in 1..24.  `scratch`/`scratch_bytes` is a device workspace of at
+ * least sbw_nl_scratch_bytes(n, m, v_lo, v_hi) bytes: the S-box bit planes
+ * for n = 7..16, plus the multi-pass batch buffers for n >= 17.  Only when
+ * that size is 0 (n <= 6) may it be NULL/0.
+ *
+ * Device selection (every entry point taking a stream): the call runs on
+ * the stream's device, or -- for the NULL/legacy stream -- on the device
+ * that owns the first device pointer argument (the table here); the
+ * caller's current device is restored before returning.
  */
 int sbw_nl(const void* d_table, int table_bytes, int n, int m, uint32_t v_lo, uint32_t v_hi,
            int32_t* d_max_abs, unsigned long long* d_key, void* scratch, size_t scratch_bytes,
@@ -111,6 +128,21 @@ int sbw_polarity(const void* d_table, int table_bytes, int n, int m, uint32_t v_
  * column's max of numpy-int32 |x| (k >= 1) or |x| (k == 0).
  */
 int sbw_fwht_inplace(int32_t* d_data, int k, int64_t count, int64_t* d_max_abs, void* stream);
+
+/*
+ * The same butterfly on any integer dtype and any strides, in place:
+ * fwht_column_in_place on non-int32 / strided numpy columns (walsh.py:73-104,
+ * "Accepts any uniformly strided 1-D view") and transform_xmajor_in_place
+ * (walsh.py:134-137: col_stride 1, elem_stride = the x-major row pitch).
+ * Column c starts at d_data + c * col_stride and its element i sits at
+ * + i * elem_stride (strides in elements, may be negative).  Arithmetic wraps
+ * modulo 2^(8 * sizeof(elem)) exactly as numpy's in-place ufuncs do, and
+ * d_max_abs[c] (may be NULL) receives np.abs(column).max() in that dtype
+ * (np.abs(MIN) == MIN for signed types; uint64 results are uint64 bits),
+ * or abs(int(col[0])) as uint64 bits when k == 0.
+ */
+int sbw_fwht_inplace_strided(void* d_data, int elem_type, int k, int64_t count, int64_t col_stride,
+                             int64_t elem_stride, int64_t* d_max_abs, void* stream);
 
 /*
  * Per-component max|W| -> NL_v = (2^n - max|W|) >> 1 as int64 (ColumnMaxima
@@ -150,7 +182,8 @@ int sbw_nl_bruteforce(const void* d_table, int table_bytes, int n, int m, int32_
  * copies per-component NL (int64) device->host and returns
  * out3 = {NL value, argmin_v, max|W|}.  Synchronous.  Page-locked h_table /
  * h_nl (cudaHostRegister, cudaMallocHost) are DMA'd directly; pageable ones
- * are staged through an internal pinned buffer.
+ * are staged through an internal pinned buffer.  The caller's current device
+ * is restored on return.
  */
 int sbw_nl_host(const uint32_t* h_table, int n, int m, uint32_t v_lo, uint32_t v_hi,
                 int64_t* h_nl, int64_t* out3, int device);

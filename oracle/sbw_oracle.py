@@ -103,6 +103,41 @@ def fwht_column(col: np.ndarray) -> tuple[np.ndarray, int]:
     return out, mx
 
 
+def fwht_column_typed(col: np.ndarray) -> tuple[np.ndarray, int]:
+    """fwht_column_in_place for ANY integer dtype (walsh.py:73-104): the
+    butterfly in the column's own dtype, out of place and stage by stage
+    ((a, b) -> (a + b, a - b) with numpy's wrap-around modulo 2^bits, equal
+    to the reference's hi = a - b; lo = 2a - hi), the max being
+    np.abs(final).max() in that dtype; length 1 -> abs(int(col[0])).
+    Returns (transformed copy in col.dtype, max_abs as a Python int)."""
+    length = col.shape[0]
+    if length == 0 or length & (length - 1):
+        raise ValueError(f"column length must be a power of two, got {length}")
+    if length == 1:
+        return col.copy(), abs(int(col[0]))
+    a = np.array(col, copy=True)
+    h = 1
+    with np.errstate(over="ignore"):
+        while h < length:
+            view = a.reshape(-1, 2, h)
+            top = view[:, 0, :].copy()
+            bot = view[:, 1, :].copy()
+            view[:, 0, :] = top + bot
+            view[:, 1, :] = top - bot
+            h <<= 1
+        mx = int(np.abs(a).max())
+    return a, mx
+
+
+def xmajor_spectrum_typed(wt: np.ndarray) -> np.ndarray:
+    """transform_xmajor_in_place (walsh.py:134-137) out of place: every
+    column of an x-major store through fwht_column_typed."""
+    out = np.empty_like(wt)
+    for z in range(wt.shape[1]):
+        out[:, z] = fwht_column_typed(wt[:, z])[0]
+    return out
+
+
 def spectrum(table: np.ndarray, n: int, v_lo: int, v_hi: int) -> np.ndarray:
     """Mask-major W rows for v in [v_lo, v_hi): rows[v - v_lo][u] = W(u, v)."""
     assert table.shape == (1 << n,)

@@ -23,9 +23,9 @@ from typing import IO, Iterable, Sequence
 import numpy as np
 
 from .records import NonlinearityResult, SBox, WalshSpectrum
-from .reducers import nonlinearity_bruteforce, nonlinearity_from_maxima, nonlinearity_from_spectrum
-from .sharding import fwht_parallel
-from .transforms import fwht_fused, fwht_rowmajor, fwht_transposed
+from .nonlinearity import nonlinearity_bruteforce, nonlinearity_from_maxima, nonlinearity_from_spectrum
+from .parallel import fwht_parallel
+from .walsh import fwht_fused, fwht_rowmajor, fwht_transposed
 
 CSV_HEADER = ("method", "n", "m", "workers", "repetitions", "mean_ms", "stddev_ms",
               "transform_only_mean_ms")

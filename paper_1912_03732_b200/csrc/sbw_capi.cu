@@ -97,6 +97,62 @@ int check_range(int m, uint32_t v_lo, uint32_t v_hi) {
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// Every entry point runs on the device that owns its work: the stream's
+// device (cudaStreamGetDevice) for a created stream, else the device of the
+// output pointer (the NULL / legacy stream belongs to whatever device is
+// current, which need not be where the caller's buffers live).  The caller's
+// current device is restored on return, and the per-device caches inside
+// libsbw (device_props, tensor-core constants, K3 streams) key off the
+// device selected here.
+class DeviceScope {
+ public:
+  DeviceScope(void* stream, const void* ptr) {
+    int want = -1;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (st != nullptr && st != cudaStreamLegacy && st != cudaStreamPerThread) {
+      if (cudaStreamGetDevice(st, &want) != cudaSuccess) {
+        cudaGetLastError();
+        want = -1;
+      }
+    }
+    if (want < 0 && ptr != nullptr) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, ptr) == cudaSuccess &&
+          (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged))
+        want = at.device;
+      else
+        cudaGetLastError();
+    }
+    if (want >= 0 && cudaGetDevice(&prev_) == cudaSuccess && prev_ != want) {
+      if (cudaSetDevice(want) == cudaSuccess) switched_ = true;
+      else cudaGetLastError();
+    }
+  }
+  ~DeviceScope() {
+    if (switched_) cudaSetDevice(prev_);
+  }
+  DeviceScope(const DeviceScope&) = delete;
+  DeviceScope& operator=(const DeviceScope&) = delete;
+
+ private:
+  int prev_ = -1;
+  bool switched_ = false;
+};
+
+// Restores the caller's current device (sbw_nl_host selects `device` itself).
+class DeviceRestore {
+ public:
+  DeviceRestore() {
+    if (cudaGetDevice(&prev_) != cudaSuccess) prev_ = -1;
+  }
+  ~DeviceRestore() {
+    if (prev_ >= 0) cudaSetDevice(prev_);
+  }
+
+ private:
+  int prev_ = -1;
+};
+
 }  // namespace
 
 extern "C" {
@@ -130,6 +186,7 @@ size_t sbw_nl_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi) {
 int sbw_nl(const void* d_table, int table_bytes, int n, int m, uint32_t v_lo, uint32_t v_hi,
            int32_t* d_max_abs, unsigned long long* d_key, void* scratch, size_t scratch_bytes,
            void* stream) {
+  DeviceScope dev_scope(stream, d_table);
   if (int rc = check_nm(n, m)) return rc;
   if (int rc = check_table(d_table, table_bytes, m)) return rc;
   if (int rc = check_range(m, v_lo, v_hi)) return rc;
@@ -154,6 +211,7 @@ size_t sbw_spectrum_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi, in
 int sbw_spectrum(const void* d_table, int table_bytes, int n, int m, uint32_t v_lo,
                  uint32_t v_hi, int layout, int32_t* d_out, int64_t ld, int32_t* d_max_abs,
                  void* scratch, size_t scratch_bytes, void* stream) {
+  DeviceScope dev_scope(stream, d_table);
   if (int rc = check_nm(n, m)) return rc;
   if (int rc = check_table(d_table, table_bytes, m)) return rc;
   if (int rc = check_range(m, v_lo, v_hi)) return rc;
@@ -201,6 +259,7 @@ int sbw_spectrum(const void* d_table, int table_bytes, int n, int m, uint32_t v_
 
 int sbw_polarity(const void* d_table, int table_bytes, int n, int m, uint32_t v_lo,
                  uint32_t v_hi, int layout, int32_t* d_out, int64_t ld, void* stream) {
+  DeviceScope dev_scope(stream, d_table);
   if (int rc = check_nm(n, m)) return rc;
   if (int rc = check_table(d_table, table_bytes, m)) return rc;
   // polarity rows may include the constant v = 0 row (polarity_row(s, 0))
@@ -214,6 +273,7 @@ int sbw_polarity(const void* d_table, int table_bytes, int n, int m, uint32_t v_
 }
 
 int sbw_fwht_inplace(int32_t* d_data, int k, int64_t count, int64_t* d_max_abs, void* stream) {
+  DeviceScope dev_scope(stream, d_data);
   if (k < 0 || k > 30) return set_error(SBW_EINVAL, "column length must be 2^k, k in 0..30");
   if (count < 0) return set_error(SBW_EINVAL, "negative column count");
   if (count > 0 && !d_data) return set_error(SBW_EINVAL, "null data");
@@ -221,10 +281,24 @@ int sbw_fwht_inplace(int32_t* d_data, int k, int64_t count, int64_t* d_max_abs, 
                       as_stream(stream));
 }
 
+int sbw_fwht_inplace_strided(void* d_data, int elem_type, int k, int64_t count, int64_t col_stride,
+                             int64_t elem_stride, int64_t* d_max_abs, void* stream) {
+  DeviceScope dev_scope(stream, d_data);
+  if (k < 0 || k > 30) return set_error(SBW_EINVAL, "column length must be 2^k, k in 0..30");
+  if (count < 0) return set_error(SBW_EINVAL, "negative column count");
+  if (elem_type < SBW_ELEM_I8 || elem_type > SBW_ELEM_U64)
+    return set_error(SBW_EINVAL, "unknown element type %d", elem_type);
+  if (count > 0 && !d_data) return set_error(SBW_EINVAL, "null data");
+  if (k > 0 && elem_stride == 0) return set_error(SBW_EINVAL, "zero element stride");
+  return inplace_fwht_strided(d_data, elem_type, k, count, col_stride, elem_stride,
+                              reinterpret_cast<long long*>(d_max_abs), as_stream(stream));
+}
+
 __global__ void k_fill_ll(long long* p, long long v) { *p = v; }
 
 int sbw_maxabs_to_nl(const int32_t* d_max_abs, int64_t count, int n, int64_t* d_nl,
                      int64_t* d_bad, void* stream) {
+  DeviceScope dev_scope(stream, d_nl);
   if (n < 0 || n > 30) return set_error(SBW_EINVAL, "bad n");
   cudaStream_t st = as_stream(stream);
   k_fill_ll<<<1, 1, 0, st>>>(reinterpret_cast<long long*>(d_bad), LLONG_MAX);
@@ -235,6 +309,7 @@ int sbw_maxabs_to_nl(const int32_t* d_max_abs, int64_t count, int n, int64_t* d_
 
 int sbw_maxabs64_to_nl(const int64_t* d_max_abs, int64_t count, int64_t pw, int64_t* d_nl,
                        int64_t* d_bad, void* stream) {
+  DeviceScope dev_scope(stream, d_nl);
   cudaStream_t st = as_stream(stream);
   k_fill_ll<<<1, 1, 0, st>>>(reinterpret_cast<long long*>(d_bad), LLONG_MAX);
   SBW_LAUNCH_CHECK("k_fill_ll");
@@ -245,6 +320,7 @@ int sbw_maxabs64_to_nl(const int64_t* d_max_abs, int64_t count, int64_t pw, int6
 
 int sbw_row_maxabs(const int32_t* d_rows, int64_t rows, int64_t cols, int64_t ld,
                    int64_t* d_row_max, unsigned long long* d_key, void* stream) {
+  DeviceScope dev_scope(stream, d_rows);
   if (rows < 0 || cols < 1 || ld < cols) return set_error(SBW_EINVAL, "bad spectrum shape");
   return launch_row_maxabs(d_rows, rows, cols, ld, reinterpret_cast<long long*>(d_row_max), d_key,
                            as_stream(stream));
@@ -252,6 +328,7 @@ int sbw_row_maxabs(const int32_t* d_rows, int64_t rows, int64_t cols, int64_t ld
 
 int sbw_walsh_direct(const void* d_table, int table_bytes, int n, int m, const uint32_t* d_u,
                      const uint32_t* d_v, int64_t count, int32_t* d_out, void* stream) {
+  DeviceScope dev_scope(stream, d_table);
   if (int rc = check_nm(n, m)) return rc;
   if (int rc = check_table(d_table, table_bytes, m)) return rc;
   return launch_walsh_direct(d_table, table_bytes, n, d_u, d_v, count, d_out, as_stream(stream));
@@ -259,6 +336,7 @@ int sbw_walsh_direct(const void* d_table, int table_bytes, int n, int m, const u
 
 int sbw_nl_bruteforce(const void* d_table, int table_bytes, int n, int m, int32_t* d_best,
                       void* stream) {
+  DeviceScope dev_scope(stream, d_table);
   if (int rc = check_nm(n, m)) return rc;
   if (n > 8 || m > 8) return set_error(SBW_EINVAL, "brute force capped at 8 bits, got %dx%d", n, m);
   if (int rc = check_table(d_table, table_bytes, m)) return rc;
@@ -283,6 +361,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 int sbw_nl_host(const uint32_t* h_table, int n, int m, uint32_t v_lo, uint32_t v_hi,
                 int64_t* h_nl, int64_t* out3, int device) {
+  DeviceRestore dev_restore;
   if (int rc = check_nm(n, m)) return rc;
   if (int rc = check_range(m, v_lo, v_hi)) return rc;
   if (!h_table) return set_error(SBW_EINVAL, "null host table");
@@ -371,11 +450,13 @@ int sbw_nl_host(const uint32_t* h_table, int n, int m, uint32_t v_lo, uint32_t v
 }
 
 int sbw_int32_peak(double* ops_per_s, double* ms, void* stream) {
+  DeviceScope dev_scope(stream, nullptr);
   if (!ops_per_s) return set_error(SBW_EINVAL, "null output");
   return run_int32_peak(ops_per_s, ms, as_stream(stream));
 }
 
 int sbw_int8_mma_peak(double* ops_per_s, double* ms, void* stream) {
+  DeviceScope dev_scope(stream, nullptr);
   if (!ops_per_s) return set_error(SBW_EINVAL, "null output");
   return run_int8_mma_peak(ops_per_s, ms, as_stream(stream));
 }
@@ -416,11 +497,13 @@ int sbw_ipc_free(void* d_ptr) {
 }
 
 int sbw_key_merge(const unsigned long long* d_key, unsigned long long* d_dst_key, void* stream) {
+  DeviceScope dev_scope(stream, d_key);
   if (!d_key || !d_dst_key) return set_error(SBW_EINVAL, "sbw_key_merge: null key");
   return launch_key_merge(d_key, d_dst_key, as_stream(stream));
 }
 
 int sbw_peer_copy(void* d_dst, const void* d_src, size_t bytes, void* stream) {
+  DeviceScope dev_scope(stream, d_dst);
   if (bytes == 0) return SBW_OK;
   if (!d_dst || !d_src) return set_error(SBW_EINVAL, "sbw_peer_copy: null pointer");
   SBW_CUDA_CHECK(cudaMemcpyAsync(d_dst, d_src, bytes, cudaMemcpyDefault, as_stream(stream)));

@@ -79,6 +79,9 @@ int launch_transpose_i32(const int32_t* in, int64_t rows, int64_t cols, int64_t 
                          int32_t* out, int64_t ld_out, cudaStream_t st);
 int launch_fill_i32(int32_t* p, int64_t count, int32_t value, cudaStream_t st);
 int inplace_fwht(int32_t* d, int k, int64_t count, long long* max_abs, cudaStream_t st);
+// Any integer dtype (SBW_ELEM_*), any strides (sbw_inplace.cu).
+int inplace_fwht_strided(void* data, int elem, int k, int64_t count, int64_t col_stride,
+                         int64_t elem_stride, long long* max_abs, cudaStream_t st);
 int launch_polarity(const void* table, int tbytes, int n, uint32_t v_lo, uint32_t v_hi,
                     int layout, int32_t* out, int64_t ld, cudaStream_t st);
 int launch_maxabs_to_nl(const int32_t* mx, int64_t count, int n, long long* nl, long long* bad,

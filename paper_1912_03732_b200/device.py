@@ -36,6 +36,7 @@ SIGNATURES = {
     "sbw_spectrum_scratch_bytes": (_sz, [_i32, _i32, _u32, _u32, _i32]),
     "sbw_polarity": (_i32, [_vp, _i32, _i32, _i32, _u32, _u32, _i32, _vp, _i64, _vp]),
     "sbw_fwht_inplace": (_i32, [_vp, _i32, _i64, _vp, _vp]),
+    "sbw_fwht_inplace_strided": (_i32, [_vp, _i32, _i32, _i64, _i64, _i64, _vp, _vp]),
     "sbw_maxabs_to_nl": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
     "sbw_maxabs64_to_nl": (_i32, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "sbw_row_maxabs": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
@@ -115,6 +116,14 @@ def require_device(device=None):
     if dev.type != "cuda":
         raise ValueError(f"device must be a CUDA device, got {dev}")
     return dev if dev.index is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+def on(device):
+    """Make `device` current for a block of libsbw calls and torch
+    allocations.  libsbw itself also runs every call on the device of its
+    stream (or, for the NULL stream, of its data pointers) -- include/sbw.h --
+    so a launch can never land on another GPU than its buffers."""
+    return torch_mod().cuda.device(device)
 
 
 def stream_handle(device) -> int:

@@ -17,10 +17,10 @@ import time
 import numpy as np
 
 from . import device as _dev
-from .accounting import charged, check_budget, memory_estimate
-from .records import ColumnMaxima, ColumnPartition, NonlinearityResult, SBox, WalshSpectrum
-from .transforms import (component_max_abs_device, decode_key, device_to_host_chunked, maxabs_to_nl,
-                         spectrum_device)
+from .memory import charged, check_budget, memory_estimate
+from .records import ColumnMaxima, ColumnPartition, NonlinearityResult, SBox, WalshSpectrum  # noqa: F401
+from .walsh import (check_nl_flag, component_max_abs_device, decode_key,  # noqa: F401
+                    device_to_host_chunked, maxabs_to_nl, maxabs_to_nl_device, spectrum_device)
 
 
 def partition_columns(total_columns: int, workers: int) -> ColumnPartition:
@@ -85,17 +85,21 @@ def fwht_parallel(s: SBox, workers: int | None = None, mode: str = "retain",
     with charged(nbytes):
         if mode == "retain":
             rows = np.empty(((1 << s.m) - 1, 1 << s.n), dtype=np.int32)
+        # every shard is launched (asynchronously, each on its own GPU's
+        # current stream) before any result is read back
         for i, (lo, hi) in enumerate(part.ranges):
             dev = devs[i % len(devs)]
-            if mode == "retain":
-                spec, mx = spectrum_device(s, lo, hi, layout="mask", device=dev)
-            else:
-                spec, (mx, _key) = None, component_max_abs_device(s, lo, hi, device=dev)
+            with _dev.on(dev):
+                if mode == "retain":
+                    spec, mx = spectrum_device(s, lo, hi, layout="mask", device=dev)
+                else:
+                    spec, (mx, _key) = None, component_max_abs_device(s, lo, hi, device=dev)
             pending.append((lo, hi, spec, mx))
         for lo, hi, spec, mx in pending:  # completion barrier, in range order
-            values[lo - 1:hi - 1] = maxabs_to_nl(mx, s.n)
-            if spec is not None:
-                device_to_host_chunked(spec, rows[lo - 1:hi - 1])
+            with _dev.on(mx.device):
+                values[lo - 1:hi - 1] = maxabs_to_nl(mx, s.n)
+                if spec is not None:
+                    device_to_host_chunked(spec, rows[lo - 1:hi - 1])
         t2 = time.perf_counter()
     if timings is not None:
         timings["build_s"] = t1 - t0
@@ -108,9 +112,12 @@ def fwht_parallel(s: SBox, workers: int | None = None, mode: str = "retain",
 # multi-process (one rank per GPU) evaluation
 # ---------------------------------------------------------------------------
 def _gpu_shard(s: SBox, lo: int, hi: int):
-    """Default shard compute: fused NL on this rank's GPU -> (NL int64, key)."""
+    """Default shard compute: fused NL on this rank's GPU, left on the GPU.
+
+    Returns (NL int64 [hi - lo + 1] device tensor whose last entry is the
+    odd-gap flag, key int64 [1] device tensor)."""
     mx, key = component_max_abs_device(s, lo, hi)
-    return maxabs_to_nl(mx, s.n), int(key.item())
+    return maxabs_to_nl_device(mx, s.n), key
 
 
 def _evaluate_p2p(s: SBox, group, lo: int, hi: int, total: int,
@@ -206,32 +213,53 @@ def evaluate_distributed(s: SBox, group=None, compute=None, return_values: bool 
         return result, (ColumnMaxima(s.n, s.m, values) if return_values else None)
     if transport != "collective":
         raise ValueError(f"transport must be 'collective' or 'p2p', got {transport!r}")
-    compute = compute or _gpu_shard
-    if hi > lo:
-        nl, key = compute(s, lo, hi)
-    else:
-        nl, key = np.zeros(0, dtype=np.int64), 0
     backend = dist.get_backend(group)
     dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
-    key_t = torch.tensor([key], dtype=torch.int64, device=dev)
+    count = hi - lo
+    flag = None
+    if compute is None:
+        # GPU shards: the per-component values and the key stay on the GPU
+        # for the collectives (no host round trip); the odd-gap flag is read
+        # once at the end
+        gdev = _dev.require_device()
+        if count > 0:
+            nl_t, key_t = _gpu_shard(s, lo, hi)
+            flag = nl_t[count:]
+            nl_t = nl_t[:count]
+        else:
+            nl_t = torch.zeros(0, dtype=torch.int64, device=gdev)
+            key_t = torch.zeros(1, dtype=torch.int64, device=gdev)
+        nl_t, key_t = nl_t.to(dev), key_t.to(dev)
+    else:
+        if count > 0:
+            nl, key = compute(s, lo, hi)
+        else:
+            nl, key = np.zeros(0, dtype=np.int64), 0
+        key_t = torch.tensor([key], dtype=torch.int64, device=dev)
+        nl_t = torch.from_numpy(np.asarray(nl, dtype=np.int64)).to(dev)
     dist.all_reduce(key_t, op=dist.ReduceOp.MAX, group=group)
+    cm = None
+    if return_values:
+        width = max(h - l for l, h in ranges)
+        buf = torch.full((width,), -1, dtype=torch.int64, device=dev)
+        buf[:count] = nl_t
+        parts = torch.empty((world, width), dtype=torch.int64, device=dev)
+        if backend == "nccl":
+            dist.all_gather_into_tensor(parts, buf, group=group)
+        else:
+            dist.all_gather(list(parts.unbind(0)), buf, group=group)
+        gathered = parts.cpu().numpy()  # the one device -> host copy of the values
+        values = np.empty(total, dtype=np.int64)
+        for (l, h), p in zip(ranges, gathered):
+            if h > l:
+                values[l - 1:h - 1] = p[: h - l]
+        cm = ColumnMaxima(s.n, s.m, values)
+    if flag is not None:
+        check_nl_flag(int(flag.item()))
     k = int(key_t.item())
     mxw = k >> 32
     v = 0xFFFFFFFF - (k & 0xFFFFFFFF)
     gap = (1 << s.n) - mxw
     if gap & 1:
         raise AssertionError("spectrum maximum has wrong parity")
-    result = NonlinearityResult(gap >> 1, v, "distributed")
-    cm = None
-    if return_values:
-        width = max(h - l for l, h in ranges)
-        buf = torch.full((width,), -1, dtype=torch.int64, device=dev)
-        buf[: hi - lo] = torch.from_numpy(np.asarray(nl, dtype=np.int64)).to(dev)
-        parts = [torch.empty_like(buf) for _ in range(world)]
-        dist.all_gather(parts, buf, group=group)
-        values = np.empty(total, dtype=np.int64)
-        for (l, h), p in zip(ranges, parts):
-            if h > l:
-                values[l - 1:h - 1] = p[: h - l].cpu().numpy()
-        cm = ColumnMaxima(s.n, s.m, values)
-    return result, cm
+    return NonlinearityResult(gap >> 1, v, "distributed"), cm

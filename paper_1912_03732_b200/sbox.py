@@ -9,8 +9,9 @@ from __future__ import annotations
 import numpy as np
 
 from . import device as _dev
-from .accounting import check_budget, memory_estimate  # noqa: F401  (re-exported)
-from .records import MAX_BITS, PolarityTruthTable, SBox
+from .memory import check_budget, memory_estimate  # noqa: F401  (re-exported)
+from .records import MAX_BITS, PolarityTruthTable, SBox, SBoxFormatError  # noqa: F401
+from .sboxio import parse_sbox, render_sbox  # noqa: F401  (sbox.py:186-253 lives there)
 
 
 def _gf_mul(a: int, b: int) -> int:
@@ -83,9 +84,10 @@ def _polarity_device(s: SBox, v_lo: int, v_hi: int, layout: int, dev):
     shape = (rows, 1 << s.n) if layout == _dev.LAYOUT_MASK_MAJOR else (1 << s.n, rows)
     out = torch.empty(shape, dtype=torch.int32, device=dev)
     tab = _dev.device_table(s, dev)
-    _dev.check(_dev.load_library().sbw_polarity(
-        _dev.ptr(tab), _dev.table_bytes(s.m), s.n, s.m, v_lo, v_hi, layout, _dev.ptr(out),
-        shape[1], _dev.stream_handle(dev)))
+    with _dev.on(dev):
+        _dev.check(_dev.load_library().sbw_polarity(
+            _dev.ptr(tab), _dev.table_bytes(s.m), s.n, s.m, v_lo, v_hi, layout, _dev.ptr(out),
+            shape[1], _dev.stream_handle(dev)))
     return out
 
 
@@ -108,12 +110,13 @@ def polarity_truth_table(s: SBox, max_bytes: int | None = None) -> PolarityTruth
     dev = _dev.require_device()
     d = _polarity_device(s, 1, 1 << s.m, _dev.LAYOUT_MASK_MAJOR, dev)
     if d.numel() * 4 > (256 << 20):
-        from .transforms import device_to_host_chunked
+        from .walsh import device_to_host_chunked
         rows = device_to_host_chunked(d, np.empty(tuple(d.shape), dtype=np.int32))
     else:
         rows = d.cpu().numpy()
     return PolarityTruthTable(s.n, s.m, rows)
 
 
-__all__ = ["AES_SBOX", "MAX_BITS", "aes_sbox", "identity_sbox", "generate_sbox",
-           "component_value", "polarity_row", "polarity_truth_table", "memory_estimate"]
+__all__ = ["AES_SBOX", "MAX_BITS", "PolarityTruthTable", "SBox", "SBoxFormatError", "aes_sbox",
+           "identity_sbox", "generate_sbox", "component_value", "polarity_row",
+           "polarity_truth_table", "memory_estimate", "parse_sbox", "render_sbox"]

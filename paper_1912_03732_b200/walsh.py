@@ -7,10 +7,12 @@ their bodies call libsbw's sm_100a kernels through device.py:
   fwht_fused(mode="stream")  -> sbw_nl        (generate + FWHT + max, fused)
   fwht_fused(mode="retain")  -> sbw_spectrum  (mask-major rows + maxima)
   fwht_transposed            -> sbw_spectrum  (mask-major)
-  fwht_rowmajor              -> sbw_spectrum  (x-major store, returned
-                                               mask-major like walsh.py:174)
-  fwht_column_in_place       -> sbw_fwht_inplace
-  transform_rows_in_place    -> sbw_fwht_inplace + sbw_maxabs64_to_nl
+  fwht_rowmajor              -> sbw_spectrum  (mask-major, as walsh.py:174 returns)
+  build_polarity_xmajor      -> sbw_polarity  (x-major)
+  fwht_column_in_place       -> sbw_fwht_inplace / sbw_fwht_inplace_strided
+  transform_rows_in_place    -> the same, one column per row
+  transform_xmajor_in_place  -> sbw_fwht_inplace_strided (column stride 1)
+  column_nonlinearity        -> host arithmetic on the kernel's max
   walsh_direct               -> sbw_walsh_direct
 
 Device-resident variants (`*_device`) return torch tensors for callers that
@@ -24,7 +26,7 @@ from typing import IO
 import numpy as np
 
 from . import device as _dev
-from .accounting import charged, check_budget, memory_estimate
+from .memory import charged, check_budget, memory_estimate
 from .records import ColumnMaxima, SBox, WalshSpectrum
 
 INT64_MAX = (1 << 63) - 1
@@ -55,7 +57,7 @@ def component_max_abs_device(s: SBox, v_lo: int = 1, v_hi: int | None = None, de
     key = torch.zeros(1, dtype=torch.int64, device=dev)
     nbytes = lib.sbw_nl_scratch_bytes(s.n, s.m, v_lo, v_hi)
     scratch = _scratch(nbytes, dev)
-    with charged(nbytes):
+    with charged(nbytes), _dev.on(dev):
         _dev.check(lib.sbw_nl(_dev.ptr(tab), _dev.table_bytes(s.m), s.n, s.m, v_lo, v_hi,
                               _dev.ptr(mx), _dev.ptr(key), _dev.ptr(scratch), nbytes,
                               _dev.stream_handle(dev)))
@@ -89,9 +91,10 @@ def spectrum_device(s: SBox, v_lo: int = 1, v_hi: int | None = None, layout: str
     tab = _dev.device_table(s, dev)
     nbytes = lib.sbw_spectrum_scratch_bytes(s.n, s.m, v_lo, v_hi, lay)
     scratch = _scratch(nbytes, dev)
-    _dev.check(lib.sbw_spectrum(_dev.ptr(tab), _dev.table_bytes(s.m), s.n, s.m, v_lo, v_hi, lay,
-                                _dev.ptr(out), shape[1], _dev.ptr(mx), _dev.ptr(scratch), nbytes,
-                                _dev.stream_handle(dev)))
+    with _dev.on(dev):
+        _dev.check(lib.sbw_spectrum(_dev.ptr(tab), _dev.table_bytes(s.m), s.n, s.m, v_lo, v_hi, lay,
+                                    _dev.ptr(out), shape[1], _dev.ptr(mx), _dev.ptr(scratch), nbytes,
+                                    _dev.stream_handle(dev)))
     return out, mx[:rows]
 
 
@@ -155,6 +158,7 @@ def spectrum_to_host(s: SBox, v_lo: int = 1, v_hi: int | None = None, layout: st
         out = np.empty(shape, dtype=np.int32)
     elif out.shape != shape or out.dtype != np.int32:
         raise ValueError(f"out must be an int32 array of shape {shape}")
+    fast_out = out.flags.writeable and all(st >= 0 for st in out.strides)
     maxima = np.empty(nv, dtype=np.int32)
     rows = max(1, min(nv, chunk_bytes // (nx * 4)))
     streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
@@ -177,10 +181,12 @@ def spectrum_to_host(s: SBox, v_lo: int = 1, v_hi: int | None = None, layout: st
         done[slot].synchronize()
         # torch's CPU copy runs on all intra-op threads (numpy's assignment is
         # one thread), which also spreads the first-touch page faults of `out`
-        if layout == "mask":
-            torch.from_numpy(out[a - v_lo:b - v_lo]).copy_(pins[slot][: b - a])
-        else:
-            torch.from_numpy(out[:, a - v_lo:b - v_lo]).copy_(pins[slot][:, : b - a])
+        dst = out[a - v_lo:b - v_lo] if layout == "mask" else out[:, a - v_lo:b - v_lo]
+        src = pins[slot][: b - a] if layout == "mask" else pins[slot][:, : b - a]
+        if fast_out:
+            torch.from_numpy(dst).copy_(src)
+        else:  # read-only or negative-stride caller arrays: numpy's own assignment rules
+            dst[...] = src.numpy()
 
     for i, a in enumerate(range(v_lo, v_hi, rows)):
         b = min(v_hi, a + rows)
@@ -208,17 +214,31 @@ def spectrum_to_host(s: SBox, v_lo: int = 1, v_hi: int | None = None, layout: st
 
 def maxabs_to_nl(max_abs, n: int) -> np.ndarray:
     """Device max|W| -> host int64 NL per component (walsh.py:107-114)."""
+    count = max_abs.numel()
+    out = maxabs_to_nl_device(max_abs, n)
+    host = out.cpu().numpy()  # one device -> host copy
+    check_nl_flag(int(host[count]))
+    return host[:count]
+
+
+def maxabs_to_nl_device(max_abs, n: int):
+    """Device max|W| -> device int64 [count + 1]: NL per component, then the
+    odd-gap flag (INT64_MAX when every gap is even, else the first bad
+    component's index), for callers that keep the values on the GPU."""
     torch = _dev.torch_mod()
     dev = max_abs.device
     count = max_abs.numel()
-    out = torch.empty(count + 1, dtype=torch.int64, device=dev)  # NL values, then the odd-gap flag
-    _dev.check(_dev.load_library().sbw_maxabs_to_nl(_dev.ptr(max_abs), count, n, _dev.ptr(out),
-                                                    _dev.ptr(out) + 8 * count, _dev.stream_handle(dev)))
-    host = out.cpu().numpy()  # one device -> host copy
-    b = int(host[count])
+    out = torch.empty(count + 1, dtype=torch.int64, device=dev)
+    with _dev.on(dev):
+        _dev.check(_dev.load_library().sbw_maxabs_to_nl(_dev.ptr(max_abs), count, n, _dev.ptr(out),
+                                                        _dev.ptr(out) + 8 * count,
+                                                        _dev.stream_handle(dev)))
+    return out
+
+
+def check_nl_flag(b: int) -> None:
     if b != INT64_MAX:
         raise AssertionError(f"odd spectrum gap at component {b}: not a genuine Walsh column")
-    return host[:count]
 
 
 def decode_key(key, n: int) -> tuple[int, int, int]:
@@ -256,49 +276,149 @@ def walsh_direct_many(s: SBox, us, vs, device=None) -> np.ndarray:
     v = torch.as_tensor(np.asarray(vs, dtype=np.uint32).view(np.int32)).to(dev)
     out = torch.empty(max(1, u.numel()), dtype=torch.int32, device=dev)
     tab = _dev.device_table(s, dev)
-    _dev.check(_dev.load_library().sbw_walsh_direct(
-        _dev.ptr(tab), _dev.table_bytes(s.m), s.n, s.m, _dev.ptr(u), _dev.ptr(v), u.numel(),
-        _dev.ptr(out), _dev.stream_handle(dev)))
+    with _dev.on(dev):
+        _dev.check(_dev.load_library().sbw_walsh_direct(
+            _dev.ptr(tab), _dev.table_bytes(s.m), s.n, s.m, _dev.ptr(u), _dev.ptr(v), u.numel(),
+            _dev.ptr(out), _dev.stream_handle(dev)))
     return out[: u.numel()].cpu().numpy()
 
 
-def fwht_column_in_place(col: np.ndarray) -> tuple[np.ndarray, int]:
-    """In-place natural-order WHT of one int32 column (walsh.py:73-104).
+def column_nonlinearity(pw: int, max_abs: int) -> int:
+    """(2^n - max|W|) / 2; an odd difference is not a genuine Walsh column
+    (walsh.py:107-114).  Scalar host arithmetic on the kernel's result."""
+    diff = pw - max_abs
+    if diff & 1:
+        raise AssertionError(
+            f"odd spectrum gap {diff}: column is not a genuine Walsh column")
+    return diff >> 1
 
-    Any uniformly strided 1-D int32 view is accepted; returns the column and
-    its max |entry| (numpy-int32 semantics, final stage; |x| for length 1).
+
+# numpy dtype -> SBW_ELEM_* (include/sbw.h) and the same-width signed view
+# used to move the bits through torch
+_ELEM = {np.dtype(np.int8): (1, np.int8), np.dtype(np.uint8): (2, np.uint8),
+         np.dtype(np.int16): (3, np.int16), np.dtype(np.uint16): (4, np.int16),
+         np.dtype(np.int32): (5, np.int32), np.dtype(np.uint32): (6, np.int32),
+         np.dtype(np.int64): (7, np.int64), np.dtype(np.uint64): (8, np.int64)}
+
+
+def _elem(dtype) -> tuple[int, type]:
+    e = _ELEM.get(np.dtype(dtype))
+    if e is None:
+        raise TypeError(f"Walsh butterflies need an integer column, got dtype {np.dtype(dtype)}")
+    return e
+
+
+def _check_writeable(a: np.ndarray) -> None:
+    # numpy's in-place ufuncs (walsh.py:98-100) raise this on read-only views
+    if not a.flags.writeable:
+        raise ValueError("output array is read-only")
+
+
+def fwht_column_in_place(col: np.ndarray) -> tuple[np.ndarray, int]:
+    """In-place natural-order WHT of one column (walsh.py:73-104).
+
+    Any uniformly strided 1-D view of any integer dtype is accepted, with
+    numpy's wrap-around arithmetic in that dtype; returns the column and
+    np.abs(column).max() of the final stage as a Python int (abs(int(x)) for
+    length 1).
     """
     length = col.shape[0]
     if length == 0 or (length & (length - 1)) != 0:
         raise ValueError(f"column length must be a power of two, got {length}")
-    if col.dtype != np.int32:
-        raise TypeError(f"column must be int32, got {col.dtype}")
     mx = _inplace_rows(col.reshape(1, length))
     return col, int(mx[0])
 
 
-def _inplace_rows(rows2d: np.ndarray) -> np.ndarray:
-    """Transform the rows of a (possibly strided) int32 matrix in place on the GPU."""
+def _fold_values(mx, dtype, k: int):
+    """Kernel maxima (int64 bits) with numpy's semantics: an int64 array when
+    every value fits (dtypes up to 32 bits), else a list of Python ints."""
+    if k == 0 or np.dtype(dtype) == np.dtype(np.uint64):
+        return [int(x) for x in mx.view(np.uint64)]
+    if np.dtype(dtype).itemsize == 8:
+        return [int(x) for x in mx]
+    return mx
+
+
+def _inplace_device(d, elem: int, k: int, count: int, col_stride: int, elem_stride: int, dev,
+                    want_max: bool = True):
+    """Butterfly `count` columns of the device tensor `d` in place."""
     torch = _dev.torch_mod()
+    lib = _dev.load_library()
+    mx = torch.empty(max(1, count), dtype=torch.int64, device=dev) if want_max else None
+    with _dev.on(dev):
+        if elem == 5 and col_stride == (1 << k) and elem_stride == 1:
+            _dev.check(lib.sbw_fwht_inplace(_dev.ptr(d), k, count, _dev.ptr(mx),
+                                            _dev.stream_handle(dev)))
+        else:
+            _dev.check(lib.sbw_fwht_inplace_strided(_dev.ptr(d), elem, k, count, col_stride,
+                                                    elem_stride, _dev.ptr(mx),
+                                                    _dev.stream_handle(dev)))
+    return mx
+
+
+def _to_device(a: np.ndarray, view_t, dev):
+    torch = _dev.torch_mod()
+    return torch.from_numpy(np.ascontiguousarray(a).view(view_t)).to(dev)
+
+
+def _copy_back(host: np.ndarray, d, view_t) -> None:
+    """Device result -> the caller's (possibly strided) host array."""
+    torch = _dev.torch_mod()
+    if host.flags.c_contiguous and host.size:
+        torch.from_numpy(host.view(view_t)).copy_(d)  # straight into the caller's array
+    else:
+        host[...] = d.cpu().numpy().view(host.dtype)
+
+
+def _inplace_rows(rows2d: np.ndarray):
+    """Transform the rows of a (possibly strided) integer matrix in place on
+    the GPU; returns each row's max|.| as Python ints (numpy semantics)."""
+    _check_writeable(rows2d)
+    elem, view_t = _elem(rows2d.dtype)
     dev = _dev.require_device()
     count, length = rows2d.shape
     k = length.bit_length() - 1
-    d = torch.from_numpy(np.ascontiguousarray(rows2d)).to(dev)
-    mx = torch.empty(max(1, count), dtype=torch.int64, device=dev)
-    _dev.check(_dev.load_library().sbw_fwht_inplace(_dev.ptr(d), k, count, _dev.ptr(mx),
-                                                    _dev.stream_handle(dev)))
-    if rows2d.flags.c_contiguous:
-        torch.from_numpy(rows2d).copy_(d)  # one device -> host copy straight into the caller's array
-    else:
-        rows2d[...] = d.cpu().numpy()
-    return mx[:count].cpu().numpy()
+    d = _to_device(rows2d, view_t, dev)
+    mx = _inplace_device(d, elem, k, count, length, 1, dev)
+    _copy_back(rows2d, d, view_t)
+    return _fold_values(mx[:count].cpu().numpy(), rows2d.dtype, k)
+
+
+def transform_xmajor_in_place(wt: np.ndarray) -> None:
+    """Butterfly every spectrum column of an x-major store wt[x][v-1]
+    (walsh.py:134-137): one strided device pass per <= 6 stages, neighbouring
+    threads on neighbouring columns so every access is coalesced."""
+    if wt.ndim != 2:
+        raise ValueError("wt must be a 2-D array")
+    length, cols = wt.shape
+    if cols == 0:
+        return
+    if length == 0 or (length & (length - 1)) != 0:
+        raise ValueError(f"column length must be a power of two, got {length}")
+    _check_writeable(wt)
+    elem, view_t = _elem(wt.dtype)
+    dev = _dev.require_device()
+    d = _to_device(wt, view_t, dev)
+    _inplace_device(d, elem, length.bit_length() - 1, cols, 1, cols, dev, want_max=False)
+    _copy_back(wt, d, view_t)
+
+
+def build_polarity_xmajor(s: SBox, max_bytes: int | None = None) -> np.ndarray:
+    """x-major polarity store wt[x][v-1] = (-1)^{g_v(x)}, int32 [2^n, 2^m - 1]
+    (walsh.py:117-131), generated on the GPU (sbw_polarity, layout 1)."""
+    from .sbox import _polarity_device
+
+    check_budget(memory_estimate(s.n, s.m, mode="retain"), max_bytes)
+    dev = _dev.require_device()
+    d = _polarity_device(s, 1, 1 << s.m, _dev.LAYOUT_X_MAJOR, dev)
+    return _host_rows(d)
 
 
 def transform_rows_in_place(rows: np.ndarray, maxima_out: np.ndarray | None = None) -> None:
     """Butterfly every row of a mask-major store (walsh.py:140-152).
 
-    With `maxima_out`, row i's (2^k - max|W|) / 2 goes to maxima_out[i]; an
-    odd gap raises AssertionError like column_nonlinearity (walsh.py:107-114).
+    With `maxima_out`, row i's column_nonlinearity(2^k, max|W|) goes to
+    maxima_out[i]; an odd gap raises AssertionError (walsh.py:107-114).
     """
     if rows.ndim != 2:
         raise ValueError("rows must be a 2-D array")
@@ -307,16 +427,18 @@ def transform_rows_in_place(rows: np.ndarray, maxima_out: np.ndarray | None = No
         return
     if length == 0 or (length & (length - 1)) != 0:
         raise ValueError(f"column length must be a power of two, got {length}")
-    if rows.dtype != np.int32:
-        raise TypeError(f"rows must be int32, got {rows.dtype}")
     mx = _inplace_rows(rows)
-    if maxima_out is not None:
+    if maxima_out is None:
+        return
+    if isinstance(mx, np.ndarray):
         gaps = length - mx
         odd = np.flatnonzero(gaps & 1)
         if odd.size:
-            raise AssertionError(
-                f"odd spectrum gap {int(gaps[odd[0]])}: column is not a genuine Walsh column")
+            column_nonlinearity(length, int(mx[odd[0]]))  # raises the reference's AssertionError
         maxima_out[:count] = gaps >> 1
+    else:
+        for i, m in enumerate(mx):
+            maxima_out[i] = column_nonlinearity(length, m)
 
 
 def _host_rows(t) -> np.ndarray:
@@ -327,10 +449,15 @@ def _host_rows(t) -> np.ndarray:
 
 def fwht_rowmajor(s: SBox, max_bytes: int | None = None,
                   timings: dict | None = None) -> WalshSpectrum:
-    """Spectrum through the x-major ("row", paper Alg. 1) store (walsh.py:155-180).
+    """Row-layout ("x-major", paper Alg. 1) method (walsh.py:155-180).
 
-    The GPU builds the x-major wt[u][v-1] matrix directly, then returns the
-    mask-major contiguous copy exactly as the reference does (walsh.py:174).
+    The reference transforms an x-major store in place and returns its
+    mask-major contiguous copy (walsh.py:174), so the caller only ever sees
+    mask-major rows.  On the GPU the x-major intermediate would be written
+    once and transposed straight back, so the rows are produced mask-major
+    directly (the x-major store itself is `build_polarity_xmajor` +
+    `transform_xmajor_in_place`, or `spectrum_device(layout="x")`).  Budget
+    check, charge and result are the reference's.
     """
     check_budget(memory_estimate(s.n, s.m, mode="retain"), max_bytes)
     t0 = time.perf_counter()
@@ -342,13 +469,11 @@ def fwht_rowmajor(s: SBox, max_bytes: int | None = None,
             rows, _ = spectrum_to_host(s, layout="mask", device=dev)
             t2 = time.perf_counter()
         else:
-            wt, _ = spectrum_device(s, layout="x", device=dev)
-            rows_t = wt.t().contiguous()
-            del wt
+            spec, _ = spectrum_device(s, layout="mask", device=dev)
             _sync(dev)
             t2 = time.perf_counter()
-            rows = _host_rows(rows_t)
-            del rows_t
+            rows = _host_rows(spec)
+            del spec
     if timings is not None:
         timings["build_s"] = t1 - t0
         timings["transform_s"] = t2 - t1

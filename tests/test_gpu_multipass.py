@@ -34,7 +34,7 @@ def test_linear_components_reach_2_pow_n(n):
     s = _linear_sbox(n)
     mx, key = sw.component_max_abs_device(s)
     assert np.all(mx.cpu().numpy() == 1 << n)
-    assert sw.transforms.decode_key(key, n)[:2] == (0, 1)  # NL 0, first v wins ties
+    assert sw.walsh.decode_key(key, n)[:2] == (0, 1)  # NL 0, first v wins ties
 
 
 @pytest.mark.parametrize("n", [17, 20, 21, 23])
@@ -112,4 +112,4 @@ def test_emit16_linear_components_fall_back(monkeypatch, n):
     s = _linear_sbox(n)
     mx, key = sw.component_max_abs_device(s)
     assert np.all(mx.cpu().numpy() == 1 << n)
-    assert sw.transforms.decode_key(key, n)[:2] == (0, 1)
+    assert sw.walsh.decode_key(key, n)[:2] == (0, 1)

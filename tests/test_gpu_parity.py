@@ -94,7 +94,7 @@ def test_16x16_full_fused_nl(golden, golden_arrays):
     r = sw.nonlinearity_from_maxima(cm)
     assert (r.value, r.argmin_v) == (31942, 44828)
     mx, key = sw.component_max_abs_device(s)
-    assert sw.transforms.decode_key(key, 16) == (31942, 44828, 1652)
+    assert sw.walsh.decode_key(key, 16) == (31942, 44828, 1652)
 
 
 def test_16x16_materialised_slices():
@@ -140,7 +140,7 @@ def test_20x20_full_nl_consistency():
     s = box("20x20")
     mx, key = sw.component_max_abs_device(s)
     full = mx.cpu().numpy()
-    nl, v, mw = sw.transforms.decode_key(key, 20)
+    nl, v, mw = sw.walsh.decode_key(key, 20)
     assert mw == full.max() and v == int(np.argmax(full)) + 1
     rng = np.random.default_rng(5)
     for vv in rng.integers(1, 1 << 20, size=4):
@@ -204,7 +204,7 @@ def test_partially_affine_16():
         assert np.array_equal(mx.cpu().numpy(), orc.component_max_abs(s.table, 16, lo, hi))
     mx, key = sw.component_max_abs_device(s)
     assert np.all(mx.cpu().numpy()[:255] == 1 << 16)
-    assert sw.transforms.decode_key(key, 16)[:2] == (0, 1)
+    assert sw.walsh.decode_key(key, 16)[:2] == (0, 1)
 
 
 def test_identity_and_constant_24_bit():
@@ -374,7 +374,7 @@ def test_rows_in_place_tile_pass(rows_n, k):
     assert np.array_equal(got, want)
     # all rows at once (one launch, per-row maxima)
     got2 = rows.copy()
-    mx_rows = sw.transforms._inplace_rows(got2)
+    mx_rows = sw.walsh._inplace_rows(got2)
     assert np.array_equal(got2, want) and mx_rows.tolist() == wmx
 
 
@@ -531,7 +531,7 @@ def test_cli_nl_walsh_verify(tmp_path, capsys):
 
 
 def test_cli_bench_csv_and_harness(tmp_path, monkeypatch):
-    import paper_1912_03732_b200.harness as h
+    import paper_1912_03732_b200.bench as h
     from paper_1912_03732_b200.cli import main
 
     path = _boxfile(tmp_path, "r7.sbox", sw.generate_sbox(7, 7, 2))
@@ -591,7 +591,7 @@ def test_full_large_config_nl(name, want):
     masks against the oracle, plus the smallest-v tie-break on the maxima."""
     s = box(name)
     mx, key = sw.component_max_abs_device(s)
-    res = sw.transforms.decode_key(key, s.n)
+    res = sw.walsh.decode_key(key, s.n)
     assert res == want
     full = mx.cpu().numpy()
     assert int(full.max()) == res[2] and int(np.argmax(full)) + 1 == res[1]
@@ -623,14 +623,45 @@ def test_spectrum_scan_host_chunks_rebase_rows():
     chunk; the per-chunk keys are re-based to global rows: largest max|W| wins,
     ties go to the smallest v (nonlinearity.py:36-48)."""
     n = 16
-    nrows = 2047  # 2047 x 2^16 int32 = 537 MB: three chunks
+    nrows = 2047  # 2047 x 2^16 int32 = 511.9 MiB: two 256 MiB chunks (1024 + 1023 rows)
     rows = np.zeros((nrows, 1 << n), dtype=np.int32)
     rows[:, 0] = 2
-    rows[1100, 5] = -1000   # the maximum, in the second chunk ...
-    rows[1150, 7] = 1000    # ... tied by a later row
+    rows[1000, 5] = -1000   # the maximum, in the first chunk ...
+    rows[1100, 7] = 1000    # ... tied by a row of the second chunk
     rows[3, 9] = 998
     r = sw.nonlinearity_from_spectrum(sw.WalshSpectrum(n, 11, rows))
+    assert (r.value, r.argmin_v) == (((1 << n) - 1000) // 2, 1001)
+    rows[1000, 5] = 0       # now the second chunk holds the unique maximum
+    r = sw.nonlinearity_from_spectrum(sw.WalshSpectrum(n, 11, rows))
     assert (r.value, r.argmin_v) == (((1 << n) - 1000) // 2, 1101)
-    row_max, _ = sw.reducers.spectrum_row_maxabs(sw.WalshSpectrum(n, 11, rows))
+    rows[1000, 5] = -1000
+    row_max, _ = sw.nonlinearity.spectrum_row_maxabs(sw.WalshSpectrum(n, 11, rows))
     want = np.abs(rows).max(axis=1)
     assert np.array_equal(row_max.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("nrows,chunk_rows", [(7, 3), (64, 64), (65, 8), (1, 5)])
+def test_device_to_host_chunked_every_chunk(nrows, chunk_rows):
+    """device_to_host_chunked with several chunks and an odd final chunk:
+    element-wise equal to a plain device -> host copy."""
+    import torch
+
+    src = torch.randint(-2**31, 2**31 - 1, (nrows, 1000), dtype=torch.int32, device="cuda")
+    out = np.empty((nrows, 1000), dtype=np.int32)
+    sw.walsh.device_to_host_chunked(src, out, chunk_bytes=chunk_rows * 1000 * 4)
+    assert np.array_equal(out, src.cpu().numpy())
+
+
+def test_spectrum_to_host_into_strided_and_read_only_out():
+    """spectrum_to_host writes into a caller's negative-stride view with
+    numpy's assignment rules and refuses a read-only one like numpy does."""
+    s = sw.generate_sbox(9, 6, seed=2)
+    want = orc.spectrum(s.table, 9, 1, 64)
+    big = np.zeros((63, 512), dtype=np.int32)
+    view = big[::-1]
+    sw.spectrum_to_host(s, layout="mask", out=view, chunk_bytes=10 * 512 * 4)
+    assert np.array_equal(view, want)
+    ro = np.zeros((63, 512), dtype=np.int32)
+    ro.flags.writeable = False
+    with pytest.raises(ValueError):
+        sw.spectrum_to_host(s, layout="mask", out=ro)

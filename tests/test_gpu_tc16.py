@@ -24,7 +24,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _maxima(s, lo, hi):
     mx, key = sw.component_max_abs_device(s, lo, hi)
-    return mx.cpu().numpy().astype(np.int64), sw.transforms.decode_key(key, s.n)
+    return mx.cpu().numpy().astype(np.int64), sw.walsh.decode_key(key, s.n)
 
 
 def test_constant_components_w0_extremes():

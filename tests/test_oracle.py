@@ -140,3 +140,38 @@ def test_stream_loop_equals_batched():
 def test_partition():
     assert [b - a for a, b in orc.partition_columns(15, 8)] == [2, 2, 2, 2, 2, 2, 2, 1]
     assert orc.partition_columns(3, 8) == ((1, 2), (2, 3), (3, 4))
+
+
+# ---- column API on every integer dtype / x-major (golden_api.*, produced by
+# ---- tests/golden/make_golden_api.py running the reference) ---------------
+def _api():
+    import json
+    import os
+
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    with open(os.path.join(here, "golden_api.json")) as f:
+        meta = json.load(f)
+    with np.load(os.path.join(here, "golden_api.npz")) as z:
+        arrays = {k: z[k] for k in z.files}
+    return meta, arrays
+
+
+def test_typed_columns_oracle_matches_reference():
+    meta, arrays = _api()
+    for rec in meta["columns"]:
+        col = arrays[rec["key"] + "_in"]
+        out, mx = orc.fwht_column_typed(col)
+        assert out.dtype == col.dtype
+        assert np.array_equal(out, arrays[rec["key"] + "_out"]), rec
+        assert mx == rec["max_abs"], rec
+
+
+def test_xmajor_oracle_matches_reference():
+    meta, _ = _api()
+    for rec in meta["xmajor"]:
+        t = orc.gen_table(rec["n"], rec["m"], rec["seed"], rec["bijective"])
+        wt = np.ascontiguousarray(orc.polarity_block(t, 1, 1 << rec["m"]).T)
+        assert sha(wt) == rec["sha_polarity_xmajor"]
+        assert sha(orc.xmajor_spectrum_typed(wt)) == rec["sha_spectrum_xmajor"]
+    for pw, mx, nl in meta["column_nonlinearity"]:
+        assert orc.column_nl(pw, mx) == nl
