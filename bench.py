@@ -363,6 +363,9 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- roofline of the dominant kernel (fused NL) ----------------------
     peak = live_peak(lib, d, "sbw_int32_peak")
+    clk_summary = clk.summary()
+    dual_issue = (2 * 4 * 32 * d.device_info(local_rank)["sm_count"]
+                  * (clk_summary["sm_max_mhz"] or 1965) * 1e6)  # packed-16x2 lane-ops/s, both int pipes
     # sbw_nl takes the tensor-core kernel for n = 12..16 (n < 16: 2^(16-n)
     # components per 2^16 tile; needs m >= 16 - n), unless SBW_TC=0
     tc_path = 12 <= n <= 16 and m >= 16 - n and os.environ.get("SBW_TC", "1") != "0"
@@ -401,8 +404,13 @@ def run_ours(args, rank, world, local_rank):
                               "(x bits 8..n-1: 4 byte-lane + n-12 int16-lane stages incl. the "
                               "max fold); the r stages run as the int8 GEMM below",
             "kernel_ms": kern_ms,
-            "peak_source": "measured live by sbw_int32_peak (int32 lane-ops/s) x 2 lanes for "
-                           "packed 16-bit; not in MEASURED_PEAKS.json",
+            "peak_source": "measured live by sbw_int32_peak (best of IADD3/LOP3, IMAD and mixed "
+                           "chains, int32 lane-ops/s) x 2 lanes for packed 16-bit; not in "
+                           "MEASURED_PEAKS.json",
+            "peak_dual_issue": dual_issue / 1e12,
+            "frac_dual_issue": achieved / dual_issue,
+            "peak_dual_issue_source": "theoretical: 4 warp-instr/clk/SM (ALU + FMA pipes dual-issued) "
+                                      "x 32 lanes x SMs x max SM clock x 2 packed 16-bit lanes",
             "tensor": {"achieved": mma_ops / (kern_ms * 1e-3) / 1e15, "peak": peak_i8 / 1e15,
                        "unit": "POP/s int8", "frac": mma_ops / (kern_ms * 1e-3) / peak_i8,
                        "ops_per_launch": mma_ops,
@@ -493,7 +501,7 @@ def run_ours(args, rank, world, local_rank):
                 "path": "sbw_nl_host C ABI (host table in, host NL out, page-locked caller "
                         "buffers), wall clock"},
         "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+        "clocks": clk_summary,
     }
     if not args.no_cpu and world == 1:  # the CPU baseline is reported at N = 1 only
         line["cpu_baseline"] = cpu_baseline(args.config, target_s=args.cpu_seconds)

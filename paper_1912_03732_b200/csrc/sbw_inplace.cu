@@ -144,7 +144,8 @@ int run_gen(void* data, int k, int64_t count, int64_t col_stride, int64_t elem_s
   const int col_fast = (col_stride == 1 && elem_stride != 1) ? 1 : 0;
   int b0 = 0;
   while (b0 < k) {
-    const int nb = (k - b0) < 6 ? (k - b0) : 6;
+    constexpr int kMaxNb = sizeof(T) == 8 ? 4 : 6;  // 2^NB elements in registers (64-bit: no spills)
+    const int nb = (k - b0) < kMaxNb ? (k - b0) : kMaxNb;
     long long* mx = (b0 + nb == k) ? max_abs : nullptr;
     const int grid = grid_cap(count << (k - nb));
     switch (nb) {
@@ -153,7 +154,10 @@ int run_gen(void* data, int k, int64_t count, int64_t col_stride, int64_t elem_s
       case 3: k_inplace_gen<T, 3><<<grid, 256, 0, st>>>(d, k, b0, count, col_stride, elem_stride, col_fast, mx); break;
       case 4: k_inplace_gen<T, 4><<<grid, 256, 0, st>>>(d, k, b0, count, col_stride, elem_stride, col_fast, mx); break;
       case 5: k_inplace_gen<T, 5><<<grid, 256, 0, st>>>(d, k, b0, count, col_stride, elem_stride, col_fast, mx); break;
-      default: k_inplace_gen<T, 6><<<grid, 256, 0, st>>>(d, k, b0, count, col_stride, elem_stride, col_fast, mx); break;
+      default:
+        if constexpr (kMaxNb >= 6)
+          k_inplace_gen<T, 6><<<grid, 256, 0, st>>>(d, k, b0, count, col_stride, elem_stride, col_fast, mx);
+        break;
     }
     SBW_LAUNCH_CHECK("k_inplace_gen");
     b0 += nb;

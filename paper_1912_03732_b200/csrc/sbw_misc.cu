@@ -2,6 +2,7 @@
 // truth tables, the layout transpose, the reducers, the direct-sum and
 // affine-distance checkers and the INT32 peak microbenchmark.
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 
 #include "sbw_internal.cuh"
@@ -731,18 +732,21 @@ int launch_bruteforce(const void* table, int tbytes, int n, int m, int32_t* best
 // ---------------------------------------------------------------------------
 // INT32 ALU peak microbenchmark.  8 independent dependency chains per
 // thread; MODE 0: add/sub pairs (IADD3, ALU pipe), MODE 1: multiply-add with
-// a runtime multiplier (IMAD, FMA pipe), MODE 2: both interleaved.  Each
+// a runtime multiplier (IMAD, FMA pipe), MODE 2: both interleaved (2:1),
+// MODE 3: LOP3 and IMAD chains 1:1 (both pipes dual-issued: the 4 warp-instr
+// per clock per SM ceiling).  The best mode is reported.  Each
 // executed lane-instruction counts as one integer op.  MODE 0 alternates
 // add and xor (IADD3 / LOP3) so no algebraic folding is possible.
 // ---------------------------------------------------------------------------
 template <int MODE>
 __global__ void __launch_bounds__(512) k_int32_peak(int iters, int mul, int32_t* sink) {
-  int x[8], y[8], z[8];
+  int x[8], y[8], z[8], w[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     x[i] = threadIdx.x + i;
     y[i] = blockIdx.x * 7 + i;
     z[i] = threadIdx.x ^ (i * 977);
+    w[i] = blockIdx.x ^ (i * 131);
   }
   const int c = mul, d = mul ^ 0x5bd1e995;
   for (int it = 0; it < iters; ++it) {
@@ -751,17 +755,27 @@ __global__ void __launch_bounds__(512) k_int32_peak(int iters, int mul, int32_t*
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         // volatile asm keeps the compiler from folding the linear chains
-        if (MODE != 1) {
+        if (MODE == 0 || MODE == 2) {
           asm volatile("add.s32 %0, %0, %1;" : "+r"(x[i]) : "r"(y[i]));
           asm volatile("xor.b32 %0, %0, %1;" : "+r"(y[i]) : "r"(x[i]));
         }
-        if (MODE != 0) asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(z[i]) : "r"(c), "r"(d));
+        if (MODE == 1 || MODE == 2) asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(z[i]) : "r"(c), "r"(d));
+        if (MODE == 3) {
+          // dual issue, 1:1: LOP3 chains (ALU pipe) beside IMAD chains (FMA
+          // pipe), 16 independent chains per thread (SASS: LOP3.LUT / IMAD)
+          // the LOP3 operand is the IMAD chain's latest value, so neither
+          // chain can be folded across iterations
+          asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(z[i]) : "r"(c), "r"(d));
+          asm volatile("lop3.b32 %0, %0, %1, %2, 0x78;" : "+r"(x[i]) : "r"(z[i]), "r"(d));  // x ^ (z & d)
+          asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(w[i]) : "r"(d), "r"(c));
+          asm volatile("lop3.b32 %0, %0, %1, %2, 0x78;" : "+r"(y[i]) : "r"(w[i]), "r"(c));
+        }
       }
     }
   }
   int s = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) s ^= x[i] ^ y[i] ^ z[i];
+  for (int i = 0; i < 8; ++i) s ^= x[i] ^ y[i] ^ z[i] ^ w[i];
   if (s == 0x7fffffff) sink[0] = s;
 }
 
@@ -775,20 +789,23 @@ int run_int32_peak(double* ops_per_s, double* ms_out, cudaStream_t st) {
   SBW_CUDA_CHECK(cudaEventCreate(&e1));
   const int blocks = dp.sm_count * 4, threads = 512, iters = 4096;
   double best = 0, best_ms = 0;
-  for (int mode = 0; mode < 3; ++mode) {
+  for (int mode = 0; mode < 4; ++mode) {
     for (int rep = 0; rep < 3; ++rep) {
       SBW_CUDA_CHECK(cudaEventRecord(e0, st));
       if (mode == 0) k_int32_peak<0><<<blocks, threads, 0, st>>>(iters, 3, sink);
       if (mode == 1) k_int32_peak<1><<<blocks, threads, 0, st>>>(iters, 3, sink);
       if (mode == 2) k_int32_peak<2><<<blocks, threads, 0, st>>>(iters, 3, sink);
+      if (mode == 3) k_int32_peak<3><<<blocks, threads, 0, st>>>(iters, 3, sink);
       SBW_LAUNCH_CHECK("k_int32_peak");
       SBW_CUDA_CHECK(cudaEventRecord(e1, st));
       SBW_CUDA_CHECK(cudaEventSynchronize(e1));
       float ms = 0;
       SBW_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
-      const double per_iter = mode == 0 ? 256.0 : (mode == 1 ? 128.0 : 384.0);
+      const double per_iter = mode == 0 ? 256.0 : (mode == 1 ? 128.0 : (mode == 2 ? 384.0 : 512.0));
       const double ops = double(blocks) * threads * iters * per_iter;
       const double rate = ops / (ms * 1e-3);
+      if (rep > 0 && getenv("SBW_PEAK_VERBOSE"))
+        fprintf(stderr, "k_int32_peak<%d>: %.3f T lane-ops/s (%.3f ms)\n", mode, rate / 1e12, ms);
       if (rep > 0 && rate > best) {
         best = rate;
         best_ms = ms;
