@@ -87,6 +87,8 @@ def main():
         jobs += [(name, lo, min(lo + step, total)) for lo in range(1, total, step)]
     # interleave the configs so partial progress covers both
     jobs.sort(key=lambda j: (j[1] / (1 << CONFIGS[j[0]][1])))
+    if len(sys.argv) > 2 and sys.argv[2] == "rev":  # a second runner from the other end
+        jobs.reverse()
     t0 = time.time()
     with mp.Pool(procs) as pool:
         for k, (name, lo, hi, dt) in enumerate(pool.imap_unordered(_chunk, jobs)):

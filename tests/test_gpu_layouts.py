@@ -1,0 +1,92 @@
+"""Materialised spectra in both layouts at every n, against the oracle and the
+reference's own full-matrix hashes.
+
+  mask-major rows[v - 1][u] = W(u, v)   (WalshSpectrum.rows, walsh.py:32-44, :174)
+  x-major    wt[u][v - 1]   = W(u, v)   (walsh.py:117-131)
+
+The x-major store is checked above n = 12 (tensor-core spectrum kernels
+n = 13..16, multi-pass K3 n >= 17) on unaligned mask slices, and the whole
+16x16 matrix (2^32 entries, 16 GiB per layout) is hashed in both layouts and
+compared with tests/golden/hashes_16x16.json, which
+tests/golden/make_golden_16x16_hashes.py computed by running the reference.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1912_03732_b200 as sw
+from oracle import sbw_oracle as orc
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.parametrize("n,v_lo,count", [(13, 77, 37), (14, 1, 64), (14, 16000, 383), (15, 5, 21),
+                                          (15, 32700, 67), (16, 1, 33), (16, 44801, 40),
+                                          (16, 65500, 35)])
+def test_xmajor_slices_tensor_core_sizes(n, v_lo, count):
+    s = sw.generate_sbox(n, n, 0, bijective=True)
+    v_hi = min(1 << n, v_lo + count)
+    want = orc.spectrum(s.table, n, v_lo, v_hi)
+    xm, mx = sw.spectrum_device(s, v_lo, v_hi, layout="x")
+    assert tuple(xm.shape) == (1 << n, v_hi - v_lo)
+    assert np.array_equal(xm.cpu().numpy(), want.T)
+    assert np.array_equal(mx.cpu().numpy(), np.abs(want.astype(np.int64)).max(axis=1))
+    mm, _ = sw.spectrum_device(s, v_lo, v_hi, layout="mask")
+    assert np.array_equal(mm.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("n,m,seed", [(17, 5, 1), (18, 4, 2), (20, 3, 3), (21, 2, 4), (24, 2, 5)])
+def test_xmajor_multipass_sizes(n, m, seed):
+    """n >= 17 (multi-pass K3 spectrum) in both layouts, every mask."""
+    s = sw.generate_sbox(n, m, seed)
+    want = orc.spectrum(s.table, n, 1, 1 << m)
+    xm, _ = sw.spectrum_device(s, layout="x")
+    assert np.array_equal(xm.cpu().numpy(), want.T)
+    mm, mx = sw.spectrum_device(s, layout="mask")
+    assert np.array_equal(mm.cpu().numpy(), want)
+    assert np.array_equal(mx.cpu().numpy(), np.abs(want.astype(np.int64)).max(axis=1))
+
+
+def test_xmajor_host_export_16x16_slice():
+    """spectrum_to_host(layout="x") on a 16x16 mask slice, chunked."""
+    s = sw.generate_sbox(16, 16, 0, bijective=True)
+    out, mx = sw.spectrum_to_host(s, 1000, 1300, layout="x", chunk_bytes=97 * 65536 * 4)
+    want = orc.spectrum(s.table, 16, 1000, 1300)
+    assert np.array_equal(out, want.T)
+    assert np.array_equal(mx, np.abs(want.astype(np.int64)).max(axis=1))
+
+
+def _golden_hashes():
+    with open(os.path.join(HERE, "golden", "hashes_16x16.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.slow
+def test_16x16_full_matrix_hashes_both_layouts():
+    """All 2^32 coefficients of the 16x16 seed-0 box, both layouts, hashed
+    and compared with the reference's own hashes (16 GiB each)."""
+    import torch
+
+    g = _golden_hashes()
+    s = sw.generate_sbox(16, 16, 0, bijective=True)
+    # mask-major: 1024-mask device chunks, streamed to the host in order
+    h = hashlib.sha256()
+    for a in range(1, 1 << 16, 1024):
+        b = min(1 << 16, a + 1024)
+        chunk, _ = sw.spectrum_device(s, a, b, layout="mask")
+        h.update(chunk.cpu().numpy().tobytes())
+        del chunk
+    assert h.hexdigest() == g["sha256_mask_major"]
+    # x-major: the whole 16 GiB store on the device, row blocks to the host
+    xm, mx = sw.spectrum_device(s, layout="x")
+    torch.cuda.synchronize()
+    h = hashlib.sha256()
+    for a in range(0, 1 << 16, 1024):
+        h.update(xm[a:a + 1024].cpu().numpy().tobytes())
+    assert h.hexdigest() == g["sha256_x_major"]
+    r = sw.nonlinearity_from_maxima(sw.ColumnMaxima(16, 16, sw.walsh.maxabs_to_nl(mx, 16)))
+    assert (r.value, r.argmin_v) == (g["nl"], g["argmin_v"])
