@@ -58,6 +58,8 @@ size_t k3_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi);
 // SBW_PASSB_TC=0 keeps the fp32 k_passb_staged kernel.
 struct PassBArgs;
 bool passb_tc_enabled();
+// cuTensorMapEncodeTiled through the runtime's driver entry point (null if unavailable)
+void* tma_encode_ptr();
 int launch_passb_tc(const PassBArgs& a, cudaStream_t st);
 int launch_k3(const void* table, int tbytes, int n, int m, uint32_t v_lo, uint32_t v_hi,
               int32_t* max_abs, unsigned long long* key, int32_t* out, int64_t ld, void* scratch,

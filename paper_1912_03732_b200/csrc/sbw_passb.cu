@@ -5,6 +5,9 @@
 // Measured: ~1 GiB batches beat L2-sized ones and a persistent
 // work-queue kernel, because launches are few and both passes run at full
 // occupancy; the scratch traffic (4 B / element) streams through HBM.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -168,8 +171,55 @@ int run_passb_staged(const PassBArgs& a, cudaStream_t st) {
   return SBW_OK;
 }
 
+// SBW_PASSB_BULK=0 keeps k_passb_regs for the H <= 5 NL pass B.
+bool passb_bulk_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SBW_PASSB_BULK");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int H>
+int run_passb_bulk(const PassBArgs& a, cudaStream_t st) {
+  DeviceProps dp;
+  if (int rc = device_props(&dp)) return rc;
+  constexpr int smem = bulk_smem_bytes<H>();
+  static int occ_dev[64] = {};
+  int& occ = occ_dev[dp.device & 63];
+  if (occ == 0) {
+    SBW_CUDA_CHECK(cudaFuncSetAttribute(k_passb_bulk<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SBW_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_passb_bulk<H>, kBulkThreads, smem));
+  }
+  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tma_encode_ptr());
+  if (!enc) return set_error(SBW_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {cuuint64_t(1) << (14 + a.e16), cuuint64_t(a.n_comp) << H};
+  const cuuint64_t strides[1] = {cuuint64_t(4) << (14 + a.e16)};
+  const cuuint32_t box[2] = {cuuint32_t(kBulkThreads), cuuint32_t(1 << H)};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(a.scratch), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(SBW_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  const int64_t ctas = a.n_comp * ((int64_t(1) << (14 + a.e16)) / kBulkThreads);
+  const int64_t cap = int64_t(dp.sm_count) * (occ > 0 ? occ : 1);
+  k_passb_bulk<H><<<int(ctas < cap ? ctas : cap), kBulkThreads, smem, st>>>(map, a);
+  SBW_LAUNCH_CHECK("k_passb_bulk");
+  return SBW_OK;
+}
+
 template <int MODE>
 int dispatch_passb_regs(int h, const PassBArgs& a, cudaStream_t st) {
+  if (MODE == MODE_NL && h <= 5 && passb_bulk_enabled()) {
+    switch (h) {
+      case 2: return run_passb_bulk<2>(a, st);
+      case 3: return run_passb_bulk<3>(a, st);
+      case 4: return run_passb_bulk<4>(a, st);
+      case 5: return run_passb_bulk<5>(a, st);
+      default: break;
+    }
+  }
   switch (h) {
     case 2: return run_passb_regs<2, MODE>(a, st);
     case 3: return run_passb_regs<3, MODE>(a, st);

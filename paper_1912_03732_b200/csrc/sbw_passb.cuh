@@ -17,6 +17,8 @@
 //           chunk prefetched while the current one computes.
 #pragma once
 
+#include <cuda.h>
+
 #include "sbw_tile_simd.cuh"
 
 namespace sbw {
@@ -268,6 +270,113 @@ __global__ void __launch_bounds__(kPassBThreads) k_passb_regs(PassBArgs a) {
       for (int i = 0; i < NI; ++i)
         __stcs(reinterpret_cast<int2*>(dst + (int64_t(i) << 15)), make_int2(w[2 * i], w[2 * i + 1]));
     }
+    if (b + 1 >= b1 || (b + 1) / chunks != comp) {  // CTA-uniform
+      publish_comp(a, comp, run);
+      run = 0;
+    }
+  }
+}
+
+// ---- H <= 5 (n = 17..20) NL pass B fed by bulk copies ------------------------
+// The same per-column arithmetic as k_passb_regs, but an item's 2^H rows of
+// 256 words (1 KiB each) reach shared memory by TMA (completion on an
+// mbarrier), kBulkStages items ahead of
+// the one being computed, one 2D TMA load per item.  k_passb_regs keeps 2^H
+// 4-byte loads per thread in flight and is latency-bound near 5 TB/s; here
+// one thread per CTA keeps kBulkStages x 2^H KiB in flight.
+#ifndef SBW_BULK_THREADS
+#define SBW_BULK_THREADS 256
+#endif
+constexpr int kBulkThreads = SBW_BULK_THREADS;
+#ifndef SBW_BULK_STAGES
+#define SBW_BULK_STAGES 2
+#endif
+constexpr int kBulkStages = SBW_BULK_STAGES;
+template <int H>
+constexpr int bulk_smem_bytes() { return kBulkStages * (1 << H) * kBulkThreads * 4; }
+
+__device__ __forceinline__ void tma_load_2d_u32(uint32_t* dst, const void* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y),
+      "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+
+__device__ __forceinline__ void bar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tSBW_BULK_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra SBW_BULK_DONE;\n\tbra SBW_BULK_WAIT;\n\tSBW_BULK_DONE:\n\t}\n" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+      "r"(parity)
+      : "memory");
+}
+
+// tmap: 2D tensor map over the batch scratch, dims {2^(14 + e16) words of a
+// row, n_comp * 2^H rows}, box {256 words, 2^H rows}: one TMA load per item.
+template <int H>
+__global__ void __launch_bounds__(kBulkThreads) k_passb_bulk(const __grid_constant__ CUtensorMap tmap, PassBArgs a) {
+  constexpr int NI = 1 << H;
+  constexpr uint32_t kRowBytes = kBulkThreads * 4;
+  extern __shared__ __align__(128) uint32_t bsm[];  // [kBulkStages][NI][256] words
+  __shared__ __align__(8) uint64_t full[kBulkStages];
+  if (passb_gated_off(a)) return;
+  const int row_log = 14 + a.e16;  // u32 words per row
+  const int64_t chunks = (int64_t(1) << row_log) / kBulkThreads;
+  const float bias2 = a.e16 ? 16842752.0f : 16809984.0f;
+  const int64_t items = a.n_comp * chunks;
+  const int64_t per_cta = (items + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per_cta;
+  const int64_t b1 = b0 + per_cta < items ? b0 + per_cta : items;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < kBulkStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(&full[s])))
+                   : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // thread 0: load item b's rows into stage s
+  auto issue = [&](int64_t b, int s) {
+    const int64_t comp = b / chunks, ch = b - comp * chunks;
+    bar_expect_tx(&full[s], NI * kRowBytes);
+    tma_load_2d_u32(bsm + s * (NI * kBulkThreads), &tmap, int(ch * kBulkThreads), int(comp * NI), &full[s]);
+  };
+  if (tid == 0)
+    for (int k = 0; k < kBulkStages && b0 + k < b1; ++k) issue(b0 + k, k);
+  int run = 0;
+  int64_t it = 0;
+  for (int64_t b = b0; b < b1; ++b, ++it) {
+    const int s = int(it % kBulkStages);
+    bar_wait_parity(&full[s], uint32_t((it / kBulkStages) & 1));
+    uint32_t u[NI];
+    const uint32_t* stg = bsm + s * (NI * kBulkThreads) + tid;
+#pragma unroll
+    for (int r = 0; r < NI; ++r) u[r] = stg[r * kBulkThreads];
+    __syncthreads();  // stage s fully read: refill it
+    if (tid == 0 && b + kBulkStages < b1) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(b + kBulkStages, s);
+    }
+    float e[2 * NI];
+#pragma unroll
+    for (int i = 0; i < NI; i += 2) load_rows_stage1(u[i], u[i + 1], e + 2 * i, bias2);
+    fwht_regs_f<2 * NI, 4, NI>(e);
+    float mf = 0.f;
+#pragma unroll
+    for (int k = 0; k < NI; ++k) mf = fmaxf(mf, __fadd_rn(fabsf(e[k]), fabsf(e[k + NI])));
+    run = max(run, 2 * __float2int_rn(mf));  // values are halved
+    const int64_t comp = b / chunks;
     if (b + 1 >= b1 || (b + 1) / chunks != comp) {  // CTA-uniform
       publish_comp(a, comp, run);
       run = 0;

@@ -367,6 +367,8 @@ int run_passb_tc(const PassBArgs& a, cudaStream_t st) {
 
 }  // namespace
 
+void* tma_encode_ptr() { return reinterpret_cast<void*>(encode_fn()); }
+
 bool passb_tc_enabled() {
   static const bool on = [] {
     const char* e = getenv("SBW_PASSB_TC");
