@@ -98,9 +98,10 @@ int check_range(int m, uint32_t v_lo, uint32_t v_hi) {
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 // Every entry point runs on the device that owns its work: the stream's
-// device (cudaStreamGetDevice) for a created stream, else the device of the
-// output pointer (the NULL / legacy stream belongs to whatever device is
-// current, which need not be where the caller's buffers live).  The caller's
+// device (cudaStreamGetDevice) for a created stream, else (NULL / legacy
+// stream, or a stream being captured into a CUDA graph) the device of the
+// data pointer (the NULL stream belongs to whatever device is current, which
+// need not be where the caller's buffers live).  The caller's
 // current device is restored on return, and the per-device caches inside
 // libsbw (device_props, tensor-core constants, K3 streams) key off the
 // device selected here.
@@ -110,9 +111,17 @@ class DeviceScope {
     int want = -1;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (st != nullptr && st != cudaStreamLegacy && st != cudaStreamPerThread) {
-      if (cudaStreamGetDevice(st, &want) != cudaSuccess) {
+      // cudaStreamGetDevice is not allowed while the stream is being
+      // captured into a CUDA graph (it invalidates the capture); a capturing
+      // caller gets the pointer's device below
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
+        if (cudaStreamGetDevice(st, &want) != cudaSuccess) {
+          cudaGetLastError();
+          want = -1;
+        }
+      } else {
         cudaGetLastError();
-        want = -1;
       }
     }
     if (want < 0 && ptr != nullptr) {

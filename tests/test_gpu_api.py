@@ -216,3 +216,37 @@ def test_bench_spawns_ranks_without_torchrun():
     line = lines[0]
     assert line["n_gpus"] == 2 and line["scaling"] == "strong"
     assert (line["result"]["nl"], line["result"]["argmin_v"]) == (1872, 3572)
+
+
+def test_libsbw_calls_capture_into_a_cuda_graph():
+    """libsbw entry points are stream-ordered and capturable: a 12x12 NL
+    captured into a CUDA graph replays to the reference's maxima (the device
+    selection must not query the capturing stream's device)."""
+    import torch
+
+    import paper_1912_03732_b200.device as d
+
+    s = sw.generate_sbox(12, 12, 0, bijective=True)
+    lib = d.load_library()
+    dev = torch.device("cuda", 0)
+    tab = d.device_table(s, dev)
+    mx = torch.empty(4095, dtype=torch.int32, device=dev)
+    key = torch.zeros(1, dtype=torch.int64, device=dev)
+    sb = lib.sbw_nl_scratch_bytes(12, 12, 1, 4096)
+    scratch = torch.empty(max(1, sb), dtype=torch.uint8, device=dev)
+    st = torch.cuda.Stream(dev)
+
+    def call():
+        d.check(lib.sbw_nl(tab.data_ptr(), 2, 12, 12, 1, 4096, mx.data_ptr(), key.data_ptr(),
+                           scratch.data_ptr(), sb, st.cuda_stream))
+
+    with torch.cuda.stream(st):
+        call()  # first call: per-device setup outside the capture
+    st.synchronize()
+    mx.zero_()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=st, capture_error_mode="relaxed"):
+        call()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(mx.cpu().numpy().astype(np.int64), orc.component_max_abs(s.table, 12, 1, 4096))

@@ -1,0 +1,59 @@
+"""configs[1] (12x12, seed 0): materialised spectrum in both layouts + maxima,
+device time without Python launch overhead: the libsbw calls are captured
+once into a CUDA graph and the graph is replayed (CUDA events around 50
+replays).  Checked against the committed golden hashes first."""
+import ctypes
+import hashlib
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_1912_03732_b200 as sw  # noqa: E402
+from paper_1912_03732_b200 import device as d  # noqa: E402
+
+g = json.load(open("tests/golden/golden.json"))["configs"]["12x12"]
+s = sw.generate_sbox(12, 12, 0, bijective=True)
+lib = d.load_library()
+dev = torch.device("cuda", 0)
+tab = d.device_table(s, dev)
+res = {}
+for layout, lay in (("mask", 0), ("x", 1)):
+    shape = (4095, 4096) if lay == 0 else (4096, 4095)
+    out = torch.empty(shape, dtype=torch.int32, device=dev)
+    mx = torch.empty(4095, dtype=torch.int32, device=dev)
+    sb = lib.sbw_spectrum_scratch_bytes(12, 12, 1, 4096, lay)
+    scratch = torch.empty(max(1, sb), dtype=torch.uint8, device=dev)
+    st = torch.cuda.Stream(dev)
+
+    def call():
+        d.check(lib.sbw_spectrum(tab.data_ptr(), 2, 12, 12, 1, 4096, lay, out.data_ptr(), shape[1],
+                                 mx.data_ptr(), scratch.data_ptr(), sb, st.cuda_stream))
+
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            call()
+    st.synchronize()
+    h = hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest()[:16]
+    assert h == g["sha_mask_major" if lay == 0 else "sha_x_major"], (layout, h)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=st, capture_error_mode="relaxed"):
+        call()
+    for _ in range(5):
+        graph.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    reps = 50
+    with torch.cuda.stream(st):
+        for _ in range(reps):
+            graph.replay()
+    e1.record(st)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / reps
+    res[layout] = us
+    print(f"12x12 spectrum {layout}-major + maxima (graph replay, L2-warm): {us:.1f} us per call, "
+          f"{4095 * 4096 * 4 / us / 1e6:.2f} TB/s of output", flush=True)
+print(json.dumps(res))
