@@ -8,7 +8,9 @@ mask range, results land in disjoint slots, so output is bit-identical for
 any shard count.  `evaluate_distributed` is the multi-process form (one rank
 per GPU, torch.distributed): each rank owns one range, the per-component
 values are all-gathered and the (max|W|, smallest v) key is max-reduced --
-the only exchange on the path.
+the only exchange on the path.  `spectrum_distributed` is the materialised
+form: every rank keeps its own range of the Walsh matrix (either layout) on
+its GPU and only the key is max-reduced.
 """
 from __future__ import annotations
 
@@ -263,3 +265,75 @@ def evaluate_distributed(s: SBox, group=None, compute=None, return_values: bool 
     if gap & 1:
         raise AssertionError("spectrum maximum has wrong parity")
     return NonlinearityResult(gap >> 1, v, "distributed"), cm
+
+
+def _key_of_maxima(mx, v_lo: int):
+    """(max|W| << 32) | (0xFFFFFFFF - v) of a shard's per-component maxima,
+    v = the smallest mask reaching the maximum (the reference's first
+    argmin, nonlinearity.py:44-49).  Device tensors stay on the device."""
+    import torch
+
+    if isinstance(mx, np.ndarray):
+        i = int(np.argmax(mx))
+        return (int(mx[i]) << 32) | (0xFFFFFFFF - (v_lo + i))
+    i = torch.argmax(mx)  # first maximal index
+    return (mx[i].to(torch.int64) << 32) | (0xFFFFFFFF - (v_lo + i))
+
+
+def spectrum_distributed(s: SBox, group=None, layout: str = "mask", compute=None,
+                         max_bytes: int | None = None):
+    """Materialised Walsh spectrum, sharded over the ranks of `group`.
+
+    Rank r computes and keeps only its mask range (lo, hi) =
+    partition_columns(2^m - 1, world)[r] (parallel.py:38-57) on its own GPU,
+    in the reference's row layout (layout="mask": int32 [hi - lo, 2^n],
+    rows[v - lo][u] = W(u, v), walsh.py:174) or x-major (layout="x": int32
+    [2^n, hi - lo], wt[u][v - lo], walsh.py:117-131).  The matrix is never
+    gathered; the only exchange is one all-reduce(MAX) of the packed
+    (max|W|, smallest v) key, so every rank also gets the global NL.
+
+    Returns (shard, (lo, hi), NonlinearityResult): the shard is a device
+    tensor (or, with an injected `compute(s, lo, hi, layout) -> (numpy
+    shard, numpy int32 max|W|)`, used by the CPU tests, a CPU tensor).
+    `max_bytes` bounds the shard like the reference's retain-mode budget
+    (walsh.py:220-222).
+    """
+    import torch
+    import torch.distributed as dist
+
+    if layout not in ("mask", "x"):
+        raise ValueError(f"layout must be 'mask' or 'x', got {layout!r}")
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    total = (1 << s.m) - 1
+    ranges = list(partition_columns(total, world).ranges)
+    ranges += [(total + 1, total + 1)] * (world - len(ranges))
+    lo, hi = ranges[rank]
+    count = hi - lo
+    check_budget(count * (1 << s.n) * 4, max_bytes)
+    backend = dist.get_backend(group)
+    shape = (count, 1 << s.n) if layout == "mask" else (1 << s.n, count)
+    if compute is None:
+        dev = _dev.require_device()
+        if count > 0:
+            shard, mx = spectrum_device(s, lo, hi, layout=layout, device=dev)
+            key_t = _key_of_maxima(mx, lo).reshape(1)
+        else:
+            shard = torch.empty(shape, dtype=torch.int32, device=dev)
+            key_t = torch.zeros(1, dtype=torch.int64, device=dev)
+    else:
+        if count > 0:
+            sh, mx = compute(s, lo, hi, layout)
+            shard = torch.from_numpy(np.ascontiguousarray(sh, dtype=np.int32))
+            key_t = torch.tensor([_key_of_maxima(np.asarray(mx), lo)], dtype=torch.int64)
+        else:
+            shard = torch.empty(shape, dtype=torch.int32)
+            key_t = torch.zeros(1, dtype=torch.int64)
+    red = key_t if backend == "nccl" else key_t.cpu()
+    dist.all_reduce(red, op=dist.ReduceOp.MAX, group=group)
+    k = int(red.item())
+    mxw = k >> 32
+    gap = (1 << s.n) - mxw
+    if gap & 1:
+        raise AssertionError("spectrum maximum has wrong parity")
+    return shard, (lo, hi), NonlinearityResult(gap >> 1, 0xFFFFFFFF - (k & 0xFFFFFFFF), "distributed")

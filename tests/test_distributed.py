@@ -67,3 +67,63 @@ def test_sharded_nl_equals_single_process(world, n, m, seed, bij):
     for rank, value, argmin, values in out:
         assert (value, argmin) == (wv, wa), rank
         assert np.array_equal(np.array(values), want), rank
+
+
+# ---------------------------------------------------------------------------
+# spectrum_distributed: the materialised Walsh matrix sharded over the ranks
+# ---------------------------------------------------------------------------
+def _oracle_spectrum_shard(s, lo, hi, layout):
+    from oracle import sbw_oracle as orc
+
+    rows = orc.spectrum(s.table, s.n, lo, hi)
+    mx = np.abs(rows).max(axis=1).astype(np.int32)
+    return (rows if layout == "mask" else rows.T), mx
+
+
+def _spec_worker(rank, world, port, n, m, seed, bij, layout, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1912_03732_b200 as sw
+
+        s = sw.generate_sbox(n, m, seed, bijective=bij)
+        shard, (lo, hi), res = sw.spectrum_distributed(s, layout=layout, compute=_oracle_spectrum_shard)
+        q.put((rank, lo, hi, res.value, res.argmin_v, shard.numpy().tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,m,seed,bij,layout", [(2, 8, 8, 0, True, "mask"), (3, 7, 5, 4, False, "x"),
+                                                       (4, 6, 2, 1, False, "mask"), (2, 5, 3, 2, False, "x")])
+def test_sharded_spectrum_equals_single_process(world, n, m, seed, bij, layout):
+    """Each rank holds exactly its partition_columns range of the matrix in
+    the requested layout; the shards tile the whole matrix; every rank gets
+    the global NL from the one key all-reduce.  (m = 2 with world 4 leaves
+    rank 3 an empty shard.)"""
+    from oracle import sbw_oracle as orc
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_spec_worker, args=(r, world, port, n, m, seed, bij, layout, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    t = orc.gen_table(n, m, seed, bij)
+    full = orc.spectrum(t, n, 1, 1 << m)
+    wv, wa = orc.nl_from_maxima(orc.component_nl(t, n, 1, 1 << m))
+    want_ranges = list(orc.partition_columns((1 << m) - 1, world))
+    want_ranges += [((1 << m), (1 << m))] * (world - len(want_ranges))
+    for rank, lo, hi, value, argmin, shard in out:
+        assert (lo, hi) == tuple(want_ranges[rank])
+        assert (value, argmin) == (wv, wa), rank
+        want = full[lo - 1:hi - 1]
+        got = np.asarray(shard, dtype=np.int32).reshape((hi - lo, 1 << n) if layout == "mask" else (1 << n, hi - lo))
+        assert np.array_equal(got, want if layout == "mask" else want.T), rank

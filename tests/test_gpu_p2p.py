@@ -70,3 +70,61 @@ def test_p2p_sharded_nl_equals_single_process(world, n, m, seed, bij):
         assert np.array_equal(np.asarray(values), cm.values), rank
     lo, hi = 1, min(1 << m, 65)
     assert np.array_equal(cm.values[: hi - lo], orc.component_nl(s.table, n, lo, hi))
+
+
+def _spec_worker(rank, world, port, n, m, seed, bij, layout, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import hashlib
+
+        import paper_1912_03732_b200 as sw
+
+        s = sw.generate_sbox(n, m, seed, bijective=bij)
+        shard, (lo, hi), res = sw.spectrum_distributed(s, layout=layout)
+        assert shard.is_cuda
+        h = hashlib.sha256(shard.cpu().numpy().tobytes()).hexdigest()
+        q.put((rank, lo, hi, res.value, res.argmin_v, h))
+    except Exception as e:
+        q.put((rank, None, None, None, None, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,m,seed,bij,layout", [(2, 12, 12, 0, True, "mask"),   # K2 spectrum
+                                                       (3, 13, 9, 3, False, "x"),      # K2 + transpose
+                                                       (2, 17, 6, 5, False, "mask")])  # K3 spectrum
+def test_sharded_spectrum_on_gpu(world, n, m, seed, bij, layout):
+    """spectrum_distributed with libsbw: each rank's device shard equals its
+    range of the single-process matrix (in the requested layout) and of the
+    oracle; the global NL comes from the one key all-reduce."""
+    import hashlib
+
+    import paper_1912_03732_b200 as sw
+    from oracle import sbw_oracle as orc
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_spec_worker, args=(r, world, port, n, m, seed, bij, layout, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(o[1] is not None for o in out), out
+    s = sw.generate_sbox(n, m, seed, bijective=bij)
+    full = orc.spectrum(s.table, n, 1, 1 << m)
+    want = orc.nl_from_maxima(orc.component_nl(s.table, n, 1, 1 << m))
+    for rank, lo, hi, value, argmin, h in out:
+        assert (value, argmin) == want, rank
+        part = full[lo - 1:hi - 1]
+        ref = np.ascontiguousarray(part if layout == "mask" else part.T)
+        assert h == hashlib.sha256(ref.tobytes()).hexdigest(), rank
