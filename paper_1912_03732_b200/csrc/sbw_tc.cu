@@ -375,7 +375,40 @@ struct TcArgs {
 };
 
 constexpr int kTcNL = 0, kTcEmit = 1, kTcSpec = 2, kTcEmit16 = 3;  // kTcEmit16: EMIT + stage 16
+// kTcSpecSt: n = 16 spectrum with the staged epilogue.  The exact W rows go
+// to a shared-memory ring of 8 KiB slots (8 u_c rows x 256 u_r: 8 KiB of one
+// contiguous mask-major row) and the three otherwise idle warps of the issuer
+// warpgroup copy each slot to global memory (STG.128, streaming).  The
+// transform warps no longer stall on the store queue before they can start
+// the next item, so the ~2 us of generation + stages per item overlaps the
+// ~6 us the SM needs to write 256 KiB (tools/micro/stg_width: 6.4 TB/s is
+// reachable with either store width).  The ring needs the smem of the second
+// B buffer: this mode generates B(i+1) into the single buffer after MMA(i).
+constexpr int kTcSpecSt = 4;
 __host__ __device__ constexpr bool is_emit(int mode) { return mode == kTcEmit || mode == kTcEmit16; }
+__host__ __device__ constexpr bool is_spec(int mode) { return mode == kTcSpec || mode == kTcSpecSt; }
+constexpr int kStSlotBytes = 8192;
+#ifndef SBW_ST_SLOTS
+#define SBW_ST_SLOTS 10
+#endif
+constexpr int kStSlots = SBW_ST_SLOTS;
+constexpr int kStOff = kBOff + kBBytes;  // after the single B buffer
+constexpr int kTcSmemSt = kStOff + kStSlots * kStSlotBytes;
+static_assert(kTcSmemSt <= 230 * 1024, "staged spectrum ring exceeds shared memory");
+#ifndef SBW_ST_INFLIGHT
+#define SBW_ST_INFLIGHT 3
+#endif
+constexpr int kStInflight = SBW_ST_INFLIGHT;  // bulk copies in flight before a slot is recycled
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(tc::smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
 
 // NL items for an n = NB <= 16 box: one 2^16 tile holds C = 2^(16 - NB)
 // components (slots); item t covers masks (base << log2 C) | slot, with base
@@ -451,14 +484,18 @@ __device__ __forceinline__ void publish_item(const TcArgs& a, const uint32_t* wm
 template <int MODE, int NB = 16>
 __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
   constexpr bool EMIT = is_emit(MODE);
-  static_assert(NB == 16 || ((MODE == kTcNL || MODE == kTcSpec) && NB >= 8 + kLogRows && kRows >= 8),
+  static_assert(NB == 16 || ((MODE == kTcNL || is_spec(MODE)) && NB >= 8 + kLogRows && kRows >= 8),
                 "n < 16: NL / SPEC with 8/16-row groups");
   constexpr int kSlots = 1 << (16 - NB);  // components per 2^16 tile
-  static_assert(MODE != kTcSpec || kC0Mma, "exact SPEC output needs the bias-block GEMM");
+  static_assert(!is_spec(MODE) || kC0Mma, "exact SPEC output needs the bias-block GEMM");
+  static_assert(MODE != kTcSpecSt || (NB >= 12 && kRows == 16), "staged spectrum: n = 12..16, 16-row generation");
+  constexpr bool kStaged = MODE == kTcSpecSt;
+  constexpr int kNBuf = kStaged ? 1 : 2;  // B operand buffers (generation runs kNBuf items ahead)
   extern __shared__ __align__(1024) uint8_t smem[];
   // full: MMA(i) done.  tmem_empty: all transform threads read D(i).
   // bfull[b]: all transform threads generated the B operand in buffer b.
   __shared__ uint64_t bar_full, bar_tmem_empty, bar_bfull[2], bar_done;
+  __shared__ uint64_t bar_st_full[kStaged ? kStSlots : 1], bar_st_empty[kStaged ? kStSlots : 1];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(16) uint32_t s_wmax[4][kSlots][kMathWarps];  // per-warp max|W| [item & 3][slot]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -479,6 +516,11 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     tc::mbar_init(&bar_bfull[0], kMathWarps * 32);
     tc::mbar_init(&bar_bfull[1], kMathWarps * 32);
     tc::mbar_init(&bar_done, kMathWarps * 32);
+    if constexpr (kStaged)
+      for (int q = 0; q < kStSlots; ++q) {
+        tc::mbar_init(&bar_st_full[q], kMathWarps * 32);
+        tc::mbar_init(&bar_st_empty[q], 1);
+      }
   }
   tc::fence_proxy_async();
   tc::fence_before();
@@ -491,10 +533,12 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kIssuerRegs));
     if (warp == 0) {
       for (int i = 0; i < n_my; ++i) {
-        tc::mbar_wait(&bar_bfull[i & 1], uint32_t((i >> 1) & 1));
+        tc::mbar_wait(&bar_bfull[i % kNBuf], uint32_t((i / kNBuf) & 1));
         if (i > 0) tc::mbar_wait(&bar_tmem_empty, uint32_t((i - 1) & 1));
         tc::fence_after();
-        issue_mma_warp(tmem, smem, i & 1, &bar_full);
+        int ibuf = i % kNBuf;
+        if constexpr (kNBuf == 1) asm volatile("mov.b32 %0, %0;" : "+r"(ibuf));  // keep descriptors in the loop
+        issue_mma_warp(tmem, smem, ibuf, &bar_full);
         if constexpr (!EMIT) {
           // bfull for item i (i >= 2) is produced after each thread stored
           // its maxima of item i - 2
@@ -511,6 +555,47 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
       }
       __syncwarp();
       tc::tmem_dealloc(tmem, 512);
+    } else if (kStaged && warp == 1 && lane == 0) {
+      // slot writer: ring position p = 32 i + j holds 8 KiB of item i's row
+      // (u_c rows 8 q .. 8 q + 7, q = j / 2 (+ 16 for odd j)), written by one
+      // bulk copy (TMA engine, async); a slot is released once the copy
+      // kStInflight positions later has been issued and its read completed
+      constexpr int P = 1 << (NB - 9);  // registers (2 P u_c rows) per component
+      int q = 0, qr = 0;
+      uint32_t ph = 0;
+      int64_t issued = 0;
+#pragma unroll 1
+      for (int il = 0; il < n_my; ++il) {
+        uint32_t vi, bp;
+        item_at<MODE, NB>(a, t_lo + il, vi, bp);
+#pragma unroll 1
+        for (int j = 0; j < 32; ++j) {
+          // position j: component slot sl, u_c rows half * P + 8 q8 .. + 7
+          const int sl = j / (P / 4), r = j % (P / 4);
+          const uint32_t v = vi | uint32_t(sl);
+          tc::mbar_wait(&bar_st_full[q], ph);
+          if (v >= a.v_lo && v < a.v_hi)
+            bulk_store(a.out + int64_t(v - a.v_lo) * a.ld + ((r & 1) * P + 8 * (r >> 1)) * 256,
+                       smem + kStOff + q * kStSlotBytes, kStSlotBytes);
+          else
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // empty group: FIFO release order
+          if (++issued > kStInflight) {
+            bulk_wait_read<kStInflight>();
+            mbar_arrive(&bar_st_empty[qr]);
+            if (++qr == kStSlots) qr = 0;
+          }
+          if (++q == kStSlots) {
+            q = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+      bulk_wait_read<0>();
+      for (int64_t k = 0; k < (issued < kStInflight ? issued : kStInflight); ++k) {
+        mbar_arrive(&bar_st_empty[qr]);
+        if (++qr == kStSlots) qr = 0;
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes complete before exit
     }
   } else {
     // ---------------- transform warps ----------------
@@ -590,7 +675,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
       else
         store_row(gs.g, smem + kBOff + buf * kBBytes, c);
     };
-    for (int k = 0; k < 2 && k < n_my; ++k) {
+    for (int k = 0; k < kNBuf && k < n_my; ++k) {
       uint32_t vn, bpn;
       item_at<MODE, NB>(a, t_lo + k, vn, bpn);
       vn |= gslot;
@@ -635,16 +720,20 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
         if (lane == 0) ring_signal(a.ring.ready + i / a.ring.L);
       }
     };
+    int st_q = 0;  // kTcSpecSt: next ring slot, its phase, and whether the ring wrapped
+    uint32_t st_ph = 0;
+    bool st_round = false;
+    (void)st_q; (void)st_ph; (void)st_round;
     for (int i = 0; i < n_my; ++i) {
       // prefetch the first plane of the item two steps ahead
-      const bool gen = i + 2 < n_my;
+      const bool gen = i + kNBuf < n_my;
       uint32_t vn = 0, bpn = 0, d = 0;
       bool reset = false;
       uint4 pa[kGW / 4];
 #pragma unroll
       for (int h = 0; h < kGW / 4; ++h) pa[h] = make_uint4(0, 0, 0, 0);
       if (gen) {
-        item_at<MODE, NB>(a, t_lo + i + 2, vn, bpn);
+        item_at<MODE, NB>(a, t_lo + i + kNBuf, vn, bpn);
         vn |= gslot;
         reset = EMIT && bpn != gs.bpcur;
         d = reset ? vn : (gs.vcur ^ vn);
@@ -670,9 +759,9 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
       };
       auto gen_store = [&]() {
         if (gen) {
-          store_b(i & 1);  // buffer i & 1 was released by MMA(i)
+          store_b(i % kNBuf);  // buffer i % kNBuf was released by MMA(i)
           tc::fence_proxy_async();
-          mbar_arrive(&bar_bfull[i & 1]);
+          mbar_arrive(&bar_bfull[i % kNBuf]);
         }
       };
       if constexpr (kC0Mma) {
@@ -866,6 +955,50 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
             }
           }
         }
+        if constexpr (kStaged) {
+          // exact W per lane into the slot ring.  Per component (slot sl,
+          // P = 2^(NB-9) registers, u_c = 2 k, 2 k + 1 for register k of the
+          // slot), steps of 4 register pairs (k, k + P/2) give 8 u_c rows of
+          // the top stage's sum half and 8 of its difference half: 32 ring
+          // positions per item for every NB; row-major 256 u_r per u_c row
+          // (each warp store is 128 contiguous bytes: no bank conflicts)
+          constexpr int P = 1 << (NB - 9);
+#pragma unroll
+          for (int qq = 0; qq < 16; ++qq) {
+            const int sl = qq / (P / 8), q8 = qq % (P / 8);
+            uint32_t lo[8], hi[8];
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint32_t x = R[sl * P + 4 * q8 + kk], y = R[sl * P + 4 * q8 + kk + P / 2];
+              const int x0 = int(x & 0xFFFFu), x1 = int(x >> 16), y0 = int(y & 0xFFFFu), y1 = int(y >> 16);
+              if constexpr (NB >= 9 + kLogRows) {  // the top stage (register k with k + P/2)
+                lo[2 * kk] = uint32_t(2 * (x0 + y0) - (1 << NB));
+                lo[2 * kk + 1] = uint32_t(2 * (x1 + y1) - (1 << NB));
+                hi[2 * kk] = uint32_t(2 * (x0 - y0));
+                hi[2 * kk + 1] = uint32_t(2 * (x1 - y1));
+              } else {  // n = 12: the GEMM output is final (u_c 2k, 2k+1 of register k)
+                lo[2 * kk] = uint32_t(2 * x0 - (1 << NB));
+                lo[2 * kk + 1] = uint32_t(2 * x1 - (1 << NB));
+                hi[2 * kk] = uint32_t(2 * y0 - (1 << NB));
+                hi[2 * kk + 1] = uint32_t(2 * y1 - (1 << NB));
+              }
+            }
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              if (st_round) tc::mbar_wait(&bar_st_empty[st_q], st_ph ^ 1u);
+              uint32_t* slot = reinterpret_cast<uint32_t*>(smem + kStOff + st_q * kStSlotBytes) + u;
+#pragma unroll
+              for (int e = 0; e < 8; ++e) slot[e * 256] = half ? hi[e] : lo[e];
+              tc::fence_proxy_async();  // generic-proxy writes -> the bulk copy (async proxy)
+              mbar_arrive(&bar_st_full[st_q]);
+              if (++st_q == kStSlots) {
+                st_q = 0;
+                st_ph ^= 1u;
+                st_round = true;
+              }
+            }
+          }
+        }
         if constexpr (MODE == kTcSpec && NB == 16) {
           // exact W of the top stage per lane (the packed S / D above may wrap
           // at |W| = 2^16), stored at u = u_c * 256 + u_r with
@@ -999,14 +1132,14 @@ int run_tc_hybrid(const TcArgs& a, int64_t items, cudaStream_t st, int grid_over
   static unsigned long long attr_done = 0;  // per device; the call is idempotent
   if (!(attr_done >> (dp.device & 63) & 1ull)) {
     SBW_CUDA_CHECK(cudaFuncSetAttribute(k_tc_hybrid<MODE, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        kTcSmem));
+                                        MODE == kTcSpecSt ? kTcSmemSt : kTcSmem));
     attr_done |= 1ull << (dp.device & 63);
   }
   TcArgs args = a;
   if (int rc = tc_consts(dp.device, st, &args.consts)) return rc;
   const int grid = grid_override > 0 ? grid_override : int(items < dp.sm_count ? items : dp.sm_count);
-  k_tc_hybrid<MODE, NB><<<grid, kAllThreads, kTcSmem, st>>>(args);
-  SBW_LAUNCH_CHECK(is_emit(MODE) ? "k_tc_hybrid<emit>" : (MODE == kTcSpec ? "k_tc_hybrid<spec>" : "k_tc_hybrid<nl>"));
+  k_tc_hybrid<MODE, NB><<<grid, kAllThreads, MODE == kTcSpecSt ? kTcSmemSt : kTcSmem, st>>>(args);
+  SBW_LAUNCH_CHECK(is_emit(MODE) ? "k_tc_hybrid<emit>" : (is_spec(MODE) ? "k_tc_hybrid<spec>" : "k_tc_hybrid<nl>"));
   return SBW_OK;
 }
 }  // namespace
@@ -1051,6 +1184,13 @@ int launch_tc_nl_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t v_
   }
 }
 
+// staged spectrum epilogue (bulk copies of 8 KiB slots) when the rows are
+// 16-byte aligned; SBW_SPEC_STAGE=0 keeps the per-lane store epilogue (A/B)
+bool spec_staged_ok(const int32_t* out, int64_t ld) {
+  static const bool on = !(getenv("SBW_SPEC_STAGE") && atoi(getenv("SBW_SPEC_STAGE")) == 0);
+  return on && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && (ld & 3) == 0;
+}
+
 int launch_tc_spec_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
                          int32_t* out, int64_t ld, cudaStream_t st) {
   TcArgs a{};
@@ -1066,7 +1206,11 @@ int launch_tc_spec_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t 
   switch (n) {
 #define SBW_TC_SPEC_CASE(N)                                                             \
     case N:                                                                             \
-      if constexpr (8 + kLogRows <= N) return run_tc_hybrid<kTcSpec, N>(a, items, st); \
+      if constexpr (8 + kLogRows <= N) {                                                \
+        if constexpr (kRows == 16 && N >= 12)                                           \
+          if (spec_staged_ok(out, ld)) return run_tc_hybrid<kTcSpecSt, N>(a, items, st); \
+        return run_tc_hybrid<kTcSpec, N>(a, items, st);                                 \
+      }                                                                                 \
       return set_error(SBW_EINVAL, "row-group generation needs n >= %d", 8 + kLogRows);
     SBW_TC_SPEC_CASE(11)
     SBW_TC_SPEC_CASE(12)
@@ -1089,6 +1233,7 @@ int launch_tc16_spec(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32
   a.max_abs = max_abs;
   a.out = out;
   a.ld = ld;
+  if (kRows == 16 && spec_staged_ok(out, ld)) return run_tc_hybrid<kTcSpecSt>(a, int64_t(v_hi) - v_lo, st);
   return run_tc_hybrid<kTcSpec>(a, int64_t(v_hi) - v_lo, st);
 }
 
