@@ -102,7 +102,7 @@ def spectrum_device(s: SBox, v_lo: int = 1, v_hi: int | None = None, layout: str
 STREAM_THRESHOLD_BYTES = 1 << 30
 
 
-def device_to_host_chunked(src, out: np.ndarray, chunk_bytes: int = 256 << 20) -> np.ndarray:
+def device_to_host_chunked(src, out: np.ndarray, chunk_bytes: int = 128 << 20) -> np.ndarray:
     """Copy a contiguous 2-D device tensor into the host array `out` (same
     shape and dtype) through two pinned staging chunks: the device -> host
     DMA of chunk i overlaps the multi-threaded copy of chunk i - 1 into
@@ -136,13 +136,17 @@ def device_to_host_chunked(src, out: np.ndarray, chunk_bytes: int = 256 << 20) -
 
 
 def spectrum_to_host(s: SBox, v_lo: int = 1, v_hi: int | None = None, layout: str = "mask",
-                     out: np.ndarray | None = None, chunk_bytes: int = 512 << 20,
+                     out: np.ndarray | None = None, chunk_bytes: int = 128 << 20,
                      device=None) -> tuple[np.ndarray, np.ndarray]:
     """Materialise W for masks [v_lo, v_hi) into a host array, chunk by chunk.
 
     Device memory stays at two chunk buffers regardless of the spectrum size
     (16 GiB at 16x16): chunk i+1 is computed on one stream while chunk i is
-    copied device->host (pinned staging) on the other.  layout "mask" fills
+    copied device->host (pinned staging) on the other.  128 MiB chunks: the
+    pinned staging costs ~0.5 s per GiB to allocate the first time in a
+    process, and smaller chunks keep the same steady rate (16x16, 17.2 GB:
+    512 MiB chunks 1.13 s first call / 0.54 s after, 128 MiB 0.77 / 0.54 s,
+    32 MiB 0.76 / 0.69 s; tools/host_chunk_probe.py).  layout "mask" fills
     out[v - v_lo][u]; layout "x" fills out[u][v - v_lo] (the reference's
     x-major store, walsh.py:117-131).  Returns (out, max_abs int32 per mask).
     """
