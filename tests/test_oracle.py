@@ -175,3 +175,26 @@ def test_xmajor_oracle_matches_reference():
         assert sha(orc.xmajor_spectrum_typed(wt)) == rec["sha_spectrum_xmajor"]
     for pw, mx, nl in meta["column_nonlinearity"]:
         assert orc.column_nl(pw, mx) == nl
+
+
+@pytest.mark.parametrize("name,masks", [("20x20", (1, 2, 3, 334146, 1048575)), ("24x16", (1, 27804, 65535))])
+def test_full_large_config_goldens(name, masks):
+    """The oracle against the reference's full per-component maxima of the two
+    large configs (tests/golden/full_<name>.npz, make_golden_full.py): the
+    overall NL / argmin and a few components including the argmin."""
+    import json
+    import os
+
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    if not os.path.exists(os.path.join(here, "full_maxima.json")):
+        pytest.skip("tests/golden/full_maxima.json not generated yet (tests/golden/make_golden_full.py)")
+    g = json.load(open(os.path.join(here, "full_maxima.json")))["configs"][name]
+    full = np.load(os.path.join(here, f"full_{name}.npz"))["max_abs"].astype(np.int64)
+    n, m, bij = CFG[name]
+    assert full.shape == ((1 << m) - 1,)
+    values = ((1 << n) - full) >> 1
+    assert sha(values) == g["sha_maxima_i64"]
+    assert orc.nl_from_maxima(values) == (g["nl"], g["argmin_v"])
+    t = orc.gen_table(n, m, 0, bij)
+    for v in masks:
+        assert int(orc.component_max_abs(t, n, v, v + 1)[0]) == int(full[v - 1]), v
