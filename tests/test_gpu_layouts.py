@@ -90,3 +90,30 @@ def test_16x16_full_matrix_hashes_both_layouts():
     assert h.hexdigest() == g["sha256_x_major"]
     r = sw.nonlinearity_from_maxima(sw.ColumnMaxima(16, 16, sw.walsh.maxabs_to_nl(mx, 16)))
     assert (r.value, r.argmin_v) == (g["nl"], g["argmin_v"])
+
+
+@pytest.mark.parametrize("n,v_lo,count", [(12, 1, 300), (13, 77, 37), (16, 44801, 40)])
+def test_staged_and_per_lane_spectrum_epilogues_agree(n, v_lo, count):
+    """sbw_spectrum takes the staged epilogue (shared-memory slot ring + bulk
+    copies) for 16-byte aligned rows and the per-lane store epilogue otherwise
+    (here: ld = 2^n + 2).  Both must give the oracle's rows."""
+    import torch
+
+    from paper_1912_03732_b200 import device as d
+
+    s = sw.generate_sbox(n, n, seed=n, bijective=True)
+    lib = d.load_library()
+    dev = torch.device("cuda", 0)
+    tab = d.device_table(s, dev)
+    want = orc.spectrum(s.table, n, v_lo, v_lo + count)
+    for ld in (1 << n, (1 << n) + 2):
+        out = torch.full((count, ld), -7, dtype=torch.int32, device=dev)
+        mx = torch.empty(count, dtype=torch.int32, device=dev)
+        sb = lib.sbw_spectrum_scratch_bytes(n, n, v_lo, v_lo + count, d.LAYOUT_MASK_MAJOR)
+        scratch = torch.empty(max(1, sb), dtype=torch.uint8, device=dev)
+        d.check(lib.sbw_spectrum(d.ptr(tab), d.table_bytes(n), n, n, v_lo, v_lo + count, d.LAYOUT_MASK_MAJOR,
+                                 d.ptr(out), ld, d.ptr(mx), d.ptr(scratch), sb, d.stream_handle(dev)))
+        got = out.cpu().numpy()
+        assert np.array_equal(got[:, : 1 << n], want), ld
+        assert (got[:, 1 << n:] == -7).all(), ld  # the padding is never written
+        assert np.array_equal(mx.cpu().numpy(), np.abs(want).max(axis=1)), ld
