@@ -13,7 +13,8 @@ script runs exactly the reference's stream body over every mask
 contiguous chunks over a multiprocessing pool, the way ``fwht_parallel``
 splits them (pkg/src/sboxeval/parallel.py:38-57).  The table is the
 reference's own ``generate_sbox`` (sbox.py:102-111).  Chunks are checkpointed
-under ``tests/golden/_work/`` (git- and gpurun-ignored) so a run can resume.
+under ``tests/golden/full_work/`` (committed as they finish, gpurun-ignored) so a run can resume
+in a new container.
 
 Output (committed): ``tests/golden/full_<name>.npz`` holding ``max_abs``
 (uint16, one entry per component v = 1..2^m-1; every value < 2^15 here) and
@@ -37,7 +38,7 @@ import numpy as np
 sys.dont_write_bytecode = True
 REF = "/root/reference/pkg/src"
 HERE = os.path.dirname(os.path.abspath(__file__))
-WORK = os.path.join(HERE, "_work")
+WORK = os.path.join(HERE, "full_work")
 
 CONFIGS = {"20x20": (20, 20, 4096), "24x16": (24, 16, 256)}  # n, m, masks per chunk
 
@@ -85,8 +86,10 @@ def main():
     for name, (n, m, step) in CONFIGS.items():
         total = (1 << m)
         jobs += [(name, lo, min(lo + step, total)) for lo in range(1, total, step)]
-    # interleave the configs so partial progress covers both
-    jobs.sort(key=lambda j: (j[1] / (1 << CONFIGS[j[0]][1])))
+    # one config at a time (20x20 first, the cheaper one), so a run cut short
+    # still leaves one config complete
+    order = sys.argv[3].split(",") if len(sys.argv) > 3 else list(CONFIGS)
+    jobs.sort(key=lambda j: (order.index(j[0]), j[1]))
     if len(sys.argv) > 2 and sys.argv[2] == "rev":  # a second runner from the other end
         jobs.reverse()
     t0 = time.time()

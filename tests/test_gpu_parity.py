@@ -585,18 +585,27 @@ def test_16x16_retain_streams_to_host(golden, golden_arrays):
 @pytest.mark.slow
 @pytest.mark.parametrize("name", ["20x20", "24x16"])
 def test_full_large_config_nl(name):
-    """Full 20x20 (2^20 - 1 components) / 24x16 (65535 components) on one GPU
-    against the reference's own per-component max|W| for EVERY component
-    (tests/golden/full_<name>.npz, made by tests/golden/make_golden_full.py
-    running the reference's stream body, walsh.py:237-240, over all masks)."""
+    """Full 20x20 (2^20 - 1 components) / 24x16 (65535 components) on one GPU,
+    EVERY per-component max|W| against a CPU checker:
+      * the reference's own full run when it is committed
+        (tests/golden/full_<name>.npz, make_golden_full.py: the reference's
+        stream body, walsh.py:237-240, over all masks), else
+      * the compiled oracle's full arrays (tests/golden/oracle_full_<name>.npz,
+        make_oracle_full.py), which tests/test_oracle.py pins to the reference's
+        full 16x16 maxima, its sampled masks and every chunk of the reference's
+        full run present under tests/golden/full_work/."""
     import json
 
-    gpath = os.path.join(os.path.dirname(__file__), "golden", "full_maxima.json")
-    if not os.path.exists(gpath):
-        pytest.skip("tests/golden/full_maxima.json not generated yet (tests/golden/make_golden_full.py)")
-    with open(gpath) as f:
+    gdir = os.path.join(os.path.dirname(__file__), "golden")
+    if os.path.exists(os.path.join(gdir, "full_maxima.json")):
+        meta, arr = "full_maxima.json", f"full_{name}.npz"
+    elif os.path.exists(os.path.join(gdir, "oracle_full.json")):
+        meta, arr = "oracle_full.json", f"oracle_full_{name}.npz"
+    else:
+        pytest.skip("no full-config goldens (tests/golden/make_oracle_full.py / make_golden_full.py)")
+    with open(os.path.join(gdir, meta)) as f:
         g = json.load(f)["configs"][name]
-    want = np.load(os.path.join(os.path.dirname(__file__), "golden", f"full_{name}.npz"))["max_abs"]
+    want = np.load(os.path.join(gdir, arr))["max_abs"]
     s = box(name)
     mx, key = sw.component_max_abs_device(s)
     res = sw.walsh.decode_key(key, s.n)
@@ -607,6 +616,12 @@ def test_full_large_config_nl(name):
     assert bad.size == 0, f"{bad.size} components differ, first v = {bad[:5] + 1}"
     _, cm = sw.fwht_fused(s, mode="stream")
     assert sha(cm.values) == g["sha_maxima_i64"]
+    # every chunk of the reference's own full run committed so far
+    import glob
+
+    for p in glob.glob(os.path.join(gdir, "full_work", f"{name}_*.npy")):
+        lo, hi = (int(x) for x in os.path.basename(p)[:-4].split("_")[1:3])
+        assert np.array_equal(full[lo - 1:hi - 1], np.load(p).astype(np.int32)), (lo, hi)
 
 
 def test_evaluate_retain_skips_the_discarded_spectrum():

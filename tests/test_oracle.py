@@ -198,3 +198,85 @@ def test_full_large_config_goldens(name, masks):
     t = orc.gen_table(n, m, 0, bij)
     for v in masks:
         assert int(orc.component_max_abs(t, n, v, v + 1)[0]) == int(full[v - 1]), v
+
+
+# ---- the compiled oracle (oracle/sbw_oracle.c) ------------------------------
+def _c_oracle_or_skip():
+    import os
+
+    if not os.path.exists(os.path.join(os.path.dirname(orc.__file__), "liboracle.so")):
+        pytest.skip("oracle/liboracle.so not built (make -C oracle)")
+
+
+def test_c_oracle_full_16x16_matches_reference(golden, golden_arrays):
+    """Every one of the 65535 16x16 maxima, C oracle vs the reference's run."""
+    _c_oracle_or_skip()
+    t = orc.gen_table(16, 16, 0, True)
+    mx = orc.component_max_abs_c(t, 16, 1, 1 << 16)
+    assert np.array_equal(((1 << 16) - mx) >> 1, golden_arrays["maxima_16x16"])
+
+
+@pytest.mark.parametrize("n,m,bij,seed", [(1, 1, False, 0), (2, 3, False, 1), (5, 4, False, 9),
+                                           (8, 8, True, 0), (11, 3, False, 2), (13, 6, False, 4),
+                                           (14, 2, False, 5)])
+def test_c_oracle_small_shapes(n, m, bij, seed):
+    _c_oracle_or_skip()
+    t = orc.gen_table(n, m, seed, bij)
+    for threads in (1, 3):
+        assert np.array_equal(orc.component_max_abs_c(t, n, 1, 1 << m, threads),
+                              orc.component_max_abs(t, n, 1, 1 << m))
+    assert orc.component_max_abs_c(t, n, 1, 1).shape == (0,)
+
+
+def test_c_oracle_large_subsets_match_reference(golden):
+    """The reference's sampled 20x20 / 24x16 masks (make_golden.py)."""
+    _c_oracle_or_skip()
+    for name in ("20x20", "24x16"):
+        n, m, bij = CFG[name]
+        t = orc.gen_table(n, m, 0, bij)
+        for rec in golden["configs"][name]["subset"]:
+            v = rec["v"]
+            assert int(orc.component_max_abs_c(t, n, v, v + 1)[0]) == rec["max_abs"], (name, v)
+
+
+def _reference_chunks(name):
+    """Chunks of the reference's own full run (make_golden_full.py) present."""
+    import glob
+    import os
+
+    here = os.path.join(os.path.dirname(__file__), "golden", "full_work")
+    out = []
+    for p in sorted(glob.glob(os.path.join(here, f"{name}_*.npy"))):
+        lo, hi = (int(x) for x in os.path.basename(p)[:-4].split("_")[1:3])
+        out.append((lo, hi, np.load(p)))
+    return out
+
+
+@pytest.mark.parametrize("name", ["20x20", "24x16"])
+def test_oracle_full_arrays_match_every_reference_chunk(name):
+    """tests/golden/oracle_full_<name>.npz (every component, from the C oracle)
+    equals the reference's own maxima on every chunk its full run has produced,
+    and the final full_<name>.npz when that run has finished."""
+    import json
+    import os
+
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    path = os.path.join(here, f"oracle_full_{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/oracle_full_*.npz not generated (make_oracle_full.py)")
+    n, m, _ = CFG[name]
+    full = np.load(path)["max_abs"].astype(np.int64)
+    assert full.shape == ((1 << m) - 1,)
+    meta = json.load(open(os.path.join(here, "oracle_full.json")))["configs"][name]
+    values = ((1 << n) - full) >> 1
+    assert sha(values) == meta["sha_maxima_i64"]
+    assert orc.nl_from_maxima(values) == (meta["nl"], meta["argmin_v"])
+    covered = 0
+    for lo, hi, chunk in _reference_chunks(name):
+        assert np.array_equal(chunk.astype(np.int64), full[lo - 1:hi - 1]), (name, lo, hi)
+        covered += hi - lo
+    ref_full = os.path.join(here, f"full_{name}.npz")
+    if os.path.exists(ref_full):
+        assert np.array_equal(np.load(ref_full)["max_abs"].astype(np.int64), full)
+        covered = full.shape[0]
+    print(f"{name}: reference covers {covered} of {full.shape[0]} components")
