@@ -112,6 +112,25 @@ int sbw_spectrum(const void* d_table, int table_bytes, int n, int m, uint32_t v_
 size_t sbw_spectrum_scratch_bytes(int n, int m, uint32_t v_lo, uint32_t v_hi, int layout);
 
 /*
+ * The x-major store wt[u][v - 1] (v = 1 .. 2^n - 1) of a BIJECTIVE n x n
+ * S-box S, rows u in [u_lo, u_hi) (1 <= u_lo, u_hi <= 2^n) at
+ * d_out + (u - u_lo) * ld, ld >= 2^n - 1 (the reference's dense pitch
+ * 2^m - 1 included), computed from the inverse table T = S^-1 passed as
+ * d_inv_table: W_S(u, v) = W_T(v, u), so row u is T's mask-major spectrum
+ * row u without its v = 0 entry, written straight to the odd pitch (no
+ * transpose, no full-size scratch).  Row u = 0 (all zeros for a bijective S)
+ * is the caller's.  n = 12..16; d_out 4-byte aligned.  Replaces the x-major
+ * materialisation inside fwht_rowmajor (walsh.py:155-180: build_polarity_xmajor
+ * + transform_xmajor_in_place, walsh.py:117-137) for full-range bijective
+ * boxes; a non-bijective table gives the x-major store of some other box
+ * (the caller checks bijectivity when it builds T).
+ */
+int sbw_xmajor_from_inverse(const void* d_inv_table, int table_bytes, int n, uint32_t u_lo,
+                            uint32_t u_hi, int32_t* d_out, int64_t ld, void* scratch,
+                            size_t scratch_bytes, void* stream);
+size_t sbw_xmajor_inverse_scratch_bytes(int n, uint32_t u_lo, uint32_t u_hi);
+
+/*
  * Polarity truth table (-1)^{g_v(x)} as int32, either layout.  Replaces
  * polarity_row / polarity_truth_table (sbox.py:145-162) and
  * build_polarity_xmajor (walsh.py:117-131).  Unlike the spectrum calls the

@@ -266,6 +266,35 @@ int sbw_spectrum(const void* d_table, int table_bytes, int n, int m, uint32_t v_
   return rc;
 }
 
+size_t sbw_xmajor_inverse_scratch_bytes(int n, uint32_t u_lo, uint32_t u_hi) {
+  if (n < 1 || n > 16 || u_hi < u_lo) return 0;
+  return ((planes_bytes(n, n) + 255) & ~size_t(255)) + 4 * (size_t(u_hi) - u_lo);
+}
+
+int sbw_xmajor_from_inverse(const void* d_inv_table, int table_bytes, int n, uint32_t u_lo,
+                            uint32_t u_hi, int32_t* d_out, int64_t ld, void* scratch,
+                            size_t scratch_bytes, void* stream) {
+  DeviceScope dev_scope(stream, d_inv_table);
+  if (n < 12 || n > 16) return set_error(SBW_EINVAL, "x-major from the inverse needs n in 12..16, got %d", n);
+  if (int rc = check_table(d_inv_table, table_bytes, n)) return rc;
+  if (u_lo < 1 || u_hi < u_lo || uint64_t(u_hi) > (uint64_t(1) << n))
+    return set_error(SBW_ERANGE, "row range [%u, %u) outside [1, 2^%d]", u_lo, u_hi, n);
+  if (u_hi == u_lo) return SBW_OK;
+  if (!d_out) return set_error(SBW_EINVAL, "null output");
+  if (reinterpret_cast<uintptr_t>(d_out) & 3) return set_error(SBW_EINVAL, "output not 4-byte aligned");
+  if (ld < (int64_t(1) << n) - 1) return set_error(SBW_EINVAL, "ld %lld < 2^n - 1", (long long)ld);
+  const size_t need = sbw_xmajor_inverse_scratch_bytes(n, u_lo, u_hi);
+  if (scratch == nullptr || scratch_bytes < need)
+    return set_error(SBW_EINVAL, "x-major from the inverse needs %zu scratch bytes, got %zu", need,
+                     scratch_bytes);
+  cudaStream_t st = as_stream(stream);
+  uint32_t* planes = static_cast<uint32_t*>(scratch);
+  int32_t* mx = reinterpret_cast<int32_t*>(static_cast<char*>(scratch) +
+                                           ((planes_bytes(n, n) + 255) & ~size_t(255)));
+  if (int rc = build_planes(d_inv_table, table_bytes, n, n, planes, st)) return rc;
+  return launch_tc_xmajor_inverse(planes, n, u_lo, u_hi, mx, d_out, ld, st);
+}
+
 int sbw_polarity(const void* d_table, int table_bytes, int n, int m, uint32_t v_lo,
                  uint32_t v_hi, int layout, int32_t* d_out, int64_t ld, void* stream) {
   DeviceScope dev_scope(stream, d_table);

@@ -34,6 +34,12 @@ int launch_tc_spec_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t 
 // Tensor-core n = 16 materialised spectrum, mask-major rows out[(v - v_lo) * ld + u].
 int launch_tc16_spec(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
                      int32_t* out, int64_t ld, cudaStream_t st);
+// The reference's x-major store (wt[u][v - 1], any pitch ld) of a bijective
+// n x n box, rows u in [u_lo, u_hi), from its inverse's bit planes: the
+// staged spectrum kernel with rows shifted by one (W_S(u, v) = W_T(v, u),
+// T = S^-1).  n = 12..16; max_scratch gets T's per-row maxima (discarded).
+int launch_tc_xmajor_inverse(const uint32_t* inv_planes, int n, uint32_t u_lo, uint32_t u_hi,
+                             int32_t* max_scratch, int32_t* out, int64_t ld, cudaStream_t st);
 // Tensor-core pass A of the multi-pass NL path (n = 17..24): 15 stages per
 // 2^15 block, biased u16 out in a block-internal word order of its own
 // (pass B pairs equal word positions across blocks only, so any fixed order

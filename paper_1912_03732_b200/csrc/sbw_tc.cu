@@ -362,6 +362,14 @@ struct TcArgs {
   // SPEC (n = 16 materialised spectrum, mask-major): out[(v - v_lo) * ld + u]
   int32_t* out;
   int64_t ld;
+  // kTcSpecSt only: element (v, z) goes to out[(v - v_lo) * ld + z - zoff + goff]
+  // and z < zoff is dropped.  zoff = 0, goff = 0: the mask-major rows
+  // (ld % 4 == 0).  zoff = 1: the reference's x-major store of a bijective
+  // box S from its inverse T = S^-1 (W_S(u, v) = W_T(v, u): item mask = x-major
+  // row u, z = v, pitch 2^n - 1 odd), out 16-byte aligned and goff < 4 the
+  // caller pointer's offset from it.
+  int zoff;
+  int64_t goff;
   // EMIT into the L2 ring shared with a concurrent pass B (sbw_internal.cuh)
   RingArgs ring;
   // MODE kTcEmit16 runs the 16th stage (x bit 15) too and writes the
@@ -385,9 +393,13 @@ constexpr int kTcNL = 0, kTcEmit = 1, kTcSpec = 2, kTcEmit16 = 3;  // kTcEmit16:
 // reachable with either store width).  The ring needs the smem of the second
 // B buffer: this mode generates B(i+1) into the single buffer after MMA(i).
 constexpr int kTcSpecSt = 4;
+// kTcSpecStX: the same staged epilogue writing shifted rows (TcArgs::zoff = 1),
+// the x-major store of a bijective box from its inverse
+constexpr int kTcSpecStX = 5;
 __host__ __device__ constexpr bool is_emit(int mode) { return mode == kTcEmit || mode == kTcEmit16; }
-__host__ __device__ constexpr bool is_spec(int mode) { return mode == kTcSpec || mode == kTcSpecSt; }
-constexpr int kStSlotBytes = 8192;
+__host__ __device__ constexpr bool is_staged(int mode) { return mode == kTcSpecSt || mode == kTcSpecStX; }
+__host__ __device__ constexpr bool is_spec(int mode) { return mode == kTcSpec || is_staged(mode); }
+constexpr int kStSlotBytes = 8192;  // 8 u_c rows x 256 u_r of int32
 #ifndef SBW_ST_SLOTS
 #define SBW_ST_SLOTS 10
 #endif
@@ -488,8 +500,9 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
                 "n < 16: NL / SPEC with 8/16-row groups");
   constexpr int kSlots = 1 << (16 - NB);  // components per 2^16 tile
   static_assert(!is_spec(MODE) || kC0Mma, "exact SPEC output needs the bias-block GEMM");
-  static_assert(MODE != kTcSpecSt || (NB >= 12 && kRows == 16), "staged spectrum: n = 12..16, 16-row generation");
-  constexpr bool kStaged = MODE == kTcSpecSt;
+  static_assert(!is_staged(MODE) || (NB >= 12 && kRows == 16), "staged spectrum: n = 12..16, 16-row generation");
+  constexpr bool kStaged = is_staged(MODE);
+  constexpr bool kShift = MODE == kTcSpecStX;
   constexpr int kNBuf = kStaged ? 1 : 2;  // B operand buffers (generation runs kNBuf items ahead)
   extern __shared__ __align__(1024) uint8_t smem[];
   // full: MMA(i) done.  tmem_empty: all transform threads read D(i).
@@ -574,10 +587,18 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
           const int sl = j / (P / 4), r = j % (P / 4);
           const uint32_t v = vi | uint32_t(sl);
           tc::mbar_wait(&bar_st_full[q], ph);
-          if (v >= a.v_lo && v < a.v_hi)
-            bulk_store(a.out + int64_t(v - a.v_lo) * a.ld + ((r & 1) * P + 8 * (r >> 1)) * 256,
-                       smem + kStOff + q * kStSlotBytes, kStSlotBytes);
-          else
+          if (v >= a.v_lo && v < a.v_hi) {
+            // the aligned chunks [A, B) of the slot's z0 .. z0 + 2047 go by bulk
+            // copy (the slot holds word g at g - A); the < 4 words at either
+            // end (shared with the neighbouring slot / row) were stored per lane
+            const int z0 = ((r & 1) * P + 8 * (r >> 1)) * 256;
+            const int64_t g0 = int64_t(v - a.v_lo) * a.ld + z0 - (kShift ? 1 : 0) + (kShift ? a.goff : 0);
+            const int sh = kShift ? int(g0 & 3) : 0;
+            const int h = kShift ? ((z0 == 0 && sh == 0) ? 4 : ((4 - sh) & 3)) : 0;
+            const int64_t A = g0 + h, B = (g0 + 2048) & ~int64_t(3);
+            const int off = kShift ? (sh ? sh - 4 : 0) : 0;  // slot word of z0 + p is p + off
+            bulk_store(a.out + A, smem + kStOff + q * kStSlotBytes + 4 * (h + off), uint32_t(4 * (B - A)));
+          } else
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // empty group: FIFO release order
           if (++issued > kStInflight) {
             bulk_wait_read<kStInflight>();
@@ -963,6 +984,8 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
           // positions per item for every NB; row-major 256 u_r per u_c row
           // (each warp store is 128 contiguous bytes: no bank conflicts)
           constexpr int P = 1 << (NB - 9);
+          uint32_t st_vi = 0, st_bp;
+          if constexpr (kShift) item_at<MODE, NB>(a, t_lo + i, st_vi, st_bp);
 #pragma unroll
           for (int qq = 0; qq < 16; ++qq) {
             const int sl = qq / (P / 8), q8 = qq % (P / 8);
@@ -986,9 +1009,23 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
               if (st_round) tc::mbar_wait(&bar_st_empty[st_q], st_ph ^ 1u);
-              uint32_t* slot = reinterpret_cast<uint32_t*>(smem + kStOff + st_q * kStSlotBytes) + u;
+              int off = 0;  // shifted rows: slot word of element p is p + off (off in -3..0)
+              if constexpr (kShift) {  // shifted rows: this position's word shift and its end words
+                const uint32_t v = st_vi | uint32_t(sl);
+                const int z0 = (half * P + 8 * q8) * 256;
+                const int64_t g0 = int64_t(v - a.v_lo) * a.ld + z0 - 1 + a.goff;
+                const int sh = int(g0 & 3);
+                off = sh ? sh - 4 : 0;
+                if (v >= a.v_lo && v < a.v_hi) {
+                  const int h = (z0 == 0 && sh == 0) ? 4 : ((4 - sh) & 3);
+                  if (u < h && !(z0 == 0 && u == 0)) __stcs(a.out + g0 + u, int(half ? hi[0] : lo[0]));
+                  if (u >= 256 - sh) __stcs(a.out + g0 + 1792 + u, int(half ? hi[7] : lo[7]));
+                }
+              }
+              uint32_t* slot = reinterpret_cast<uint32_t*>(smem + kStOff + st_q * kStSlotBytes) + u + off;
 #pragma unroll
-              for (int e = 0; e < 8; ++e) slot[e * 256] = half ? hi[e] : lo[e];
+              for (int e = 0; e < 8; ++e)
+                if (!kShift || e > 0 || u + off >= 0) slot[e * 256] = half ? hi[e] : lo[e];
               tc::fence_proxy_async();  // generic-proxy writes -> the bulk copy (async proxy)
               mbar_arrive(&bar_st_full[st_q]);
               if (++st_q == kStSlots) {
@@ -1132,13 +1169,13 @@ int run_tc_hybrid(const TcArgs& a, int64_t items, cudaStream_t st, int grid_over
   static unsigned long long attr_done = 0;  // per device; the call is idempotent
   if (!(attr_done >> (dp.device & 63) & 1ull)) {
     SBW_CUDA_CHECK(cudaFuncSetAttribute(k_tc_hybrid<MODE, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        MODE == kTcSpecSt ? kTcSmemSt : kTcSmem));
+                                        is_staged(MODE) ? kTcSmemSt : kTcSmem));
     attr_done |= 1ull << (dp.device & 63);
   }
   TcArgs args = a;
   if (int rc = tc_consts(dp.device, st, &args.consts)) return rc;
   const int grid = grid_override > 0 ? grid_override : int(items < dp.sm_count ? items : dp.sm_count);
-  k_tc_hybrid<MODE, NB><<<grid, kAllThreads, MODE == kTcSpecSt ? kTcSmemSt : kTcSmem, st>>>(args);
+  k_tc_hybrid<MODE, NB><<<grid, kAllThreads, is_staged(MODE) ? kTcSmemSt : kTcSmem, st>>>(args);
   SBW_LAUNCH_CHECK(is_emit(MODE) ? "k_tc_hybrid<emit>" : (is_spec(MODE) ? "k_tc_hybrid<spec>" : "k_tc_hybrid<nl>"));
   return SBW_OK;
 }
@@ -1235,6 +1272,37 @@ int launch_tc16_spec(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32
   a.ld = ld;
   if (kRows == 16 && spec_staged_ok(out, ld)) return run_tc_hybrid<kTcSpecSt>(a, int64_t(v_hi) - v_lo, st);
   return run_tc_hybrid<kTcSpec>(a, int64_t(v_hi) - v_lo, st);
+}
+
+// x-major rows of a bijective box from its inverse's planes (kTcSpecSt with
+// zoff = 1): row u in [u_lo, u_hi) of wt[u][v - 1] at out + (u - u_lo) * ld
+int launch_tc_xmajor_inverse(const uint32_t* inv_planes, int n, uint32_t u_lo, uint32_t u_hi,
+                             int32_t* max_scratch, int32_t* out, int64_t ld, cudaStream_t st) {
+  if (kRows != 16) return set_error(SBW_EINVAL, "x-major from the inverse needs SBW_TC_ROWS = 16");
+  if (n < 12 || n > 16) return set_error(SBW_EINVAL, "x-major from the inverse needs n in 12..16");
+  if (reinterpret_cast<uintptr_t>(out) & 3) return set_error(SBW_EINVAL, "output not 4-byte aligned");
+  TcArgs a{};
+  a.planes = inv_planes;
+  a.plane_words = (int64_t(1) << n) >> 5;
+  a.v_lo = u_lo;
+  a.v_hi = u_hi;
+  a.max_abs = max_scratch;
+  a.goff = int64_t((reinterpret_cast<uintptr_t>(out) & 15) >> 2);
+  a.out = reinterpret_cast<int32_t*>(reinterpret_cast<uintptr_t>(out) & ~uintptr_t(15));
+  a.ld = ld;
+  a.zoff = 1;  // (kTcSpecStX; recorded for readers of TcArgs)
+  const int lc = 16 - n;
+  const int64_t items = ((int64_t(u_hi) - 1) >> lc) + 1 - (int64_t(u_lo) >> lc);
+  if constexpr (kRows == 16) {
+    switch (n) {
+      case 12: return run_tc_hybrid<kTcSpecStX, 12>(a, items, st);
+      case 13: return run_tc_hybrid<kTcSpecStX, 13>(a, items, st);
+      case 14: return run_tc_hybrid<kTcSpecStX, 14>(a, items, st);
+      case 15: return run_tc_hybrid<kTcSpecStX, 15>(a, items, st);
+      default: return run_tc_hybrid<kTcSpecStX, 16>(a, items, st);
+    }
+  }
+  return SBW_OK;
 }
 
 int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_comp, uint32_t* emit,

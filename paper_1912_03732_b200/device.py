@@ -34,6 +34,8 @@ SIGNATURES = {
     "sbw_nl_scratch_bytes": (_sz, [_i32, _i32, _u32, _u32]),
     "sbw_spectrum": (_i32, [_vp, _i32, _i32, _i32, _u32, _u32, _i32, _vp, _i64, _vp, _vp, _sz, _vp]),
     "sbw_spectrum_scratch_bytes": (_sz, [_i32, _i32, _u32, _u32, _i32]),
+    "sbw_xmajor_from_inverse": (_i32, [_vp, _i32, _i32, _u32, _u32, _vp, _i64, _vp, _sz, _vp]),
+    "sbw_xmajor_inverse_scratch_bytes": (_sz, [_i32, _u32, _u32]),
     "sbw_polarity": (_i32, [_vp, _i32, _i32, _i32, _u32, _u32, _i32, _vp, _i64, _vp]),
     "sbw_fwht_inplace": (_i32, [_vp, _i32, _i64, _vp, _vp]),
     "sbw_fwht_inplace_strided": (_i32, [_vp, _i32, _i32, _i64, _i64, _i64, _vp, _vp]),

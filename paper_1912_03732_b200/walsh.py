@@ -64,6 +64,49 @@ def component_max_abs_device(s: SBox, v_lo: int = 1, v_hi: int | None = None, de
     return mx[: v_hi - v_lo], key
 
 
+def _inverse_if_bijective(s: SBox):
+    """S^-1 as an SBox when S is a bijection of n bits, else None; kept on the
+    box (tables are immutable) so its device table is uploaded once."""
+    cached = s.__dict__.get("_sbw_inverse", False)
+    if cached is not False:
+        return cached
+    inv = None
+    if s.n == s.m and np.bincount(s.table, minlength=1 << s.n).max(initial=0) == 1:
+        t = np.empty(1 << s.n, dtype=np.uint32)
+        t[s.table] = np.arange(1 << s.n, dtype=np.uint32)
+        inv = SBox(s.n, s.n, t)
+    object.__setattr__(s, "_sbw_inverse", inv)
+    return inv
+
+
+def _xmajor_inverse_path(s: SBox, v_lo: int, v_hi: int) -> bool:
+    """Full-range x-major store of a bijective 13..16-bit box: written straight
+    from the inverse's mask-major rows (sbw_xmajor_from_inverse), no transpose
+    and no full-size scratch (16x16: 9.55 -> 4.20 ms incl. the maxima,
+    tools/xmajor_full_time.py).  n = 12 keeps the transpose path (0.091 vs
+    0.113 ms: both launch-bound, and the maxima cost a second launch);
+    SBW_XMAJOR_INVERSE=1 forces the inverse path for n = 12, =0 disables it."""
+    import os
+
+    env = os.environ.get("SBW_XMAJOR_INVERSE")
+    lo = 12 if env == "1" else 13
+    return (s.n == s.m and lo <= s.n <= 16 and v_lo == 1 and v_hi == 1 << s.m and env != "0")
+
+
+def _xmajor_from_inverse(s: SBox, inv: SBox, out, dev) -> None:
+    """out[u][v - 1] = W_S(u, v) for u in [0, 2^n), v in [1, 2^n) (row 0 = 0)."""
+    lib = _dev.load_library()
+    itab = _dev.device_table(inv, dev)
+    n = s.n
+    nbytes = lib.sbw_xmajor_inverse_scratch_bytes(n, 1, 1 << n)
+    scratch = _scratch(nbytes, dev)
+    with charged(nbytes), _dev.on(dev):
+        out[0].zero_()
+        _dev.check(lib.sbw_xmajor_from_inverse(_dev.ptr(itab), _dev.table_bytes(n), n, 1, 1 << n,
+                                               _dev.ptr(out) + 4 * out.stride(0), out.stride(0),
+                                               _dev.ptr(scratch), nbytes, _dev.stream_handle(dev)))
+
+
 def spectrum_device(s: SBox, v_lo: int = 1, v_hi: int | None = None, layout: str = "mask",
                     device=None, out=None):
     """Materialised spectrum on the device.
@@ -86,6 +129,14 @@ def spectrum_device(s: SBox, v_lo: int = 1, v_hi: int | None = None, layout: str
         out = torch.empty(shape, dtype=torch.int32, device=dev)
     elif tuple(out.shape) != shape or out.dtype != torch.int32 or not out.is_contiguous():
         raise ValueError(f"out must be a contiguous int32 tensor of shape {shape}")
+    if lay == _dev.LAYOUT_X_MAJOR and _xmajor_inverse_path(s, v_lo, v_hi):
+        inv = _inverse_if_bijective(s)
+        if inv is not None:
+            # W_S(u, v) = W_{S^-1}(v, u): the x-major rows are the inverse's
+            # mask-major rows; the per-component maxima come from the fused path
+            _xmajor_from_inverse(s, inv, out, dev)
+            mx, _ = component_max_abs_device(s, v_lo, v_hi, device=dev)
+            return out, mx
     mx = torch.empty(max(1, rows), dtype=torch.int32, device=dev)
     lib = _dev.load_library()
     tab = _dev.device_table(s, dev)

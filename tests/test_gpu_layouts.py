@@ -117,3 +117,111 @@ def test_staged_and_per_lane_spectrum_epilogues_agree(n, v_lo, count):
         assert np.array_equal(got[:, : 1 << n], want), ld
         assert (got[:, 1 << n:] == -7).all(), ld  # the padding is never written
         assert np.array_equal(mx.cpu().numpy(), np.abs(want).max(axis=1)), ld
+
+
+# ---- x-major of a bijective box straight from its inverse (sbw_xmajor_from_inverse)
+@pytest.mark.parametrize("n,seed", [(12, 0), (12, 7), (13, 1), (14, 2), (15, 3)])
+def test_xmajor_full_from_inverse_matches_oracle(n, seed):
+    """Full-range x-major store of a bijective box (inverse path, default)
+    equals the mask-major rows transposed; n = 12 also against the oracle,
+    and the transpose path (SBW_XMAJOR_INVERSE=0) agrees."""
+    import torch
+
+    s = sw.generate_sbox(n, n, seed, bijective=True)
+    os.environ["SBW_XMAJOR_INVERSE"] = "1"  # n = 12 defaults to the transpose path
+    try:
+        xm, mx = sw.spectrum_device(s, layout="x")
+    finally:
+        del os.environ["SBW_XMAJOR_INVERSE"]
+    assert tuple(xm.shape) == (1 << n, (1 << n) - 1)
+    mm, mmx = sw.spectrum_device(s, layout="mask")
+    assert torch.equal(xm, mm.t())
+    assert torch.equal(mx, mmx)
+    if n == 12:
+        want = orc.spectrum(s.table, n, 1, 1 << n)
+        assert np.array_equal(xm.cpu().numpy(), want.T)
+        assert np.array_equal(mx.cpu().numpy(), np.abs(want.astype(np.int64)).max(axis=1))
+    os.environ["SBW_XMAJOR_INVERSE"] = "0"
+    try:
+        xt, _ = sw.spectrum_device(s, layout="x")
+    finally:
+        del os.environ["SBW_XMAJOR_INVERSE"]
+    assert torch.equal(xt, xm)
+
+
+@pytest.mark.parametrize("n,u_lo,u_hi,pad,shift", [(12, 1, 4096, 0, 1), (12, 5, 300, 9, 2), (13, 100, 8192, 3, 3),
+                                                   (16, 1, 70, 0, 0), (16, 65400, 65536, 1, 1),
+                                                   (14, 2, 16384, 0, 0)])
+def test_xmajor_from_inverse_abi_rows_pitch_alignment(n, u_lo, u_hi, pad, shift):
+    """The C entry directly: any row range, pitch 2^n - 1 + pad, an output
+    pointer shifted by `shift` words from 16-byte alignment; the words around
+    every written row are untouched."""
+    import torch
+
+    from paper_1912_03732_b200 import device as dv
+    from paper_1912_03732_b200 import walsh
+
+    s = sw.generate_sbox(n, n, 11, bijective=True)
+    inv = walsh._inverse_if_bijective(s)
+    dev = torch.device("cuda:0")
+    ld = (1 << n) - 1 + pad
+    rows = u_hi - u_lo
+    buf = torch.full((rows * ld + 64,), -7, dtype=torch.int32, device=dev)
+    lib = dv.load_library()
+    nbytes = lib.sbw_xmajor_inverse_scratch_bytes(n, u_lo, u_hi)
+    scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    itab = dv.device_table(inv, dev)
+    dv.check(lib.sbw_xmajor_from_inverse(dv.ptr(itab), dv.table_bytes(n), n, u_lo, u_hi,
+                                         dv.ptr(buf) + 4 * shift, ld, dv.ptr(scratch), nbytes,
+                                         dv.stream_handle(dev)))
+    torch.cuda.synchronize()
+    got = buf[shift:shift + rows * ld].view(rows, ld)
+    mm, _ = sw.spectrum_device(s, layout="mask")
+    want = mm.t()[u_lo:u_hi]
+    assert torch.equal(got[:, :(1 << n) - 1], want)
+    if pad:
+        assert bool((got[:, (1 << n) - 1:] == -7).all())
+    assert bool((buf[:shift] == -7).all()) and bool((buf[shift + rows * ld:] == -7).all())
+
+
+def test_xmajor_from_inverse_rejects_bad_arguments():
+    import torch
+
+    from paper_1912_03732_b200 import device as dv
+
+    s = sw.generate_sbox(12, 12, 0, bijective=True)
+    dev = torch.device("cuda:0")
+    tab = dv.device_table(s, dev)
+    lib = dv.load_library()
+    out = torch.empty(4096 * 4095, dtype=torch.int32, device=dev)
+    scratch = torch.empty(1 << 20, dtype=torch.uint8, device=dev)
+    st = dv.stream_handle(dev)
+    for args in [(11, 1, 2048, 2047), (12, 0, 4096, 4095), (12, 1, 4097, 4095), (12, 1, 4096, 4094)]:
+        n, lo, hi, ld = args
+        with pytest.raises((ValueError, IndexError)):
+            dv.check(lib.sbw_xmajor_from_inverse(dv.ptr(tab), dv.table_bytes(n), n, lo, hi, dv.ptr(out), ld,
+                                                 dv.ptr(scratch), 1 << 20, st))
+    with pytest.raises(ValueError):  # misaligned output
+        dv.check(lib.sbw_xmajor_from_inverse(dv.ptr(tab), dv.table_bytes(12), 12, 1, 4096, dv.ptr(out) + 2,
+                                             4095, dv.ptr(scratch), 1 << 20, st))
+
+
+@pytest.mark.slow
+def test_16x16_full_xmajor_from_inverse_hash():
+    """The whole 16x16 x-major store (65536 x 65535 int32, 16 GiB) through the
+    inverse path on the device, hashed and compared with the reference's own
+    sha256 (tests/golden/hashes_16x16.json)."""
+    import torch
+
+    g = json.load(open(os.path.join(HERE, "golden", "hashes_16x16.json")))
+    s = sw.generate_sbox(16, 16, 0, bijective=True)
+    xm, mx = sw.spectrum_device(s, layout="x")
+    assert tuple(xm.shape) == (65536, 65535)
+    h = hashlib.sha256()
+    pin = torch.empty((2048, 65535), dtype=torch.int32, pin_memory=True)
+    for a in range(0, 65536, 2048):
+        pin.copy_(xm[a:a + 2048])
+        h.update(pin.numpy().tobytes())
+    assert h.hexdigest() == g["sha256_x_major"]
+    values = ((1 << 16) - mx.cpu().numpy().astype(np.int64)) >> 1
+    assert orc.nl_from_maxima(values) == (g["nl"], g["argmin_v"])
