@@ -186,6 +186,60 @@ def device_to_host_chunked(src, out: np.ndarray, chunk_bytes: int = 128 << 20) -
     return out
 
 
+def _xmajor_to_host_from_inverse(s, inv, out, maxima, fast_out, chunk_bytes, dev):
+    """Full x-major store of a bijective box to the host by ROW chunks of the
+    x-major matrix (sbw_xmajor_from_inverse), each a contiguous block of the
+    caller's array; double-buffered like the mask-major export."""
+    torch = _dev.torch_mod()
+    n = s.n
+    nx, nv = 1 << n, (1 << n) - 1
+    rows = max(1, min(nx, chunk_bytes // (nv * 4)))
+    lib = _dev.load_library()
+    itab = _dev.device_table(inv, dev)
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    bufs = [torch.empty((rows, nv), dtype=torch.int32, device=dev) for _ in range(2)]
+    pins = [torch.empty((rows, nv), dtype=torch.int32, pin_memory=True) for _ in range(2)]
+    done = [None, None]
+    sbytes = lib.sbw_xmajor_inverse_scratch_bytes(n, 1, 1 + rows)
+    scratch = [_scratch(sbytes, dev), _scratch(sbytes, dev)]
+    mx, _ = component_max_abs_device(s, 1, 1 << n, device=dev)
+    torch.cuda.current_stream(dev).synchronize()  # tables and maxima visible to both streams
+    pending = []
+
+    def drain(slot, a, b):
+        done[slot].synchronize()
+        if fast_out:
+            torch.from_numpy(out[a:b]).copy_(pins[slot][: b - a])
+        else:
+            out[a:b] = pins[slot][: b - a].numpy()
+
+    for i, a in enumerate(range(0, nx, rows)):
+        b = min(nx, a + rows)
+        slot = i & 1
+        if len(pending) == 2:
+            drain(*pending.pop(0))
+        st = streams[slot]
+        with torch.cuda.stream(st):
+            buf = bufs[slot]
+            lo = max(a, 1)
+            if a == 0:
+                buf[0].zero_()  # W_S(0, v) = 0 for v != 0 (S bijective)
+            if b > lo:
+                _dev.check(lib.sbw_xmajor_from_inverse(
+                    _dev.ptr(itab), _dev.table_bytes(n), n, lo, b, _dev.ptr(buf) + 4 * nv * (lo - a), nv,
+                    _dev.ptr(scratch[slot]), sbytes, st.cuda_stream))
+            pins[slot][: b - a].copy_(buf[: b - a], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            done[slot] = ev
+        pending.append((slot, a, b))
+    for p in pending:
+        drain(*p)
+    torch.cuda.synchronize(dev)
+    maxima[:] = mx.cpu().numpy()
+    return out, maxima
+
+
 def spectrum_to_host(s: SBox, v_lo: int = 1, v_hi: int | None = None, layout: str = "mask",
                      out: np.ndarray | None = None, chunk_bytes: int = 128 << 20,
                      device=None) -> tuple[np.ndarray, np.ndarray]:
@@ -215,6 +269,10 @@ def spectrum_to_host(s: SBox, v_lo: int = 1, v_hi: int | None = None, layout: st
         raise ValueError(f"out must be an int32 array of shape {shape}")
     fast_out = out.flags.writeable and all(st >= 0 for st in out.strides)
     maxima = np.empty(nv, dtype=np.int32)
+    if layout == "x" and _xmajor_inverse_path(s, v_lo, v_hi):
+        inv = _inverse_if_bijective(s)
+        if inv is not None:
+            return _xmajor_to_host_from_inverse(s, inv, out, maxima, fast_out, chunk_bytes, dev)
     rows = max(1, min(nv, chunk_bytes // (nx * 4)))
     streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
     bufs, pins, done = [], [], []

@@ -81,8 +81,13 @@ def test_16x16_full_matrix_hashes_both_layouts():
         h.update(chunk.cpu().numpy().tobytes())
         del chunk
     assert h.hexdigest() == g["sha256_mask_major"]
-    # x-major: the whole 16 GiB store on the device, row blocks to the host
-    xm, mx = sw.spectrum_device(s, layout="x")
+    # x-major: the whole 16 GiB store on the device by the mask-major +
+    # transpose path (the inverse path has its own hash test below)
+    os.environ["SBW_XMAJOR_INVERSE"] = "0"
+    try:
+        xm, mx = sw.spectrum_device(s, layout="x")
+    finally:
+        del os.environ["SBW_XMAJOR_INVERSE"]
     torch.cuda.synchronize()
     h = hashlib.sha256()
     for a in range(0, 1 << 16, 1024):
@@ -225,3 +230,22 @@ def test_16x16_full_xmajor_from_inverse_hash():
     assert h.hexdigest() == g["sha256_x_major"]
     values = ((1 << 16) - mx.cpu().numpy().astype(np.int64)) >> 1
     assert orc.nl_from_maxima(values) == (g["nl"], g["argmin_v"])
+
+
+@pytest.mark.parametrize("n,chunk_rows", [(13, 1000), (14, 4096), (15, 333)])
+def test_xmajor_full_host_export_from_inverse(n, chunk_rows):
+    """spectrum_to_host(layout="x") over every mask of a bijective box goes by
+    row chunks of the x-major matrix (inverse path): equal to the device store
+    of the transpose path, including an odd final chunk and row 0."""
+    import torch
+
+    s = sw.generate_sbox(n, n, 3, bijective=True)
+    out, mx = sw.spectrum_to_host(s, layout="x", chunk_bytes=chunk_rows * ((1 << n) - 1) * 4)
+    os.environ["SBW_XMAJOR_INVERSE"] = "0"
+    try:
+        want, wmx = sw.spectrum_device(s, layout="x")
+    finally:
+        del os.environ["SBW_XMAJOR_INVERSE"]
+    assert out.shape == (1 << n, (1 << n) - 1)
+    assert np.array_equal(out, want.cpu().numpy())
+    assert np.array_equal(mx, wmx.cpu().numpy())
