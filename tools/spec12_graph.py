@@ -56,4 +56,49 @@ for layout, lay in (("mask", 0), ("x", 1)):
     res[layout] = us
     print(f"12x12 spectrum {layout}-major + maxima (graph replay, L2-warm): {us:.1f} us per call, "
           f"{4095 * 4096 * 4 / us / 1e6:.2f} TB/s of output", flush=True)
+# x-major from the inverse box (sbw_xmajor_from_inverse) + row 0 + maxima by sbw_nl
+from paper_1912_03732_b200 import walsh  # noqa: E402
+
+inv = walsh._inverse_if_bijective(s)
+itab = d.device_table(inv, dev)
+out = torch.empty((4096, 4095), dtype=torch.int32, device=dev)
+mx = torch.empty(4095, dtype=torch.int32, device=dev)
+key = torch.zeros(1, dtype=torch.int64, device=dev)
+xb = lib.sbw_xmajor_inverse_scratch_bytes(12, 1, 4096)
+nb = lib.sbw_nl_scratch_bytes(12, 12, 1, 4096)
+xs = torch.empty(xb, dtype=torch.uint8, device=dev)
+ns = torch.empty(max(1, nb), dtype=torch.uint8, device=dev)
+st = torch.cuda.Stream(dev)
+
+
+def call_inv():
+    out[0].zero_()
+    d.check(lib.sbw_xmajor_from_inverse(itab.data_ptr(), 2, 12, 1, 4096, out.data_ptr() + 4 * 4095, 4095,
+                                        xs.data_ptr(), xb, st.cuda_stream))
+    d.check(lib.sbw_nl(tab.data_ptr(), 2, 12, 12, 1, 4096, mx.data_ptr(), key.data_ptr(), ns.data_ptr(), nb,
+                       st.cuda_stream))
+
+
+with torch.cuda.stream(st):
+    for _ in range(3):
+        call_inv()
+st.synchronize()
+h = hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest()[:16]
+assert h == g["sha_x_major"], ("x-inverse", h)
+graph = torch.cuda.CUDAGraph()
+with torch.cuda.graph(graph, stream=st, capture_error_mode="relaxed"):
+    call_inv()
+for _ in range(5):
+    graph.replay()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(st)
+with torch.cuda.stream(st):
+    for _ in range(50):
+        graph.replay()
+e1.record(st)
+torch.cuda.synchronize()
+us = e0.elapsed_time(e1) * 1e3 / 50
+res["x_inverse"] = us
+print(f"12x12 x-major from the inverse + maxima (graph replay, L2-warm): {us:.1f} us per call", flush=True)
 print(json.dumps(res))
