@@ -25,6 +25,11 @@ int launch_tc16_nl(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t
 bool tc_path_enabled();
 // Tensor-core NL for n = 11..15 (2^(16-n) components per 2^16 tile); needs
 // m >= 16 - n so every slot's mask is a valid mask.
+// k_tc_lut (sbw_tc_lut.cu): the same n = 16 NL job with the GEMM over x bits
+// 8..15 and a table-lookup generation; launch_tc16_nl takes it unless SBW_TC_LUT=0
+bool tc_lut_enabled();
+int launch_tc16_nl_lut(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
+                       unsigned long long* key, cudaStream_t st);
 int tc_min_small_n();  // smallest n of launch_tc_nl_small (11, or 12 for 16-row generation builds)
 int launch_tc_nl_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
                        unsigned long long* key, cudaStream_t st);

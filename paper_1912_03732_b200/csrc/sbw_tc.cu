@@ -1064,7 +1064,8 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_hybrid(TcArgs a) {
 
 // int8 MMA peak: one CTA per SM, one thread issues `reps` chains of 8
 // accumulating 128x256x32 MMAs on fixed smem operands (A 32 KiB, B 64 KiB).
-__global__ void __launch_bounds__(128, 1) k_int8_mma_peak(int reps, int* sink) {
+// mn = 1: B as an MN-major SWIZZLE_128B operand (probe: SBW_PEAK_MN=1), mn = 2: A reused from one 32 KiB block
+__global__ void __launch_bounds__(128, 1) k_int8_mma_peak(int reps, int* sink, int mn) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
@@ -1080,6 +1081,16 @@ __global__ void __launch_bounds__(128, 1) k_int8_mma_peak(int reps, int* sink) {
   if (warp == 0) {
     const uint64_t da = tc::sdesc(tc::smem_u32(smem), 128, 2048);
     const uint64_t db = tc::sdesc(tc::smem_u32(smem + 32768), 128, 2048);
+    if (mn == 1) {
+      const uint32_t b0 = tc::smem_u32(smem + 32768);
+      const uint64_t dmn = uint64_t((b0 & 0x3FFFFu) >> 4) | (uint64_t(1024 >> 4) << 16) | (uint64_t(2048 >> 4) << 32) |
+                           (uint64_t(1) << 46) | (uint64_t(2) << 61);
+      for (int r = 0; r < reps; ++r)
+#pragma unroll
+        for (int kb = 0; kb < 8; ++kb)
+          tc::mma_i8_elect(tmem, da + uint64_t(kb * 16), dmn + uint64_t((kb * 8192) >> 4), kIdesc | (1u << 16),
+                           (r | kb) ? 1u : 0u);
+    } else
     for (int r = 0; r < reps; ++r)
 #pragma unroll
       for (int kb = 0; kb < 8; ++kb)
@@ -1113,7 +1124,8 @@ int run_int8_mma_peak(double* ops_per_s, double* ms_out, cudaStream_t st) {
   double best = 0, best_ms = 0;
   for (int rep = 0; rep < 4; ++rep) {
     SBW_CUDA_CHECK(cudaEventRecord(e0, st));
-    k_int8_mma_peak<<<dp.sm_count, 128, smem, st>>>(reps, sink);
+    static const int mn = getenv("SBW_PEAK_MN") ? atoi(getenv("SBW_PEAK_MN")) : 0;
+    k_int8_mma_peak<<<dp.sm_count, 128, smem, st>>>(reps, sink, mn);
     SBW_LAUNCH_CHECK("k_int8_mma_peak");
     SBW_CUDA_CHECK(cudaEventRecord(e1, st));
     SBW_CUDA_CHECK(cudaEventSynchronize(e1));
@@ -1183,6 +1195,7 @@ int run_tc_hybrid(const TcArgs& a, int64_t items, cudaStream_t st, int grid_over
 
 int launch_tc16_nl(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
                    unsigned long long* key, cudaStream_t st) {
+  if (tc_lut_enabled()) return launch_tc16_nl_lut(planes, v_lo, v_hi, max_abs, key, st);
   TcArgs a{};
   a.planes = planes;
   a.plane_words = 2048;

@@ -1,0 +1,410 @@
+// k_tc_lut: the n = 16 nonlinearity kernel with the GEMM contracting over the
+// HIGH input bits and a table-lookup generation (K2L in DESIGN.md).
+//
+// Same job as k_tc_hybrid<NL, 16> (sbw_tc.cu): per output mask v,
+// polarity_row (sbox.py:145-152) + fwht_column_in_place (walsh.py:73-104) +
+// column_nonlinearity (walsh.py:107-114), all 16 butterfly stages of the
+// 2^16-point transform, only max|W| leaves the chip.  The split x = c * 256 + r
+// (r = x bits 0..7, c = bits 8..15) is used the other way round:
+//
+//   Generation (r bits 0..4, 5 stages, no bit expansion).  The 32 component
+//   bits of one plane word are 4 bytes; a 256-entry shared-memory table maps
+//   a byte straight to the biased 8-point WHT of its 8 bits (8 output bytes,
+//   LDS.64), and two byte-lane butterfly stages across the 4 lookups finish
+//   the 32-point WHT of the word: U[c][32 ks + e5] in [0, 32], offset 16 on
+//   all but e5 = 0.  The (w >> k) & 0x01010101 expansion and three of the
+//   byte stages of k_tc_hybrid (0.5 + 0.375 ALU instructions per element)
+//   become one PRMT + one LDS.64 per 8 elements.
+//
+//   GEMM (c bits 0..7, 8 stages).  D[u_c][n] = sum_c A[u_c][c] U[c][n],
+//   A = -H_256 (s8), U the B operand (u8, MN-major SWIZZLE_128B: the 32 bytes
+//   a thread produces for one (c, word) are contiguous), plus the bias K block
+//   of the 32-row form: +4096 on every entry and +4096 more on row u_c = 0, so
+//   D = W_13 / 2 + 2^12 in [0, 2^13] exactly (the biased s form).
+//
+//   Integer stages (r bits 5..7 = column bits 5..7).  tcgen05.ld .pack::16b,
+//   two packed int16 stages, the top stage fused with the VIMNMX3 fold.
+//
+// Output positions are permuted relative to k_tc_hybrid (TMEM lane = u_c, not
+// u_r), which the max does not see; the materialising modes keep k_tc_hybrid.
+// Pipeline, warp roles, Gray mask order and publishing are those of
+// k_tc_hybrid (one MMA-issuing warp, 8 transform warps, mbarriers only).
+#include <cstdlib>
+#include <mutex>
+
+#include "sbw_internal.cuh"
+#include "sbw_launch.h"
+#include "sbw_tc.cuh"
+#include "sbw_tile_simd.cuh"
+
+namespace sbw {
+namespace {
+
+#ifndef SBW_LUT_COPIES
+#define SBW_LUT_COPIES 16  // table replicas (lane & 15 picks one): LDS.64 without bank conflicts
+#endif
+constexpr int kCopies = SBW_LUT_COPIES;
+constexpr int kMathWarps = 8;
+// A = -H_256 needs only two 128 x 128 blocks: with Hs = -H_128,
+//   rows u < 128 : A[u][c] = Hs[u][c & 127]
+//   rows u >= 128: A[u][c] = Hs[u & 127][c & 127] for c < 128, -Hs[..] for c >= 128,
+// so both M = 128 halves read Hs for K blocks 0..3 and Hs / -Hs for K blocks
+// 4..7 (32 KiB instead of 64 KiB; the space holds the lookup table replicas).
+constexpr int kHsOff = 0;                       // Hs, 128 x 128 s8, K-major core matrices
+constexpr int kNegOff = kHsOff + 128 * 128;     // -Hs
+constexpr int kAbOff = kNegOff + 128 * 128;     // A's bias K block, 2 halves x (128 x 32)
+constexpr int kBbOff = kAbOff + 2 * 128 * 32;   // B's bias block, 256 x 32, K-major
+constexpr int kBOff = kBbOff + 256 * 32;        // 2 x (256 x 256) generated B, MN-major SW128
+constexpr int kBBytes = 256 * 256;
+constexpr int kLutOff = kBOff + 2 * kBBytes;    // kCopies x 256 x 8 bytes
+constexpr int kLutBytes = kCopies * 2048;
+constexpr int kSmem = kLutOff + kLutBytes;
+constexpr int kImgBytes = kBOff + kLutBytes;    // constant image: Hs | -Hs | A bias | Bb | LUT
+static_assert(kBOff % 1024 == 0, "SW128 atoms need 1024-byte alignment");
+static_assert(kSmem <= 227 * 1024 - 1024, "k_tc_lut shared memory");
+// bias (the 32-row form of sbw_tc.cu): 4096 per D entry as 9 columns of
+// 127, ..., 8 against B columns of 4; twice on row u_c = 0
+constexpr int kBiasT = 4096, kBiasB = 4;
+constexpr int kBiasCols = (kBiasT / kBiasB + 126) / 127;
+static_assert(2 * kBiasCols <= 32, "bias block is one K block");
+constexpr uint32_t kIdescK = tc::idesc_i8(128, 256, /*A s8*/ true, /*B u8*/ false);
+constexpr uint32_t kIdescMN = kIdescK | (1u << 16);  // B MN-major
+constexpr int kIssuerRegs = 32, kMathRegs = 232;
+constexpr int kAllThreads = 128 + kMathWarps * 32;
+
+// MN-major SWIZZLE_128B descriptor (u8): atoms of 8 K-rows x 128 bytes of N
+// (1024 B, 1024-aligned), 16-byte chunk j of K-row i at chunk j ^ i; LBO = the
+// distance between atoms along N, SBO = between 8-row groups along K.
+__device__ __forceinline__ uint64_t sdesc_mn_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((saddr & 0x3FFFFu) >> 4) | (uint64_t((lbo >> 4) & 0x3FFFu) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFFu) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+
+// bias K block of A (against B's columns of kBiasB): +4096 on every row, +4096 more on u = 0
+__device__ __forceinline__ int a_bias_value(int u, int k) {
+  const int col = k % kBiasCols, last = kBiasT / kBiasB - 127 * (kBiasCols - 1);
+  if (k < kBiasCols) return col < kBiasCols - 1 ? 127 : last;
+  if (k < 2 * kBiasCols) return u == 0 ? (col < kBiasCols - 1 ? 127 : last) : 0;
+  return 0;
+}
+
+// constant image: Hs, -Hs and A's bias block (K-major core matrices), B's
+// bias block, the lookup table
+__global__ void k_lut_consts(uint8_t* img) {
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int e = t0; e < 128 * 128; e += nt) {
+    const int u = e >> 7, p = e & 127;
+    const int v = (__popc(u & p) & 1) ? 1 : -1;  // -H_128
+    const int off = ((u >> 3) * 8 + (p >> 4)) * 128 + (u & 7) * 16 + (p & 15);
+    img[kHsOff + off] = uint8_t(v);
+    img[kNegOff + off] = uint8_t(-v);
+  }
+  for (int e = t0; e < 256 * 32; e += nt) {
+    const int u = e >> 5, k = e & 31, ul = u & 127;
+    img[kAbOff + (u >> 7) * 4096 + ((ul >> 3) * 2 + (k >> 4)) * 128 + (ul & 7) * 16 + (k & 15)] =
+        uint8_t(a_bias_value(u, k));
+  }
+  for (int e = t0; e < 256 * 32; e += nt) {
+    const int n = e >> 5, k = e & 31;
+    img[kBbOff + ((n >> 3) * 2 + (k >> 4)) * 128 + (n & 7) * 16 + (k & 15)] = k < 2 * kBiasCols ? kBiasB : 0;
+  }
+  // table: byte b -> 8-point WHT of its bits, +4 on outputs e != 0 (every byte in [0, 8])
+  for (int e = t0; e < 256 * kCopies * 8; e += nt) {
+    const int oe = e & 7, cp = (e >> 3) % kCopies, b = e / (8 * kCopies);
+    int s = oe ? 4 : 0;
+    for (int j = 0; j < 8; ++j)
+      if ((b >> j) & 1) s += (__popc(oe & j) & 1) ? -1 : 1;
+    img[kBOff + (b * kCopies + cp) * 8 + oe] = uint8_t(s);
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ uint2 lds64(uint32_t saddr) {
+  uint2 r;
+  asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(saddr));
+  return r;
+}
+
+struct LutArgs {
+  const uint8_t* consts;
+  const uint32_t* planes;  // [16][2048]
+  uint32_t v_lo, v_hi;
+  int32_t* max_abs;
+  unsigned long long* key;
+};
+
+__device__ __forceinline__ void publish(const uint32_t* wmax, uint32_t v, const LutArgs& a) {
+  const uint4 x = *reinterpret_cast<const uint4*>(wmax);
+  const uint4 y = *reinterpret_cast<const uint4*>(wmax + 4);
+  const int m = int(max(max(max(x.x, x.y), max(x.z, x.w)), max(max(y.x, y.y), max(y.z, y.w))));
+  a.max_abs[v - a.v_lo] = m;
+  if (a.key) atomicMax(a.key, nl_key(m, v));
+}
+
+// MMA chain of one mask: 2 M-halves x (8 K blocks of generated B + the bias block)
+__device__ __forceinline__ void issue_mma(uint32_t tmem, const uint8_t* smem, int buf, uint64_t* bar) {
+  const uint64_t dhs = tc::sdesc(tc::smem_u32(smem + kHsOff), 128, 1024);
+  const uint64_t dab = tc::sdesc(tc::smem_u32(smem + kAbOff), 128, 256);
+  const uint64_t db0 = sdesc_mn_sw128(tc::smem_u32(smem + kBOff + buf * kBBytes), 1024, 2048);
+  const uint64_t dbb = tc::sdesc(tc::smem_u32(smem + kBbOff), 128, 256);
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int kb = 0; kb < 9; ++kb) {
+      // A: K block kb of half h = block kb & 3 of Hs (-Hs for h = 1, kb >= 4)
+      const uint64_t da = kb == 8 ? dab + uint64_t((h * 4096) >> 4)
+                                  : dhs + uint64_t((((h == 1 && kb >= 4) ? kNegOff - kHsOff : 0) + (kb & 3) * 256) >> 4);
+      // B: K block kb = 32 K-rows = 4 groups of 8 (2048 B each)
+      const uint64_t db = kb == 8 ? dbb : db0 + uint64_t((kb * 8192) >> 4);
+      tc::mma_i8_elect(tmem + h * 256, da, db, kb == 8 ? kIdescK : kIdescMN, kb > 0 ? 1u : 0u);
+    }
+  tc::mma_commit_elect(bar);
+}
+
+// One plane word (32 component bits of row c, r = 32 ks ..) -> the 32 bytes
+// U[c][32 ks .. 32 ks + 31]: four table lookups (r bits 0..2) and two
+// byte-lane stages across them (r bits 3, 4; diff + 2^t per byte, so every
+// byte stays in [0, 2^(t+1)]).
+__device__ __forceinline__ void word_to_bytes(uint32_t w, uint32_t lut, uint4& lo, uint4& hi) {
+  constexpr uint32_t M = 0x01010101u;
+  // byte i -> table address: one PRMT (ALU pipe) + one IMAD (FMA pipe) per lookup
+  const uint2 l0 = lds64(__byte_perm(w, 0u, 0x4440u) * uint32_t(8 * kCopies) + lut);
+  const uint2 l1 = lds64(__byte_perm(w, 0u, 0x4441u) * uint32_t(8 * kCopies) + lut);
+  const uint2 l2 = lds64(__byte_perm(w, 0u, 0x4442u) * uint32_t(8 * kCopies) + lut);
+  const uint2 l3 = lds64(__byte_perm(w, 0u, 0x4443u) * uint32_t(8 * kCopies) + lut);
+  // stage r bit 3: (l0, l1), (l2, l3); bias 8
+  const uint32_t s0x = l0.x + l1.x, s0y = l0.y + l1.y, d0x = l0.x - l1.x + (M << 3), d0y = l0.y - l1.y + (M << 3);
+  const uint32_t s1x = l2.x + l3.x, s1y = l2.y + l3.y, d1x = l2.x - l3.x + (M << 3), d1y = l2.y - l3.y + (M << 3);
+  // stage r bit 4: (s0, s1), (d0, d1); bias 16.  Output index e5 = 8 i + e3, i = (bit 4, bit 3)
+  lo = make_uint4(s0x + s1x, s0y + s1y, d0x + d1x, d0y + d1y);                                    // i = 0, 1
+  hi = make_uint4(s0x - s1x + (M << 4), s0y - s1y + (M << 4), d0x - d1x + (M << 4), d0y - d1y + (M << 4));  // i = 2, 3
+}
+
+__global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar_full, bar_tmem_empty, bar_bfull[2], bar_done;
+  __shared__ uint32_t tmem_slot;
+  __shared__ __align__(16) uint32_t s_wmax[4][kMathWarps];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t total = int64_t(a.v_hi) - a.v_lo;
+  const int64_t t_lo = total * blockIdx.x / gridDim.x;
+  const int n_my = int(total * (blockIdx.x + 1) / gridDim.x - t_lo);
+
+  for (int e = tid; e < kBOff / 16; e += kAllThreads)
+    reinterpret_cast<uint4*>(smem)[e] = __ldg(reinterpret_cast<const uint4*>(a.consts) + e);
+  for (int e = tid; e < kLutBytes / 16; e += kAllThreads)
+    reinterpret_cast<uint4*>(smem + kLutOff)[e] = __ldg(reinterpret_cast<const uint4*>(a.consts + kBOff) + e);
+  if (warp == 0) tc::tmem_alloc(&tmem_slot, 512);
+  if (tid == 0) {
+    tc::mbar_init(&bar_full, 1);
+    tc::mbar_init(&bar_tmem_empty, kMathWarps * 32);
+    tc::mbar_init(&bar_bfull[0], kMathWarps * 32);
+    tc::mbar_init(&bar_bfull[1], kMathWarps * 32);
+    tc::mbar_init(&bar_done, kMathWarps * 32);
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp < 4) {
+    // ---------------- issuer warpgroup ----------------
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kIssuerRegs));
+    if (warp == 0) {
+      for (int i = 0; i < n_my; ++i) {
+        tc::mbar_wait(&bar_bfull[i & 1], uint32_t((i >> 1) & 1));
+        if (i > 0) tc::mbar_wait(&bar_tmem_empty, uint32_t((i - 1) & 1));
+        tc::fence_after();
+        issue_mma(tmem, smem, i & 1, &bar_full);
+        // bfull(i) (i >= 2) follows every thread's store of its maxima of item i - 2
+        if (i >= 2 && lane == 0)
+          publish(s_wmax[(i - 2) & 3], mask_at(int64_t(a.v_lo) + t_lo + i - 2, a.v_lo, a.v_hi), a);
+      }
+      tc::mbar_wait(&bar_done, 0u);
+      tc::fence_after();
+      if (lane == 0)
+        for (int i = n_my - 2 < 0 ? 0 : n_my - 2; i < n_my; ++i)
+          publish(s_wmax[i & 3], mask_at(int64_t(a.v_lo) + t_lo + i, a.v_lo, a.v_hi), a);
+      __syncwarp();
+      tc::tmem_dealloc(tmem, 512);
+    }
+  } else {
+    // ---------------- transform warps ----------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kMathRegs));
+    const int mt = tid - 128, mw = mt >> 5;
+    // generation: rows cA = 16 mw + (lane & 7) + 8 (lane >> 4) and cA + 128, plane
+    // words 4 q .. 4 q + 3 of each (q = lane bit 3).  A quarter-warp (one STS.128
+    // phase) is 8 consecutive rows of one q: chunk positions j ^ (c & 7) all differ.
+    const int q = (lane >> 3) & 1;
+    const int cA = 16 * mw + (lane & 7) + 8 * (lane >> 4);
+    const uint32_t* __restrict__ planes = a.planes;
+    const uint32_t lut = tc::smem_u32(smem + kLutOff) + uint32_t(lane & (kCopies - 1)) * 8u;
+    uint32_t g[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) g[k] = 0;
+    uint32_t vcur = 0;
+    auto load_pl = [&](int i, uint4 (&x)[2]) {
+      const uint32_t* p = planes + int64_t(i) * 2048 + cA * 8 + 4 * q;
+      x[0] = __ldg(reinterpret_cast<const uint4*>(p));
+      x[1] = __ldg(reinterpret_cast<const uint4*>(p + 128 * 8));
+    };
+    auto xor_pl = [&](const uint4 (&x)[2]) {
+      g[0] ^= x[0].x; g[1] ^= x[0].y; g[2] ^= x[0].z; g[3] ^= x[0].w;
+      g[4] ^= x[1].x; g[5] ^= x[1].y; g[6] ^= x[1].z; g[7] ^= x[1].w;
+    };
+    auto xor_all = [&](uint32_t d) {
+      while (d) {
+        const int i = __ffs(d) - 1;
+        d &= d - 1;
+        uint4 x[2];
+        load_pl(i, x);
+        xor_pl(x);
+      }
+    };
+    // B rows of one item: the table lookups and byte stages run into registers
+    // (o[]) while no TMEM values are live, so all 32 lookups of a thread are in
+    // flight together; the stores follow once MMA(i) has released the buffer.
+    uint4 o[16];
+    auto gen_compute = [&]() {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) word_to_bytes(g[k], lut, o[2 * k], o[2 * k + 1]);
+    };
+    auto gen_sts = [&](int buf) {
+      uint8_t* bb = smem + kBOff + buf * kBBytes;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int c = cA + 128 * half;
+        uint8_t* row = bb + (c >> 3) * 2048 + q * 1024 + (c & 7) * 128;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          *reinterpret_cast<uint4*>(row + (((2 * w) ^ (c & 7)) << 4)) = o[2 * (4 * half + w)];
+          *reinterpret_cast<uint4*>(row + (((2 * w + 1) ^ (c & 7)) << 4)) = o[2 * (4 * half + w) + 1];
+        }
+      }
+      tc::fence_proxy_async();
+      mbar_arrive(&bar_bfull[buf]);
+    };
+    for (int k = 0; k < 3 && k < n_my; ++k) {
+      const uint32_t vn = mask_at(int64_t(a.v_lo) + t_lo + k, a.v_lo, a.v_hi);
+      xor_all(vcur ^ vn);
+      vcur = vn;
+      gen_compute();
+      if (k < 2) gen_sts(k);  // item 2 stays in o[] until MMA(0) has released buffer 0
+    }
+    // TMEM lane of this thread (warp w may only touch lanes 32 (w % 4) .. + 31)
+    const uint32_t tbase = tmem + (uint32_t((mw & 3) * 32) << 16) + uint32_t(mw >> 2) * 256;
+    for (int i = 0; i < n_my; ++i) {
+      // prefetch the first changed plane of the item three steps ahead
+      const bool gen = i + 3 < n_my;
+      uint32_t vn = 0, d = 0;
+      uint4 pa[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+      if (gen) {
+        vn = mask_at(int64_t(a.v_lo) + t_lo + i + 3, a.v_lo, a.v_hi);
+        d = vcur ^ vn;
+        if (d) {
+          load_pl(__ffs(d) - 1, pa);
+          d &= d - 1;
+        }
+      }
+      tc::mbar_wait(&bar_full, uint32_t(i & 1));
+      tc::fence_after();
+      uint32_t R[128];
+      uint32_t(&R0)[64] = *reinterpret_cast<uint32_t(*)[64]>(&R[0]);
+      uint32_t(&R1)[64] = *reinterpret_cast<uint32_t(*)[64]>(&R[64]);
+      tc::tmem_ld_x64_p16(tbase, R0);
+      tc::tmem_ld_x64_p16(tbase + 128, R1);
+      tc::wait_ld_tied(R0);
+      tc::wait_ld_tied(R1);
+      tc::fence_before();
+      mbar_arrive(&bar_tmem_empty);      // MMA(i+1) may start: nothing else sits in that gap
+      if (i + 2 < n_my) gen_sts(i & 1);  // B(i+2) into the buffer MMA(i) released
+      // R[j] = columns (2j, 2j + 1): column bits 5, 6 = register bits 4, 5
+      // (stages 14, 15; lane bias 2^13, 2^14), register bit 6 = the top stage
+#pragma unroll
+      for (int sb = 4; sb < 6; ++sb)
+#pragma unroll
+        for (int k = 0; k < 128; ++k)
+          if ((k & (1 << sb)) == 0) {
+            const uint32_t x = R[k], y = R[k | (1 << sb)];
+            R[k] = x + y;
+            R[k | (1 << sb)] = x - y + (0x02000200u << sb);
+          }
+      uint32_t mx = 0u, mn = 0xFFFFFFFFu;
+#pragma unroll
+      for (int k = 0; k < 64; ++k) {
+        const uint32_t x = R[k], y = R[k + 64];
+        const uint32_t S = x + y;
+        const uint32_t D = x - y + 0x80008000u;
+        mx = __vimax3_u16x2(mx, S, D);
+        mn = __vimin3_u16x2(mn, S, D);
+      }
+      const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<16>(mx, mn)));
+      if (lane == 0) s_wmax[i & 3][mw] = m;
+      if (gen) {  // B(i+3) into registers (R is dead)
+        xor_pl(pa);
+        if (d) xor_all(d);  // rare: more than one changed bit
+        vcur = vn;
+        gen_compute();
+      }
+    }
+    tc::fence_before();
+    mbar_arrive(&bar_done);
+  }
+}
+
+std::mutex g_lut_mu;
+uint8_t* g_lut_consts[64] = {};
+int lut_consts(int dev, cudaStream_t st, const uint8_t** out) {
+  std::lock_guard<std::mutex> lk(g_lut_mu);
+  if (!g_lut_consts[dev & 63]) {
+    uint8_t* p = nullptr;
+    SBW_CUDA_CHECK(cudaMalloc(&p, kImgBytes));
+    k_lut_consts<<<64, 256, 0, st>>>(p);
+    SBW_LAUNCH_CHECK("k_lut_consts");
+    SBW_CUDA_CHECK(cudaStreamSynchronize(st));
+    g_lut_consts[dev & 63] = p;
+  }
+  *out = g_lut_consts[dev & 63];
+  return SBW_OK;
+}
+
+}  // namespace
+
+// SBW_TC_LUT=0 keeps k_tc_hybrid<NL, 16> for the n = 16 NL path (A/B runs)
+bool tc_lut_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SBW_TC_LUT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+int launch_tc16_nl_lut(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
+                       unsigned long long* key, cudaStream_t st) {
+  const int64_t items = int64_t(v_hi) - v_lo;
+  if (items <= 0) return SBW_OK;
+  DeviceProps dp;
+  if (int rc = device_props(&dp)) return rc;
+  static unsigned long long attr_done = 0;
+  if (!(attr_done >> (dp.device & 63) & 1ull)) {
+    SBW_CUDA_CHECK(cudaFuncSetAttribute(k_tc_lut, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    attr_done |= 1ull << (dp.device & 63);
+  }
+  LutArgs a{};
+  if (int rc = lut_consts(dp.device, st, &a.consts)) return rc;
+  a.planes = planes;
+  a.v_lo = v_lo;
+  a.v_hi = v_hi;
+  a.max_abs = max_abs;
+  a.key = key;
+  const int grid = int(items < dp.sm_count ? items : dp.sm_count);
+  k_tc_lut<<<grid, kAllThreads, kSmem, st>>>(a);
+  SBW_LAUNCH_CHECK("k_tc_lut");
+  return SBW_OK;
+}
+
+}  // namespace sbw
