@@ -44,6 +44,19 @@ namespace {
 #define SBW_LUT_COPIES 16  // table replicas (lane & 15 picks one): LDS.64 without bank conflicts
 #endif
 constexpr int kCopies = SBW_LUT_COPIES;
+#ifndef SBW_LUT_STS_EARLY
+#define SBW_LUT_STS_EARLY 0  // 1: B(i+2) stores issued under the TMEM loads of item i (measured 1.11 vs 0.86 ms)
+#endif
+#ifndef SBW_LUT_DONE_LATE
+#define SBW_LUT_DONE_LATE 0  // 1: proxy fence + bfull arrive after the item's stages (0.864 vs 0.862 ms)
+#endif
+#ifndef SBW_LUT_SPLIT
+#define SBW_LUT_SPLIT 1  // lookups of B(i+3) issued before item i's stages, their byte stages after the fold
+#endif
+#ifndef SBW_LUT_GEN7
+#define SBW_LUT_GEN7 1  // r bits 5, 6 as two more byte-lane stages across a thread's 4 words (else int16 stages)
+#endif
+constexpr int kGenStages = SBW_LUT_GEN7 ? 7 : 5;  // r stages before the GEMM
 constexpr int kMathWarps = 8;
 // A = -H_256 needs only two 128 x 128 blocks: with Hs = -H_128,
 //   rows u < 128 : A[u][c] = Hs[u][c & 127]
@@ -64,7 +77,7 @@ static_assert(kBOff % 1024 == 0, "SW128 atoms need 1024-byte alignment");
 static_assert(kSmem <= 227 * 1024 - 1024, "k_tc_lut shared memory");
 // bias (the 32-row form of sbw_tc.cu): 4096 per D entry as 9 columns of
 // 127, ..., 8 against B columns of 4; twice on row u_c = 0
-constexpr int kBiasT = 4096, kBiasB = 4;
+constexpr int kBiasT = 1 << (kGenStages + 7), kBiasB = 1 << (kGenStages - 3);
 constexpr int kBiasCols = (kBiasT / kBiasB + 126) / 127;
 static_assert(2 * kBiasCols <= 32, "bias block is one K block");
 constexpr uint32_t kIdescK = tc::idesc_i8(128, 256, /*A s8*/ true, /*B u8*/ false);
@@ -124,7 +137,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 __device__ __forceinline__ uint2 lds64(uint32_t saddr) {
   uint2 r;
-  asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(saddr));
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(saddr));
   return r;
 }
 
@@ -165,19 +178,23 @@ __device__ __forceinline__ void issue_mma(uint32_t tmem, const uint8_t* smem, in
 }
 
 // One plane word (32 component bits of row c, r = 32 ks ..) -> the 32 bytes
-// U[c][32 ks .. 32 ks + 31]: four table lookups (r bits 0..2) and two
-// byte-lane stages across them (r bits 3, 4; diff + 2^t per byte, so every
-// byte stays in [0, 2^(t+1)]).
-__device__ __forceinline__ void word_to_bytes(uint32_t w, uint32_t lut, uint4& lo, uint4& hi) {
-  constexpr uint32_t M = 0x01010101u;
-  // byte i -> table address: one PRMT (ALU pipe) + one IMAD (FMA pipe) per lookup
+// U[c][32 ks .. 32 ks + 31]: four table lookups (r bits 0..2; byte i -> table
+// address by one PRMT on the ALU pipe + one IMAD on the FMA pipe) ...
+__device__ __forceinline__ void word_lookup(uint32_t w, uint32_t lut, uint4& lo, uint4& hi) {
   const uint2 l0 = lds64(__byte_perm(w, 0u, 0x4440u) * uint32_t(8 * kCopies) + lut);
   const uint2 l1 = lds64(__byte_perm(w, 0u, 0x4441u) * uint32_t(8 * kCopies) + lut);
   const uint2 l2 = lds64(__byte_perm(w, 0u, 0x4442u) * uint32_t(8 * kCopies) + lut);
   const uint2 l3 = lds64(__byte_perm(w, 0u, 0x4443u) * uint32_t(8 * kCopies) + lut);
+  lo = make_uint4(l0.x, l0.y, l1.x, l1.y);
+  hi = make_uint4(l2.x, l2.y, l3.x, l3.y);
+}
+// ... and two byte-lane stages across them (r bits 3, 4; diff + 2^t per byte,
+// so every byte stays in [0, 2^(t+1)]), in place.
+__device__ __forceinline__ void word_stages(uint4& lo, uint4& hi) {
+  constexpr uint32_t M = 0x01010101u;
   // stage r bit 3: (l0, l1), (l2, l3); bias 8
-  const uint32_t s0x = l0.x + l1.x, s0y = l0.y + l1.y, d0x = l0.x - l1.x + (M << 3), d0y = l0.y - l1.y + (M << 3);
-  const uint32_t s1x = l2.x + l3.x, s1y = l2.y + l3.y, d1x = l2.x - l3.x + (M << 3), d1y = l2.y - l3.y + (M << 3);
+  const uint32_t s0x = lo.x + lo.z, s0y = lo.y + lo.w, d0x = lo.x - lo.z + (M << 3), d0y = lo.y - lo.w + (M << 3);
+  const uint32_t s1x = hi.x + hi.z, s1y = hi.y + hi.w, d1x = hi.x - hi.z + (M << 3), d1y = hi.y - hi.w + (M << 3);
   // stage r bit 4: (s0, s1), (d0, d1); bias 16.  Output index e5 = 8 i + e3, i = (bit 4, bit 3)
   lo = make_uint4(s0x + s1x, s0y + s1y, d0x + d1x, d0y + d1y);                                    // i = 0, 1
   hi = make_uint4(s0x - s1x + (M << 4), s0y - s1y + (M << 4), d0x - d1x + (M << 4), d0y - d1y + (M << 4));  // i = 2, 3
@@ -269,9 +286,35 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
     // (o[]) while no TMEM values are live, so all 32 lookups of a thread are in
     // flight together; the stores follow once MMA(i) has released the buffer.
     uint4 o[16];
-    auto gen_compute = [&]() {
+    auto gen_lookup = [&]() {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) word_to_bytes(g[k], lut, o[2 * k], o[2 * k + 1]);
+      for (int k = 0; k < 8; ++k) word_lookup(g[k], lut, o[2 * k], o[2 * k + 1]);
+    };
+    auto gen_stages = [&]() {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) word_stages(o[2 * k], o[2 * k + 1]);
+      if constexpr (kGenStages == 7) {
+        // r bits 5, 6: across the 4 words of each row (diff + 32, + 64 per byte: every byte in [0, 128])
+        auto bfly = [](uint4& x, uint4& y, uint32_t b) {
+          const uint4 s4 = make_uint4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
+          y = make_uint4(x.x - y.x + b, x.y - y.y + b, x.z - y.z + b, x.w - y.w + b);
+          x = s4;
+        };
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {  // lo / hi chunk of every word
+            bfly(o[8 * h + j], o[8 * h + 2 + j], 0x20202020u);
+            bfly(o[8 * h + 4 + j], o[8 * h + 6 + j], 0x20202020u);
+            bfly(o[8 * h + j], o[8 * h + 4 + j], 0x40404040u);
+            bfly(o[8 * h + 2 + j], o[8 * h + 6 + j], 0x40404040u);
+          }
+        }
+      }
+    };
+    auto gen_compute = [&]() {
+      gen_lookup();
+      gen_stages();
     };
     auto gen_sts = [&](int buf) {
       uint8_t* bb = smem + kBOff + buf * kBBytes;
@@ -285,6 +328,8 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
           *reinterpret_cast<uint4*>(row + (((2 * w + 1) ^ (c & 7)) << 4)) = o[2 * (4 * half + w) + 1];
         }
       }
+    };
+    auto gen_done = [&](int buf) {  // generic-proxy stores -> visible to the tensor core, then bfull
       tc::fence_proxy_async();
       mbar_arrive(&bar_bfull[buf]);
     };
@@ -293,7 +338,10 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
       xor_all(vcur ^ vn);
       vcur = vn;
       gen_compute();
-      if (k < 2) gen_sts(k);  // item 2 stays in o[] until MMA(0) has released buffer 0
+      if (k < 2) {  // item 2 stays in o[] until MMA(0) has released buffer 0
+        gen_sts(k);
+        gen_done(k);
+      }
     }
     // TMEM lane of this thread (warp w may only touch lanes 32 (w % 4) .. + 31)
     const uint32_t tbase = tmem + (uint32_t((mw & 3) * 32) << 16) + uint32_t(mw >> 2) * 256;
@@ -317,15 +365,31 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
       uint32_t(&R1)[64] = *reinterpret_cast<uint32_t(*)[64]>(&R[64]);
       tc::tmem_ld_x64_p16(tbase, R0);
       tc::tmem_ld_x64_p16(tbase + 128, R1);
+#if SBW_LUT_STS_EARLY
+      if (i + 2 < n_my) gen_sts(i & 1);  // B(i+2) into the buffer MMA(i) released, under the TMEM loads
+#endif
       tc::wait_ld_tied(R0);
       tc::wait_ld_tied(R1);
       tc::fence_before();
-      mbar_arrive(&bar_tmem_empty);      // MMA(i+1) may start: nothing else sits in that gap
+      mbar_arrive(&bar_tmem_empty);      // MMA(i+1) may start: no fence or barrier sits in that gap
+#if !SBW_LUT_STS_EARLY
       if (i + 2 < n_my) gen_sts(i & 1);  // B(i+2) into the buffer MMA(i) released
+#endif
+#if !SBW_LUT_DONE_LATE
+      if (i + 2 < n_my) gen_done(i & 1);
+#endif
+#if SBW_LUT_SPLIT
+      if (gen) {  // B(i+3): lookups in flight under this item's stages
+        xor_pl(pa);
+        if (d) xor_all(d);  // rare: more than one changed bit
+        vcur = vn;
+        gen_lookup();
+      }
+#endif
       // R[j] = columns (2j, 2j + 1): column bits 5, 6 = register bits 4, 5
       // (stages 14, 15; lane bias 2^13, 2^14), register bit 6 = the top stage
 #pragma unroll
-      for (int sb = 4; sb < 6; ++sb)
+      for (int sb = 4; sb < (kGenStages == 7 ? 4 : 6); ++sb)
 #pragma unroll
         for (int k = 0; k < 128; ++k)
           if ((k & (1 << sb)) == 0) {
@@ -344,12 +408,19 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
       }
       const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<16>(mx, mn)));
       if (lane == 0) s_wmax[i & 3][mw] = m;
+#if SBW_LUT_DONE_LATE
+      if (i + 2 < n_my) gen_done(i & 1);  // MMA(i+2) cannot start before the next TMEM read anyway
+#endif
+#if SBW_LUT_SPLIT
+      if (gen) gen_stages();
+#else
       if (gen) {  // B(i+3) into registers (R is dead)
         xor_pl(pa);
         if (d) xor_all(d);  // rare: more than one changed bit
         vcur = vn;
         gen_compute();
       }
+#endif
     }
     tc::fence_before();
     mbar_arrive(&bar_done);
