@@ -393,10 +393,23 @@ def run_ours(args, rank, world, local_rank):
         alu_ops = (n - 8) * (1 << n) * nmask
         mma_ops = 2 * 256 * 256 * 288 * items
         achieved = alu_ops / (kern_ms * 1e-3)
+        # n = 16 (unless SBW_TC_LUT=0): k_tc_lut, the GEMM contracts x bits
+        # 8..15 and the other 8 stages are 3 by table lookup (byte -> 8-point
+        # WHT, LDS.64), 4 as byte-lane butterflies and the top one on packed
+        # int16 lanes with the max fold.  Its busiest unit is the tensor pipe
+        # (ncu: 2304 MMA cycles of ~3200 per component; ALU pipe ~52 %), so the
+        # GEMM half is the primary roofline there and the integer half sits
+        # beside it under "integer".
+        lut = n == 16 and os.environ.get("SBW_TC_LUT", "1") != "0"
+        kernel_name = (
+            "k_tc_lut (tcgen05 int8 GEMM over x bits 8..15; x bits 0..7: 3 stages by shared-memory "
+            "table lookup, 4 byte-lane stages on the GEMM operand, the top stage + max fold on packed "
+            "int16 lanes)" if lut else
+            f"k_tc_hybrid<NL, {n}> (tcgen05 int8 GEMM over x bits 0..7; x bits 8..{n - 1} on "
+            "the integer ALUs: 4 byte-lane stages on the GEMM operand + packed int16 stages)")
         roofline = {
             "bound": "int32_alu",
-            "kernel": f"k_tc_hybrid<NL, {n}> (tcgen05 int8 GEMM over x bits 0..7; x bits 8..{n - 1} on "
-                      "the integer ALUs: 4 byte-lane stages on the GEMM operand + packed int16 stages)",
+            "kernel": kernel_name,
             "achieved": achieved / 1e12, "peak": 2 * peak / 1e12, "unit": "Tops/s",
             "frac": achieved / (2 * peak), "traffic": traffic,
             "ops_per_launch": alu_ops,
@@ -423,6 +436,25 @@ def run_ours(args, rank, world, local_rank):
                                  "vs_packed16_alu_peak": n * (1 << n) * nmask / (kern_ms * 1e-3)
                                  / (2 * peak)},
         }
+        if lut:
+            # primary: the tensor pipe; "integer" keeps the previous primary numbers
+            integer = {k: roofline[k] for k in ("achieved", "peak", "unit", "frac", "ops_per_launch",
+                                                "ops_definition", "peak_source", "peak_dual_issue",
+                                                "frac_dual_issue", "peak_dual_issue_source")}
+            integer["ops_definition"] = (
+                "integer half: 8 stages x 2^16 butterfly element-ops per component (x bits 0..7: "
+                "3 by table lookup, 4 byte-lane, 1 int16-lane stage incl. the max fold) against the "
+                "packed-16x2 ALU rate")
+            t = roofline["tensor"]
+            roofline = {
+                "bound": "tensor", "kernel": kernel_name,
+                "achieved": t["achieved"], "peak": t["peak"], "unit": t["unit"], "frac": t["frac"],
+                "traffic": traffic, "ops_per_launch": t["ops_per_launch"],
+                "ops_definition": "GEMM half: 2 * 256 (M) * 256 (N) * 288 (K: x bits 8..15 + the bias "
+                                  "block) int8 ops per component, 8 of the 16 stages",
+                "kernel_ms": kern_ms, "peak_source": t["peak_source"],
+                "integer": integer, "whole_fwht_equiv": roofline["whole_fwht_equiv"],
+            }
     elif n >= 17:
         # Multi-pass K3: pass A (k_tc_hybrid<emit>) writes every component's
         # stage-15 partial transform as u16 and pass B reads it back -- 4 B of

@@ -44,15 +44,10 @@ namespace {
 #define SBW_LUT_COPIES 16  // table replicas (lane & 15 picks one): LDS.64 without bank conflicts
 #endif
 constexpr int kCopies = SBW_LUT_COPIES;
-#ifndef SBW_LUT_STS_EARLY
-#define SBW_LUT_STS_EARLY 0  // 1: B(i+2) stores issued under the TMEM loads of item i (measured 1.11 vs 0.86 ms)
+#ifndef SBW_LUT_HALVES
+#define SBW_LUT_HALVES 1  // the two M = 128 halves of a component complete and are consumed separately
 #endif
-#ifndef SBW_LUT_DONE_LATE
-#define SBW_LUT_DONE_LATE 0  // 1: proxy fence + bfull arrive after the item's stages (0.864 vs 0.862 ms)
-#endif
-#ifndef SBW_LUT_SPLIT
-#define SBW_LUT_SPLIT 1  // lookups of B(i+3) issued before item i's stages, their byte stages after the fold
-#endif
+constexpr bool kHalves = SBW_LUT_HALVES;
 #ifndef SBW_LUT_GEN7
 #define SBW_LUT_GEN7 1  // r bits 5, 6 as two more byte-lane stages across a thread's 4 words (else int16 stages)
 #endif
@@ -157,24 +152,22 @@ __device__ __forceinline__ void publish(const uint32_t* wmax, uint32_t v, const 
   if (a.key) atomicMax(a.key, nl_key(m, v));
 }
 
-// MMA chain of one mask: 2 M-halves x (8 K blocks of generated B + the bias block)
-__device__ __forceinline__ void issue_mma(uint32_t tmem, const uint8_t* smem, int buf, uint64_t* bar) {
+// MMA chain of one M = 128 half of a mask: 8 K blocks of generated B + the bias block
+__device__ __forceinline__ void issue_mma_half(uint32_t tmem, const uint8_t* smem, int buf, int h, uint64_t* bar) {
   const uint64_t dhs = tc::sdesc(tc::smem_u32(smem + kHsOff), 128, 1024);
   const uint64_t dab = tc::sdesc(tc::smem_u32(smem + kAbOff), 128, 256);
   const uint64_t db0 = sdesc_mn_sw128(tc::smem_u32(smem + kBOff + buf * kBBytes), 1024, 2048);
   const uint64_t dbb = tc::sdesc(tc::smem_u32(smem + kBbOff), 128, 256);
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int kb = 0; kb < 9; ++kb) {
-      // A: K block kb of half h = block kb & 3 of Hs (-Hs for h = 1, kb >= 4)
-      const uint64_t da = kb == 8 ? dab + uint64_t((h * 4096) >> 4)
-                                  : dhs + uint64_t((((h == 1 && kb >= 4) ? kNegOff - kHsOff : 0) + (kb & 3) * 256) >> 4);
-      // B: K block kb = 32 K-rows = 4 groups of 8 (2048 B each)
-      const uint64_t db = kb == 8 ? dbb : db0 + uint64_t((kb * 8192) >> 4);
-      tc::mma_i8_elect(tmem + h * 256, da, db, kb == 8 ? kIdescK : kIdescMN, kb > 0 ? 1u : 0u);
-    }
-  tc::mma_commit_elect(bar);
+  for (int kb = 0; kb < 9; ++kb) {
+    // A: K block kb of half h = block kb & 3 of Hs (-Hs for h = 1, kb >= 4)
+    const uint64_t da = kb == 8 ? dab + uint64_t((h * 4096) >> 4)
+                                : dhs + uint64_t((((h == 1 && kb >= 4) ? kNegOff - kHsOff : 0) + (kb & 3) * 256) >> 4);
+    // B: K block kb = 32 K-rows = 4 groups of 8 (2048 B each)
+    const uint64_t db = kb == 8 ? dbb : db0 + uint64_t((kb * 8192) >> 4);
+    tc::mma_i8_elect(tmem + h * 256, da, db, kb == 8 ? kIdescK : kIdescMN, kb > 0 ? 1u : 0u);
+  }
+  if (bar) tc::mma_commit_elect(bar);
 }
 
 // One plane word (32 component bits of row c, r = 32 ks ..) -> the 32 bytes
@@ -202,7 +195,11 @@ __device__ __forceinline__ void word_stages(uint4& lo, uint4& hi) {
 
 __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar_full, bar_tmem_empty, bar_bfull[2], bar_done;
+  // full[h]: MMA(i) half h done (kHalves; else full[0] = both).  tmem_empty[h]:
+  // D(i) half h read.  kHalves: warps 0-3 (half 0) also arrive on tmem_empty[1]
+  // once they have seen full[1](i), so full[1] never runs two phases ahead of
+  // their parity wait.  bfull[b]: every transform thread stored B into buffer b.
+  __shared__ uint64_t bar_full[2], bar_tmem_empty[2], bar_bfull[2], bar_done;
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(16) uint32_t s_wmax[4][kMathWarps];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -216,8 +213,10 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
     reinterpret_cast<uint4*>(smem + kLutOff)[e] = __ldg(reinterpret_cast<const uint4*>(a.consts + kBOff) + e);
   if (warp == 0) tc::tmem_alloc(&tmem_slot, 512);
   if (tid == 0) {
-    tc::mbar_init(&bar_full, 1);
-    tc::mbar_init(&bar_tmem_empty, kMathWarps * 32);
+    tc::mbar_init(&bar_full[0], 1);
+    tc::mbar_init(&bar_full[1], 1);
+    tc::mbar_init(&bar_tmem_empty[0], kHalves ? kMathWarps * 16 : kMathWarps * 32);
+    tc::mbar_init(&bar_tmem_empty[1], kMathWarps * 32);
     tc::mbar_init(&bar_bfull[0], kMathWarps * 32);
     tc::mbar_init(&bar_bfull[1], kMathWarps * 32);
     tc::mbar_init(&bar_done, kMathWarps * 32);
@@ -234,10 +233,21 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
     if (warp == 0) {
       for (int i = 0; i < n_my; ++i) {
         tc::mbar_wait(&bar_bfull[i & 1], uint32_t((i >> 1) & 1));
-        if (i > 0) tc::mbar_wait(&bar_tmem_empty, uint32_t((i - 1) & 1));
-        tc::fence_after();
-        issue_mma(tmem, smem, i & 1, &bar_full);
-        // bfull(i) (i >= 2) follows every thread's store of its maxima of item i - 2
+        if constexpr (kHalves) {
+          // half h of D(i-1) read -> MMA(i) half h; the halves commit separately
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (i > 0) tc::mbar_wait(&bar_tmem_empty[h], uint32_t((i - 1) & 1));
+            tc::fence_after();
+            issue_mma_half(tmem, smem, i & 1, h, &bar_full[h]);
+          }
+        } else {
+          if (i > 0) tc::mbar_wait(&bar_tmem_empty[0], uint32_t((i - 1) & 1));
+          tc::fence_after();
+          issue_mma_half(tmem, smem, i & 1, 0, nullptr);
+          issue_mma_half(tmem, smem, i & 1, 1, &bar_full[0]);
+        }
+        // tmem_empty(i-1) follows every thread's store of its maxima of item i - 2
         if (i >= 2 && lane == 0)
           publish(s_wmax[(i - 2) & 3], mask_at(int64_t(a.v_lo) + t_lo + i - 2, a.v_lo, a.v_hi), a);
       }
@@ -345,6 +355,7 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
     }
     // TMEM lane of this thread (warp w may only touch lanes 32 (w % 4) .. + 31)
     const uint32_t tbase = tmem + (uint32_t((mw & 3) * 32) << 16) + uint32_t(mw >> 2) * 256;
+    const int hg = kHalves ? (mw >> 2) : 0;  // which M half this warp reads
     for (int i = 0; i < n_my; ++i) {
       // prefetch the first changed plane of the item three steps ahead
       const bool gen = i + 3 < n_my;
@@ -358,69 +369,71 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
           d &= d - 1;
         }
       }
-      tc::mbar_wait(&bar_full, uint32_t(i & 1));
+      tc::mbar_wait(&bar_full[hg], uint32_t(i & 1));
       tc::fence_after();
       uint32_t R[128];
       uint32_t(&R0)[64] = *reinterpret_cast<uint32_t(*)[64]>(&R[0]);
       uint32_t(&R1)[64] = *reinterpret_cast<uint32_t(*)[64]>(&R[64]);
       tc::tmem_ld_x64_p16(tbase, R0);
       tc::tmem_ld_x64_p16(tbase + 128, R1);
-#if SBW_LUT_STS_EARLY
-      if (i + 2 < n_my) gen_sts(i & 1);  // B(i+2) into the buffer MMA(i) released, under the TMEM loads
-#endif
       tc::wait_ld_tied(R0);
       tc::wait_ld_tied(R1);
       tc::fence_before();
-      mbar_arrive(&bar_tmem_empty);      // MMA(i+1) may start: no fence or barrier sits in that gap
-#if !SBW_LUT_STS_EARLY
-      if (i + 2 < n_my) gen_sts(i & 1);  // B(i+2) into the buffer MMA(i) released
-#endif
-#if !SBW_LUT_DONE_LATE
-      if (i + 2 < n_my) gen_done(i & 1);
-#endif
-#if SBW_LUT_SPLIT
-      if (gen) {  // B(i+3): lookups in flight under this item's stages
-        xor_pl(pa);
-        if (d) xor_all(d);  // rare: more than one changed bit
-        vcur = vn;
-        gen_lookup();
+      // MMA(i+1) (this half) may start: no fence or store sits in that gap.
+      // (B stores issued under the TMEM loads: 1.11 vs 0.86 ms; the proxy fence
+      // and bfull arrive moved behind the fold: 0.864 vs 0.862 ms.)
+      mbar_arrive(&bar_tmem_empty[hg]);
+      // B(i+2) from o[] into the buffer MMA(i) released; then B(i+3): plane XOR
+      // and the 32 lookups, in flight under the fold
+      auto next_b = [&]() {
+        if (i + 2 < n_my) {
+          gen_sts(i & 1);
+          gen_done(i & 1);
+        }
+        if (gen) {
+          xor_pl(pa);
+          if (d) xor_all(d);  // rare: more than one changed bit
+          vcur = vn;
+          gen_lookup();
+        }
+      };
+      // R[j] = columns (2j, 2j + 1), D = W_15 / 2 + 2^14; register bit 6 = column
+      // bit 7 = r bit 7: the top stage, fused with the max / min fold
+      auto fold = [&]() {
+#pragma unroll
+        for (int sb = 4; sb < (kGenStages == 7 ? 4 : 6); ++sb)  // 5-stage generation: r bits 5, 6 here
+#pragma unroll
+          for (int k = 0; k < 128; ++k)
+            if ((k & (1 << sb)) == 0) {
+              const uint32_t x = R[k], y = R[k | (1 << sb)];
+              R[k] = x + y;
+              R[k | (1 << sb)] = x - y + (0x02000200u << sb);
+            }
+        uint32_t mx = 0u, mn = 0xFFFFFFFFu;
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          const uint32_t x = R[k], y = R[k + 64];
+          const uint32_t S = x + y;
+          const uint32_t D = x - y + 0x80008000u;
+          mx = __vimax3_u16x2(mx, S, D);
+          mn = __vimin3_u16x2(mn, S, D);
+        }
+        const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<16>(mx, mn)));
+        if (lane == 0) s_wmax[i & 3][mw] = m;
+      };
+      if (kHalves && hg == 0) {
+        // half 0 is ready half a GEMM before MMA(i) has released B(i)'s buffer:
+        // fold first, store afterwards
+        fold();
+        tc::mbar_wait(&bar_full[1], uint32_t(i & 1));
+        tc::fence_after();
+        mbar_arrive(&bar_tmem_empty[1]);
+        next_b();
+      } else {
+        next_b();
+        fold();
       }
-#endif
-      // R[j] = columns (2j, 2j + 1): column bits 5, 6 = register bits 4, 5
-      // (stages 14, 15; lane bias 2^13, 2^14), register bit 6 = the top stage
-#pragma unroll
-      for (int sb = 4; sb < (kGenStages == 7 ? 4 : 6); ++sb)
-#pragma unroll
-        for (int k = 0; k < 128; ++k)
-          if ((k & (1 << sb)) == 0) {
-            const uint32_t x = R[k], y = R[k | (1 << sb)];
-            R[k] = x + y;
-            R[k | (1 << sb)] = x - y + (0x02000200u << sb);
-          }
-      uint32_t mx = 0u, mn = 0xFFFFFFFFu;
-#pragma unroll
-      for (int k = 0; k < 64; ++k) {
-        const uint32_t x = R[k], y = R[k + 64];
-        const uint32_t S = x + y;
-        const uint32_t D = x - y + 0x80008000u;
-        mx = __vimax3_u16x2(mx, S, D);
-        mn = __vimin3_u16x2(mn, S, D);
-      }
-      const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<16>(mx, mn)));
-      if (lane == 0) s_wmax[i & 3][mw] = m;
-#if SBW_LUT_DONE_LATE
-      if (i + 2 < n_my) gen_done(i & 1);  // MMA(i+2) cannot start before the next TMEM read anyway
-#endif
-#if SBW_LUT_SPLIT
       if (gen) gen_stages();
-#else
-      if (gen) {  // B(i+3) into registers (R is dead)
-        xor_pl(pa);
-        if (d) xor_all(d);  // rare: more than one changed bit
-        vcur = vn;
-        gen_compute();
-      }
-#endif
     }
     tc::fence_before();
     mbar_arrive(&bar_done);

@@ -78,14 +78,16 @@ print(json.dumps(out))
 
 
 def test_tensor_core_kernel_matches_alu_kernel():
-    """Same maxima and key from k_tc_hybrid<NL> and from k_tile_simd<16> (SBW_TC=0)."""
+    """Same maxima and key from the three n = 16 NL kernels: k_tc_lut (default),
+    k_tc_hybrid<NL> (SBW_TC_LUT=0) and the all-ALU k_tile_simd<16> (SBW_TC=0)."""
     res = {}
-    for tc in ("1", "0"):
-        p = subprocess.run([sys.executable, "-c", _ARM, ROOT], env=dict(os.environ, SBW_TC=tc),
+    for arm, env in (("lut", {}), ("hybrid", {"SBW_TC_LUT": "0"}), ("alu", {"SBW_TC": "0"})):
+        p = subprocess.run([sys.executable, "-c", _ARM, ROOT], env=dict(os.environ, **env),
                            capture_output=True, text=True, timeout=600)
         assert p.returncode == 0, p.stderr[-2000:]
-        res[tc] = json.loads(p.stdout.strip().splitlines()[-1])
-    assert res["1"] == res["0"]
+        res[arm] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["lut"] == res["alu"]
+    assert res["hybrid"] == res["alu"]
 
 
 def test_live_peak_microbenchmarks():
