@@ -48,6 +48,9 @@ constexpr int kCopies = SBW_LUT_COPIES;
 #define SBW_LUT_HALVES 1  // the two M = 128 halves of a component complete and are consumed separately
 #endif
 constexpr bool kHalves = SBW_LUT_HALVES;
+#ifndef SBW_LUT_WARPS_DEFAULT
+#define SBW_LUT_WARPS_DEFAULT 16  // transform warps: 8 (k_tc_lut) or 16 (k_tc_lut16); SBW_LUT_WARPS overrides
+#endif
 #ifndef SBW_LUT_GEN7
 #define SBW_LUT_GEN7 1  // r bits 5, 6 as two more byte-lane stages across a thread's 4 words (else int16 stages)
 #endif
@@ -440,6 +443,194 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_tc_lut16: the same job with 16 transform warps (4 per SM sub-partition
+// instead of 2, so one warp's TMEM / table-lookup latency hides behind three
+// others).  Warp mw = (column half ch, M half h, lane quarter): it reads the 128
+// TMEM columns {64 ch .. + 63} u {128 + 64 ch .. + 63} of its lanes (the top
+// stage pairs column n with n + 128) into 64 packed registers, and generates
+// one (row c, word quad q) unit of B: 4 plane words, 16 lookups, 32 output
+// registers.  Every warp runs: wait full[h](i) -> read D -> tmem_empty[h] ->
+// fold -> B(i+2) into registers -> (half 0: wait full[1](i), tmem_empty[1]) ->
+// store B(i+2) -> bfull, so TMEM values and B bytes are never live together
+// (112 registers per transform thread: 640 threads x 96 at launch, the issuer
+// warpgroup drops to 24).
+constexpr int kW16 = 16;
+constexpr int kThreads16 = 128 + kW16 * 32;
+constexpr int kIssuerRegs16 = 24, kMathRegs16 = 112;
+static_assert(4 * 32 * kIssuerRegs16 + kW16 * 32 * kMathRegs16 <= kThreads16 * 96,
+              "setmaxnreg split must fit the CTA's launch allocation (640 x 96 registers)");
+
+__global__ void __launch_bounds__(kThreads16, 1) k_tc_lut16(LutArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar_full[2], bar_tmem_empty[2], bar_bfull[2], bar_done;
+  __shared__ uint32_t tmem_slot;
+  __shared__ __align__(16) uint32_t s_wmax[4][kW16];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t total = int64_t(a.v_hi) - a.v_lo;
+  const int64_t t_lo = total * blockIdx.x / gridDim.x;
+  const int n_my = int(total * (blockIdx.x + 1) / gridDim.x - t_lo);
+
+  for (int e = tid; e < kBOff / 16; e += kThreads16)
+    reinterpret_cast<uint4*>(smem)[e] = __ldg(reinterpret_cast<const uint4*>(a.consts) + e);
+  for (int e = tid; e < kLutBytes / 16; e += kThreads16)
+    reinterpret_cast<uint4*>(smem + kLutOff)[e] = __ldg(reinterpret_cast<const uint4*>(a.consts + kBOff) + e);
+  if (warp == 0) tc::tmem_alloc(&tmem_slot, 512);
+  if (tid == 0) {
+    tc::mbar_init(&bar_full[0], 1);
+    tc::mbar_init(&bar_full[1], 1);
+    tc::mbar_init(&bar_tmem_empty[0], kW16 * 16);  // the half-0 warps
+    tc::mbar_init(&bar_tmem_empty[1], kW16 * 32);  // the half-1 warps + the half-0 warps after full[1]
+    tc::mbar_init(&bar_bfull[0], kW16 * 32);
+    tc::mbar_init(&bar_bfull[1], kW16 * 32);
+    tc::mbar_init(&bar_done, kW16 * 32);
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kIssuerRegs16));
+    if (warp == 0) {
+      auto publish16 = [&](int i) {
+        const uint32_t* w = s_wmax[i & 3];
+        uint32_t m = 0;
+#pragma unroll
+        for (int k = 0; k < kW16; ++k) m = max(m, w[k]);
+        const uint32_t v = mask_at(int64_t(a.v_lo) + t_lo + i, a.v_lo, a.v_hi);
+        a.max_abs[v - a.v_lo] = int(m);
+        if (a.key) atomicMax(a.key, nl_key(int(m), v));
+      };
+      for (int i = 0; i < n_my; ++i) {
+        tc::mbar_wait(&bar_bfull[i & 1], uint32_t((i >> 1) & 1));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (i > 0) tc::mbar_wait(&bar_tmem_empty[h], uint32_t((i - 1) & 1));
+          tc::fence_after();
+          issue_mma_half(tmem, smem, i & 1, h, &bar_full[h]);
+        }
+        if (i >= 2 && lane == 0) publish16(i - 2);
+      }
+      tc::mbar_wait(&bar_done, 0u);
+      tc::fence_after();
+      if (lane == 0)
+        for (int i = n_my - 2 < 0 ? 0 : n_my - 2; i < n_my; ++i) publish16(i);
+      __syncwarp();
+      tc::tmem_dealloc(tmem, 512);
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kMathRegs16));
+    const int mt = tid - 128, mw = mt >> 5;
+    const int hg = (mw >> 2) & 1, ch = mw >> 3;
+    // generation unit: row c = 16 mw + (lane & 7) + 8 (lane >> 4), word quad q = lane bit 3
+    const int q = (lane >> 3) & 1;
+    const int c = 16 * mw + (lane & 7) + 8 * (lane >> 4);
+    const uint32_t* __restrict__ pl = a.planes + c * 8 + 4 * q;
+    const uint32_t lut = tc::smem_u32(smem + kLutOff) + uint32_t(lane & (kCopies - 1)) * 8u;
+    const uint32_t row_off = uint32_t(kBOff + (c >> 3) * 2048 + q * 1024 + (c & 7) * 128);
+    uint4 g = make_uint4(0, 0, 0, 0);
+    uint32_t vcur = 0;
+    auto xor_all = [&](uint32_t d) {
+      while (d) {
+        const int i = __ffs(d) - 1;
+        d &= d - 1;
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(pl + int64_t(i) * 2048));
+        g.x ^= x.x; g.y ^= x.y; g.z ^= x.z; g.w ^= x.w;
+      }
+    };
+    uint4 o[8];
+    auto gen_compute = [&]() {
+      word_lookup(g.x, lut, o[0], o[1]);
+      word_lookup(g.y, lut, o[2], o[3]);
+      word_lookup(g.z, lut, o[4], o[5]);
+      word_lookup(g.w, lut, o[6], o[7]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) word_stages(o[2 * k], o[2 * k + 1]);
+      auto bfly = [](uint4& x, uint4& y, uint32_t b) {
+        const uint4 s4 = make_uint4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
+        y = make_uint4(x.x - y.x + b, x.y - y.y + b, x.z - y.z + b, x.w - y.w + b);
+        x = s4;
+      };
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {  // r bits 5, 6 across the 4 words
+        bfly(o[j], o[2 + j], 0x20202020u);
+        bfly(o[4 + j], o[6 + j], 0x20202020u);
+        bfly(o[j], o[4 + j], 0x40404040u);
+        bfly(o[2 + j], o[6 + j], 0x40404040u);
+      }
+    };
+    auto gen_sts = [&](int buf) {
+      uint8_t* row = smem + row_off + buf * kBBytes;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        *reinterpret_cast<uint4*>(row + (((2 * w) ^ (c & 7)) << 4)) = o[2 * w];
+        *reinterpret_cast<uint4*>(row + (((2 * w + 1) ^ (c & 7)) << 4)) = o[2 * w + 1];
+      }
+      tc::fence_proxy_async();
+      mbar_arrive(&bar_bfull[buf]);
+    };
+    for (int k = 0; k < 2 && k < n_my; ++k) {
+      const uint32_t vn = mask_at(int64_t(a.v_lo) + t_lo + k, a.v_lo, a.v_hi);
+      xor_all(vcur ^ vn);
+      vcur = vn;
+      gen_compute();
+      gen_sts(k);
+    }
+    const uint32_t tbase = tmem + (uint32_t((mw & 3) * 32) << 16) + uint32_t(hg) * 256 + uint32_t(ch) * 64;
+    for (int i = 0; i < n_my; ++i) {
+      // prefetch the first changed plane of the item two steps ahead
+      const bool gen = i + 2 < n_my;
+      uint32_t vn = 0, d = 0;
+      uint4 pa = make_uint4(0, 0, 0, 0);
+      if (gen) {
+        vn = mask_at(int64_t(a.v_lo) + t_lo + i + 2, a.v_lo, a.v_hi);
+        d = vcur ^ vn;
+        if (d) {
+          pa = __ldg(reinterpret_cast<const uint4*>(pl + int64_t(__ffs(d) - 1) * 2048));
+          d &= d - 1;
+        }
+      }
+      tc::mbar_wait(&bar_full[hg], uint32_t(i & 1));
+      tc::fence_after();
+      {
+        uint32_t X[32], Y[32];  // columns 64 ch + (2j, 2j+1) and the same + 128
+        tc::tmem_ld_x32_p16(tbase, X);
+        tc::tmem_ld_x32_p16(tbase + 128, Y);
+        tc::wait_ld_tied(X);
+        tc::wait_ld_tied(Y);
+        tc::fence_before();
+        mbar_arrive(&bar_tmem_empty[hg]);
+        uint32_t mx = 0u, mn = 0xFFFFFFFFu;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const uint32_t S = X[k] + Y[k];
+          const uint32_t D = X[k] - Y[k] + 0x80008000u;
+          mx = __vimax3_u16x2(mx, S, D);
+          mn = __vimin3_u16x2(mn, S, D);
+        }
+        const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<16>(mx, mn)));
+        if (lane == 0) s_wmax[i & 3][mw] = m;
+      }
+      if (gen) {
+        g.x ^= pa.x; g.y ^= pa.y; g.z ^= pa.z; g.w ^= pa.w;
+        if (d) xor_all(d);  // rare: more than one changed bit
+        vcur = vn;
+        gen_compute();
+      }
+      if (hg == 0) {  // B(i)'s buffer is free once MMA(i) half 1 is done too
+        tc::mbar_wait(&bar_full[1], uint32_t(i & 1));
+        tc::fence_after();
+        mbar_arrive(&bar_tmem_empty[1]);
+      }
+      if (gen) gen_sts(i & 1);
+    }
+    tc::fence_before();
+    mbar_arrive(&bar_done);
+  }
+}
+
 std::mutex g_lut_mu;
 uint8_t* g_lut_consts[64] = {};
 int lut_consts(int dev, cudaStream_t st, const uint8_t** out) {
@@ -476,6 +667,7 @@ int launch_tc16_nl_lut(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int
   static unsigned long long attr_done = 0;
   if (!(attr_done >> (dp.device & 63) & 1ull)) {
     SBW_CUDA_CHECK(cudaFuncSetAttribute(k_tc_lut, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    SBW_CUDA_CHECK(cudaFuncSetAttribute(k_tc_lut16, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     attr_done |= 1ull << (dp.device & 63);
   }
   LutArgs a{};
@@ -486,6 +678,12 @@ int launch_tc16_nl_lut(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int
   a.max_abs = max_abs;
   a.key = key;
   const int grid = int(items < dp.sm_count ? items : dp.sm_count);
+  static const int warps = getenv("SBW_LUT_WARPS") ? atoi(getenv("SBW_LUT_WARPS")) : SBW_LUT_WARPS_DEFAULT;
+  if (warps == 16) {
+    k_tc_lut16<<<grid, kThreads16, kSmem, st>>>(a);
+    SBW_LAUNCH_CHECK("k_tc_lut16");
+    return SBW_OK;
+  }
   k_tc_lut<<<grid, kAllThreads, kSmem, st>>>(a);
   SBW_LAUNCH_CHECK("k_tc_lut");
   return SBW_OK;
