@@ -455,6 +455,9 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
 // store B(i+2) -> bfull, so TMEM values and B bytes are never live together
 // (112 registers per transform thread: 640 threads x 96 at launch, the issuer
 // warpgroup drops to 24).
+#ifndef SBW_LUT_PIN
+#define SBW_LUT_PIN 1
+#endif
 constexpr int kW16 = 16;
 constexpr int kThreads16 = 128 + kW16 * 32;
 constexpr int kIssuerRegs16 = 24, kMathRegs16 = 112;
@@ -529,7 +532,14 @@ __global__ void __launch_bounds__(kThreads16, 1) k_tc_lut16(LutArgs a) {
     const int c = 16 * mw + (lane & 7) + 8 * (lane >> 4);
     const uint32_t* __restrict__ pl = a.planes + c * 8 + 4 * q;
     const uint32_t lut = tc::smem_u32(smem + kLutOff) + uint32_t(lane & (kCopies - 1)) * 8u;
-    const uint32_t row_off = uint32_t(kBOff + (c >> 3) * 2048 + q * 1024 + (c & 7) * 128);
+    uint32_t row_off = uint32_t(kBOff + (c >> 3) * 2048 + q * 1024 + (c & 7) * 128);
+    uint32_t sw = uint32_t(c & 7) << 4;  // swizzle XOR of this row's chunk offsets
+#if SBW_LUT_PIN
+    // thread constants as opaque register values: otherwise ptxas re-derives them from
+    // S2R SR_TID.X in every iteration (short-scoreboard stalls on the S2R results)
+    asm volatile("mov.b32 %0, %0;" : "+r"(row_off));
+    asm volatile("mov.b32 %0, %0;" : "+r"(sw));
+#endif
     uint4 g = make_uint4(0, 0, 0, 0);
     uint32_t vcur = 0;
     auto xor_all = [&](uint32_t d) {
@@ -565,8 +575,8 @@ __global__ void __launch_bounds__(kThreads16, 1) k_tc_lut16(LutArgs a) {
       uint8_t* row = smem + row_off + buf * kBBytes;
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
-        *reinterpret_cast<uint4*>(row + (((2 * w) ^ (c & 7)) << 4)) = o[2 * w];
-        *reinterpret_cast<uint4*>(row + (((2 * w + 1) ^ (c & 7)) << 4)) = o[2 * w + 1];
+        *reinterpret_cast<uint4*>(row + (uint32_t(32 * w) ^ sw)) = o[2 * w];
+        *reinterpret_cast<uint4*>(row + (uint32_t(32 * w + 16) ^ sw)) = o[2 * w + 1];
       }
       tc::fence_proxy_async();
       mbar_arrive(&bar_bfull[buf]);
@@ -578,7 +588,10 @@ __global__ void __launch_bounds__(kThreads16, 1) k_tc_lut16(LutArgs a) {
       gen_compute();
       gen_sts(k);
     }
-    const uint32_t tbase = tmem + (uint32_t((mw & 3) * 32) << 16) + uint32_t(hg) * 256 + uint32_t(ch) * 64;
+    uint32_t tbase = tmem + (uint32_t((mw & 3) * 32) << 16) + uint32_t(hg) * 256 + uint32_t(ch) * 64;
+#if SBW_LUT_PIN
+    asm volatile("mov.b32 %0, %0;" : "+r"(tbase));
+#endif
     for (int i = 0; i < n_my; ++i) {
       // prefetch the first changed plane of the item two steps ahead
       const bool gen = i + 2 < n_my;
