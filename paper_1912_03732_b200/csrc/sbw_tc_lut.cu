@@ -455,9 +455,6 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
 // store B(i+2) -> bfull, so TMEM values and B bytes are never live together
 // (112 registers per transform thread: 640 threads x 96 at launch, the issuer
 // warpgroup drops to 24).
-#ifndef SBW_LUT_PIN
-#define SBW_LUT_PIN 1
-#endif
 constexpr int kW16 = 16;
 constexpr int kThreads16 = 128 + kW16 * 32;
 constexpr int kIssuerRegs16 = 24, kMathRegs16 = 112;
@@ -471,8 +468,18 @@ __global__ void __launch_bounds__(kThreads16, 1) k_tc_lut16(LutArgs a) {
   __shared__ __align__(16) uint32_t s_wmax[4][kW16];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t total = int64_t(a.v_hi) - a.v_lo;
-  const int64_t t_lo = total * blockIdx.x / gridDim.x;
-  const int n_my = int(total * (blockIdx.x + 1) / gridDim.x - t_lo);
+  const int64_t t_lo64 = total * blockIdx.x / gridDim.x;
+  const int n_my = int(total * (blockIdx.x + 1) / gridDim.x - t_lo64);
+  const uint32_t q_lo = a.v_lo + uint32_t(t_lo64);  // natural position of this CTA's first mask (< 2^24)
+  // mask_at in 32-bit arithmetic (positions and masks are below 2^24)
+  auto mask32 = [&](uint32_t qpos) -> uint32_t {
+    const uint32_t b = qpos & ~255u;
+    if (b >= a.v_lo && b + 256u <= a.v_hi) {
+      const uint32_t kk = qpos & 255u;
+      return b | (kk ^ (kk >> 1));
+    }
+    return qpos;
+  };
 
   for (int e = tid; e < kBOff / 16; e += kThreads16)
     reinterpret_cast<uint4*>(smem)[e] = __ldg(reinterpret_cast<const uint4*>(a.consts) + e);
@@ -502,7 +509,7 @@ __global__ void __launch_bounds__(kThreads16, 1) k_tc_lut16(LutArgs a) {
         uint32_t m = 0;
 #pragma unroll
         for (int k = 0; k < kW16; ++k) m = max(m, w[k]);
-        const uint32_t v = mask_at(int64_t(a.v_lo) + t_lo + i, a.v_lo, a.v_hi);
+        const uint32_t v = mask32(q_lo + uint32_t(i));
         a.max_abs[v - a.v_lo] = int(m);
         if (a.key) atomicMax(a.key, nl_key(int(m), v));
       };
@@ -532,14 +539,10 @@ __global__ void __launch_bounds__(kThreads16, 1) k_tc_lut16(LutArgs a) {
     const int c = 16 * mw + (lane & 7) + 8 * (lane >> 4);
     const uint32_t* __restrict__ pl = a.planes + c * 8 + 4 * q;
     const uint32_t lut = tc::smem_u32(smem + kLutOff) + uint32_t(lane & (kCopies - 1)) * 8u;
-    uint32_t row_off = uint32_t(kBOff + (c >> 3) * 2048 + q * 1024 + (c & 7) * 128);
-    uint32_t sw = uint32_t(c & 7) << 4;  // swizzle XOR of this row's chunk offsets
-#if SBW_LUT_PIN
-    // thread constants as opaque register values: otherwise ptxas re-derives them from
-    // S2R SR_TID.X in every iteration (short-scoreboard stalls on the S2R results)
-    asm volatile("mov.b32 %0, %0;" : "+r"(row_off));
-    asm volatile("mov.b32 %0, %0;" : "+r"(sw));
-#endif
+    const uint32_t row_off = uint32_t(kBOff + (c >> 3) * 2048 + q * 1024 + (c & 7) * 128);
+    const uint32_t sw = uint32_t(c & 7) << 4;  // swizzle XOR of this row's chunk offsets
+    // (pinning these thread constants in registers, so ptxas cannot re-derive them
+    // from S2R SR_TID.X every iteration, was slower: 0.725 vs 0.711 ms at 112 registers)
     uint4 g = make_uint4(0, 0, 0, 0);
     uint32_t vcur = 0;
     auto xor_all = [&](uint32_t d) {
@@ -582,23 +585,21 @@ __global__ void __launch_bounds__(kThreads16, 1) k_tc_lut16(LutArgs a) {
       mbar_arrive(&bar_bfull[buf]);
     };
     for (int k = 0; k < 2 && k < n_my; ++k) {
-      const uint32_t vn = mask_at(int64_t(a.v_lo) + t_lo + k, a.v_lo, a.v_hi);
+      const uint32_t vn = mask32(q_lo + uint32_t(k));
       xor_all(vcur ^ vn);
       vcur = vn;
       gen_compute();
       gen_sts(k);
     }
-    uint32_t tbase = tmem + (uint32_t((mw & 3) * 32) << 16) + uint32_t(hg) * 256 + uint32_t(ch) * 64;
-#if SBW_LUT_PIN
-    asm volatile("mov.b32 %0, %0;" : "+r"(tbase));
-#endif
+    const uint32_t tbase = tmem + (uint32_t((mw & 3) * 32) << 16) + uint32_t(hg) * 256 + uint32_t(ch) * 64;
+
     for (int i = 0; i < n_my; ++i) {
       // prefetch the first changed plane of the item two steps ahead
       const bool gen = i + 2 < n_my;
       uint32_t vn = 0, d = 0;
       uint4 pa = make_uint4(0, 0, 0, 0);
       if (gen) {
-        vn = mask_at(int64_t(a.v_lo) + t_lo + i + 2, a.v_lo, a.v_hi);
+        vn = mask32(q_lo + uint32_t(i) + 2u);
         d = vcur ^ vn;
         if (d) {
           pa = __ldg(reinterpret_cast<const uint4*>(pl + int64_t(__ffs(d) - 1) * 2048));
