@@ -30,6 +30,11 @@ bool tc_path_enabled();
 bool tc_lut_enabled();
 int launch_tc16_nl_lut(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
                        unsigned long long* key, cudaStream_t st);
+// k_tc_lut_emit: pass A of the multi-pass path with the table-lookup generation
+// (exact but measured slower; launch_tc_emit takes it only with SBW_TC_LUT_EMIT=1)
+bool tc_lut_emit_enabled();
+int launch_tc_emit_lut(const uint32_t* planes, int n, uint32_t v_first, int64_t n_comp, uint32_t* emit,
+                       uint32_t run_lo, uint32_t run_hi, cudaStream_t st, const int* gate, int gate_on);
 int tc_min_small_n();  // smallest n of launch_tc_nl_small (11, or 12 for 16-row generation builds)
 int launch_tc_nl_small(const uint32_t* planes, int n, uint32_t v_lo, uint32_t v_hi, int32_t* max_abs,
                        unsigned long long* key, cudaStream_t st);

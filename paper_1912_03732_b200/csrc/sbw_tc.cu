@@ -1321,6 +1321,8 @@ int launch_tc_xmajor_inverse(const uint32_t* inv_planes, int n, uint32_t u_lo, u
 int launch_tc_emit(const uint32_t* planes, int n, uint32_t v_first, int64_t n_comp, uint32_t* emit,
                    uint32_t run_lo, uint32_t run_hi, cudaStream_t st, int emit16, int* flag, const int* gate,
                    int gate_on) {
+  if (!emit16 && tc_lut_emit_enabled())
+    return launch_tc_emit_lut(planes, n, v_first, n_comp, emit, run_lo, run_hi, st, gate, gate_on);
   TcArgs a{};
   a.run_lo = run_lo;
   a.run_hi = run_hi;

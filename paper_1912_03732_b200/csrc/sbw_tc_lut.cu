@@ -101,7 +101,19 @@ __device__ __forceinline__ int a_bias_value(int u, int k) {
 
 // constant image: Hs, -Hs and A's bias block (K-major core matrices), B's
 // bias block, the lookup table
-__global__ void k_lut_consts(uint8_t* img) {
+// EMIT (pass A of the multi-pass path): 14 stages in front of the top int16
+// stage (x bit 15 is left out of the GEMM), bias 2^13 per entry and 2^13 more on
+// row u = 0 of EACH M half
+constexpr int kBiasTE = kBiasT / 2;
+constexpr int kBiasColsE = (kBiasTE / kBiasB + 126) / 127;
+__device__ __forceinline__ int a_bias_value_emit(int ul, int k) {
+  const int col = k % kBiasColsE, last = kBiasTE / kBiasB - 127 * (kBiasColsE - 1);
+  if (k < kBiasColsE) return col < kBiasColsE - 1 ? 127 : last;
+  if (k < 2 * kBiasColsE) return ul == 0 ? (col < kBiasColsE - 1 ? 127 : last) : 0;
+  return 0;
+}
+
+__global__ void k_lut_consts(uint8_t* img, int emit) {
   const int t0 = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
   for (int e = t0; e < 128 * 128; e += nt) {
     const int u = e >> 7, p = e & 127;
@@ -113,7 +125,7 @@ __global__ void k_lut_consts(uint8_t* img) {
   for (int e = t0; e < 256 * 32; e += nt) {
     const int u = e >> 5, k = e & 31, ul = u & 127;
     img[kAbOff + (u >> 7) * 4096 + ((ul >> 3) * 2 + (k >> 4)) * 128 + (ul & 7) * 16 + (k & 15)] =
-        uint8_t(a_bias_value(u, k));
+        uint8_t(emit ? a_bias_value_emit(ul, k) : a_bias_value(u, k));
   }
   for (int e = t0; e < 256 * 32; e += nt) {
     const int n = e >> 5, k = e & 31;
@@ -645,19 +657,254 @@ __global__ void __launch_bounds__(kThreads16, 1) k_tc_lut16(LutArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_tc_lut_emit: pass A of the multi-pass path (n = 17..24) with the same
+// table-lookup generation.  An item is one component x one 2^16 block pair bp;
+// x bit 15 (the pair's block parity = c bit 7 = the M half) stays out of the
+// GEMM -- half h multiplies Hs (128 x 128) with B rows 128 h .. 128 h + 127 only:
+// 2 x (4 + 1) MMAs per item instead of 18 -- so D = W_14 / 2 + 2^13 for x bits
+// 0..6 and 8..14, the int16 stage adds x bit 7, and the thread writes the
+// biased u16 s = W_15 / 2 + 2^14 of block 2 bp + h in a block-internal word order
+// of its own: word ((ch 16 + jj) 128 + u7) 4 + (0..3) for its jj-th uint4 (pass B
+// only pairs equal word positions across blocks, sbw_passb.cuh).  Replaces
+// k_tc_hybrid<EMIT> (7 int16 stages per item on the ALUs).
+struct LutEmitArgs {
+  const uint8_t* consts;
+  const uint32_t* planes;
+  int64_t plane_words;  // 2^n / 32
+  uint32_t v_first;     // batch position j holds mask mask_at(v_first + j, run_lo, run_hi)
+  uint32_t run_lo, run_hi;
+  int64_t n_comp, n_items;
+  int n_full;
+  uint32_t* emit;
+  const int* gate;  // run only if (*gate != 0) == gate_on (gate may be null)
+  int gate_on;
+};
+
+__device__ __forceinline__ void issue_mma_half_emit(uint32_t tmem, const uint8_t* smem, int buf, int h,
+                                                    uint64_t* bar) {
+  const uint64_t dhs = tc::sdesc(tc::smem_u32(smem + kHsOff), 128, 1024);
+  const uint64_t dab = tc::sdesc(tc::smem_u32(smem + kAbOff), 128, 256);
+  const uint64_t db0 = sdesc_mn_sw128(tc::smem_u32(smem + kBOff + buf * kBBytes), 1024, 2048);
+  const uint64_t dbb = tc::sdesc(tc::smem_u32(smem + kBbOff), 128, 256);
+#pragma unroll
+  for (int kb = 0; kb < 5; ++kb) {
+    const uint64_t da = kb == 4 ? dab + uint64_t((h * 4096) >> 4) : dhs + uint64_t((kb * 256) >> 4);
+    const uint64_t db = kb == 4 ? dbb : db0 + uint64_t(((4 * h + kb) * 8192) >> 4);
+    tc::mma_i8_elect(tmem + h * 256, da, db, kb == 4 ? kIdescK : kIdescMN, kb > 0 ? 1u : 0u);
+  }
+  tc::mma_commit_elect(bar);
+}
+
+__global__ void __launch_bounds__(kThreads16, 1) k_tc_lut_emit(LutEmitArgs a) {
+  static_assert(kGenStages == 7, "k_tc_lut_emit assumes the 7-stage generation");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar_full[2], bar_tmem_empty[2], bar_bfull[2], bar_done;
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (a.gate && ((*a.gate != 0) != (a.gate_on != 0))) return;  // CTA-uniform, before any setup
+  const int64_t t_lo = a.n_items * blockIdx.x / gridDim.x;
+  const int n_my = int(a.n_items * (blockIdx.x + 1) / gridDim.x - t_lo);
+
+  for (int e = tid; e < kBOff / 16; e += kThreads16)
+    reinterpret_cast<uint4*>(smem)[e] = __ldg(reinterpret_cast<const uint4*>(a.consts) + e);
+  for (int e = tid; e < kLutBytes / 16; e += kThreads16)
+    reinterpret_cast<uint4*>(smem + kLutOff)[e] = __ldg(reinterpret_cast<const uint4*>(a.consts + kBOff) + e);
+  if (warp == 0) tc::tmem_alloc(&tmem_slot, 512);
+  if (tid == 0) {
+    tc::mbar_init(&bar_full[0], 1);
+    tc::mbar_init(&bar_full[1], 1);
+    tc::mbar_init(&bar_tmem_empty[0], kW16 * 16);
+    tc::mbar_init(&bar_tmem_empty[1], kW16 * 32);
+    tc::mbar_init(&bar_bfull[0], kW16 * 32);
+    tc::mbar_init(&bar_bfull[1], kW16 * 32);
+    tc::mbar_init(&bar_done, kW16 * 32);
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kIssuerRegs16));
+    if (warp == 0) {
+      for (int i = 0; i < n_my; ++i) {
+        tc::mbar_wait(&bar_bfull[i & 1], uint32_t((i >> 1) & 1));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (i > 0) tc::mbar_wait(&bar_tmem_empty[h], uint32_t((i - 1) & 1));
+          tc::fence_after();
+          issue_mma_half_emit(tmem, smem, i & 1, h, &bar_full[h]);
+        }
+      }
+      tc::mbar_wait(&bar_done, 0u);
+      tc::fence_after();
+      __syncwarp();
+      tc::tmem_dealloc(tmem, 512);
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kMathRegs16));
+    const int mt = tid - 128, mw = mt >> 5;
+    const int hg = (mw >> 2) & 1, ch = mw >> 3;
+    const int q = (lane >> 3) & 1;
+    const int c = 16 * mw + (lane & 7) + 8 * (lane >> 4);
+    const uint32_t* __restrict__ pl = a.planes + c * 8 + 4 * q;
+    const uint32_t lut = tc::smem_u32(smem + kLutOff) + uint32_t(lane & (kCopies - 1)) * 8u;
+    const uint32_t row_off = uint32_t(kBOff + (c >> 3) * 2048 + q * 1024 + (c & 7) * 128);
+    const uint32_t sw = uint32_t(c & 7) << 4;
+    uint4 g = make_uint4(0, 0, 0, 0);
+    uint32_t vcur = 0, bpcur = 0;
+    // items of a CTA are consecutive: (block pair bp, batch position pos) cursors
+    // stepped incrementally (one 64-bit division at the start, none in the loop)
+    const uint32_t ncomp = uint32_t(a.n_comp);
+    auto mask32 = [&](uint32_t qpos) -> uint32_t {  // mask_at in 32-bit arithmetic (masks < 2^24)
+      const uint32_t b = qpos & ~255u;
+      if (b >= a.run_lo && b + 256u <= a.run_hi) {
+        const uint32_t kk = qpos & 255u;
+        return b | (kk ^ (kk >> 1));
+      }
+      return qpos;
+    };
+    auto step = [&](uint32_t& bp, uint32_t& pos) {
+      if (++pos == ncomp) {
+        pos = 0;
+        ++bp;
+      }
+    };
+    uint32_t bp_i = uint32_t(t_lo / a.n_comp), pos_i = uint32_t(t_lo - int64_t(bp_i) * a.n_comp);  // item i
+    uint32_t bp_g = bp_i, pos_g = pos_i;                                                            // item generated next
+    auto xor_all = [&](uint32_t d, uint32_t bp) {
+      while (d) {
+        const int i = __ffs(d) - 1;
+        d &= d - 1;
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(pl + int64_t(i) * a.plane_words + int64_t(bp) * 2048));
+        g.x ^= x.x; g.y ^= x.y; g.z ^= x.z; g.w ^= x.w;
+      }
+    };
+    uint4 o[8];
+    auto gen_compute = [&]() {
+      word_lookup(g.x, lut, o[0], o[1]);
+      word_lookup(g.y, lut, o[2], o[3]);
+      word_lookup(g.z, lut, o[4], o[5]);
+      word_lookup(g.w, lut, o[6], o[7]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) word_stages(o[2 * k], o[2 * k + 1]);
+      auto bfly = [](uint4& x, uint4& y, uint32_t b) {
+        const uint4 s4 = make_uint4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
+        y = make_uint4(x.x - y.x + b, x.y - y.y + b, x.z - y.z + b, x.w - y.w + b);
+        x = s4;
+      };
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        bfly(o[j], o[2 + j], 0x20202020u);
+        bfly(o[4 + j], o[6 + j], 0x20202020u);
+        bfly(o[j], o[4 + j], 0x40404040u);
+        bfly(o[2 + j], o[6 + j], 0x40404040u);
+      }
+    };
+    auto gen_sts = [&](int buf) {
+      uint8_t* row = smem + row_off + buf * kBBytes;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        *reinterpret_cast<uint4*>(row + (uint32_t(32 * w) ^ sw)) = o[2 * w];
+        *reinterpret_cast<uint4*>(row + (uint32_t(32 * w + 16) ^ sw)) = o[2 * w + 1];
+      }
+      tc::fence_proxy_async();
+      mbar_arrive(&bar_bfull[buf]);
+    };
+    auto advance = [&](uint32_t vn, uint32_t bpn, uint4 pa, uint32_t d, bool reset) {
+      if (reset) {
+        g = make_uint4(0, 0, 0, 0);
+        bpcur = bpn;
+      }
+      g.x ^= pa.x; g.y ^= pa.y; g.z ^= pa.z; g.w ^= pa.w;
+      if (d) xor_all(d, bpn);
+      vcur = vn;
+    };
+    for (int k = 0; k < 2 && k < n_my; ++k) {
+      const uint32_t vn = mask32(a.v_first + pos_g), bpn = bp_g;
+      step(bp_g, pos_g);
+      const bool reset = bpn != bpcur;
+      advance(vn, bpn, make_uint4(0, 0, 0, 0), reset ? vn : (vcur ^ vn), reset);
+      gen_compute();
+      gen_sts(k);
+    }
+    const uint32_t tbase = tmem + (uint32_t((mw & 3) * 32) << 16) + uint32_t(hg) * 256 + uint32_t(ch) * 64;
+    const int u7 = 32 * (mw & 3) + lane;
+    for (int i = 0; i < n_my; ++i) {
+      // prefetch the first changed plane of the item two steps ahead
+      const bool gen = i + 2 < n_my;
+      uint32_t vn = 0, bpn = 0, d = 0;
+      bool reset = false;
+      uint4 pa = make_uint4(0, 0, 0, 0);
+      if (gen) {
+        vn = mask32(a.v_first + pos_g);
+        bpn = bp_g;
+        step(bp_g, pos_g);
+        reset = bpn != bpcur;
+        d = reset ? vn : (vcur ^ vn);
+        if (d) {
+          pa = __ldg(reinterpret_cast<const uint4*>(pl + int64_t(__ffs(d) - 1) * a.plane_words + int64_t(bpn) * 2048));
+          d &= d - 1;
+        }
+      }
+      // where this thread's words of item i go: component slot pos_i of the batch, block 2 bp + h
+      uint32_t* dst = a.emit + (int64_t(pos_i) << (a.n_full - 1)) + (int64_t(2 * bp_i + hg) << 14) +
+                      (int64_t(ch) * 16 * 128 + u7) * 4;
+      step(bp_i, pos_i);
+      tc::mbar_wait(&bar_full[hg], uint32_t(i & 1));
+      tc::fence_after();
+      {
+        uint32_t X[32], Y[32];  // columns 64 ch + (2j, 2j+1) and the same + 128 (x bit 7)
+        tc::tmem_ld_x32_p16(tbase, X);
+        tc::tmem_ld_x32_p16(tbase + 128, Y);
+        tc::wait_ld_tied(X);
+        tc::wait_ld_tied(Y);
+        tc::fence_before();
+        mbar_arrive(&bar_tmem_empty[hg]);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const uint32_t x = X[k], y = Y[k];
+          X[k] = x + y;
+          Y[k] = x - y + 0x40004000u;
+        }
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          __stcs(reinterpret_cast<uint4*>(dst + jj * 512), make_uint4(X[4 * jj], X[4 * jj + 1], X[4 * jj + 2], X[4 * jj + 3]));
+          __stcs(reinterpret_cast<uint4*>(dst + (8 + jj) * 512),
+                 make_uint4(Y[4 * jj], Y[4 * jj + 1], Y[4 * jj + 2], Y[4 * jj + 3]));
+        }
+      }
+      if (gen) {
+        advance(vn, bpn, pa, d, reset);
+        gen_compute();
+      }
+      if (hg == 0) {  // B(i)'s buffer is free once MMA(i) half 1 is done too
+        tc::mbar_wait(&bar_full[1], uint32_t(i & 1));
+        tc::fence_after();
+        mbar_arrive(&bar_tmem_empty[1]);
+      }
+      if (gen) gen_sts(i & 1);
+    }
+    tc::fence_before();
+    mbar_arrive(&bar_done);
+  }
+}
+
 std::mutex g_lut_mu;
-uint8_t* g_lut_consts[64] = {};
-int lut_consts(int dev, cudaStream_t st, const uint8_t** out) {
+uint8_t* g_lut_consts[2][64] = {};
+int lut_consts(int dev, cudaStream_t st, const uint8_t** out, int emit = 0) {
   std::lock_guard<std::mutex> lk(g_lut_mu);
-  if (!g_lut_consts[dev & 63]) {
+  if (!g_lut_consts[emit][dev & 63]) {
     uint8_t* p = nullptr;
     SBW_CUDA_CHECK(cudaMalloc(&p, kImgBytes));
-    k_lut_consts<<<64, 256, 0, st>>>(p);
+    k_lut_consts<<<64, 256, 0, st>>>(p, emit);
     SBW_LAUNCH_CHECK("k_lut_consts");
     SBW_CUDA_CHECK(cudaStreamSynchronize(st));
-    g_lut_consts[dev & 63] = p;
+    g_lut_consts[emit][dev & 63] = p;
   }
-  *out = g_lut_consts[dev & 63];
+  *out = g_lut_consts[emit][dev & 63];
   return SBW_OK;
 }
 
@@ -700,6 +947,46 @@ int launch_tc16_nl_lut(const uint32_t* planes, uint32_t v_lo, uint32_t v_hi, int
   }
   k_tc_lut<<<grid, kAllThreads, kSmem, st>>>(a);
   SBW_LAUNCH_CHECK("k_tc_lut");
+  return SBW_OK;
+}
+
+// Off by default (SBW_TC_LUT_EMIT=1 selects it): exact, but pass A is bound by the
+// 128 KiB an SM must write per item, not by its arithmetic, and the full runs
+// measured 852 vs 814 ms (20x20) and 954 vs 919 ms (24x16) against k_tc_hybrid<EMIT>.
+bool tc_lut_emit_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SBW_TC_LUT_EMIT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+int launch_tc_emit_lut(const uint32_t* planes, int n, uint32_t v_first, int64_t n_comp, uint32_t* emit,
+                       uint32_t run_lo, uint32_t run_hi, cudaStream_t st, const int* gate, int gate_on) {
+  LutEmitArgs a{};
+  a.planes = planes;
+  a.plane_words = (int64_t(1) << n) >> 5;
+  a.v_first = v_first;
+  a.run_lo = run_lo;
+  a.run_hi = run_hi;
+  a.n_comp = n_comp;
+  a.n_items = n_comp << (n - 16);
+  a.n_full = n;
+  a.emit = emit;
+  a.gate = gate;
+  a.gate_on = gate_on;
+  if (a.n_items <= 0) return SBW_OK;
+  DeviceProps dp;
+  if (int rc = device_props(&dp)) return rc;
+  static unsigned long long attr_done = 0;
+  if (!(attr_done >> (dp.device & 63) & 1ull)) {
+    SBW_CUDA_CHECK(cudaFuncSetAttribute(k_tc_lut_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    attr_done |= 1ull << (dp.device & 63);
+  }
+  if (int rc = lut_consts(dp.device, st, &a.consts, 1)) return rc;
+  const int grid = int(a.n_items < dp.sm_count ? a.n_items : dp.sm_count);
+  k_tc_lut_emit<<<grid, kThreads16, kSmem, st>>>(a);
+  SBW_LAUNCH_CHECK("k_tc_lut_emit");
   return SBW_OK;
 }
 

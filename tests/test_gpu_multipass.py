@@ -113,3 +113,40 @@ def test_emit16_linear_components_fall_back(monkeypatch, n):
     mx, key = sw.component_max_abs_device(s)
     assert np.all(mx.cpu().numpy() == 1 << n)
     assert sw.walsh.decode_key(key, n)[:2] == (0, 1)
+
+
+_LUT_EMIT_ARM = r"""
+import json, sys, hashlib
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1912_03732_b200 as sw
+out = {}
+for n, m, lo, hi in [(17, 8, 1, 256), (18, 18, 1000, 3000), (20, 20, 1, 5000), (21, 16, 7, 300), (24, 16, 1, 40)]:
+    s = sw.generate_sbox(n, m, n + m, bijective=False)
+    mx, key = sw.component_max_abs_device(s, lo, hi)
+    out[f"{n},{m}"] = [hashlib.sha256(mx.cpu().numpy().tobytes()).hexdigest(), int(key.item())]
+lin = sw.SBox(17, 8, np.arange(1 << 17, dtype=np.uint32) & 0xFF)   # linear components: W = +2^17 at one u
+mx, key = sw.component_max_abs_device(lin, 1, 256)
+out["linear17"] = [int(mx.min()), int(mx.max())]
+print(json.dumps(out))
+"""
+
+
+def test_table_lookup_pass_a_matches_default():
+    """k_tc_lut_emit (SBW_TC_LUT_EMIT=1, off by default: exact but slower) writes the
+    same pass-A scratch contents up to its block-internal order: maxima and keys
+    equal those of the default k_tc_hybrid<EMIT> path, incl. the |W| = 2^n extreme."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for arm in ("1", "0"):
+        p = subprocess.run(["timeout", "300", sys.executable, "-c", _LUT_EMIT_ARM, root],
+                           env=dict(os.environ, SBW_TC_LUT_EMIT=arm), capture_output=True, text=True)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[arm] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["1"] == res["0"]
+    assert res["1"]["linear17"] == [1 << 17, 1 << 17]
