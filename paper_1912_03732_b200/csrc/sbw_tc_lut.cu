@@ -467,6 +467,9 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
 // store B(i+2) -> bfull, so TMEM values and B bytes are never live together
 // (112 registers per transform thread: 640 threads x 96 at launch, the issuer
 // warpgroup drops to 24).
+#ifndef SBW_LUT16_TWO_LOADS
+#define SBW_LUT16_TWO_LOADS 1
+#endif
 constexpr int kW16 = 16;
 constexpr int kThreads16 = 128 + kW16 * 32;
 constexpr int kIssuerRegs16 = 24, kMathRegs16 = 112;
@@ -620,6 +623,36 @@ __global__ void __launch_bounds__(kThreads16, 1) k_tc_lut16(LutArgs a) {
       }
       tc::mbar_wait(&bar_full[hg], uint32_t(i & 1));
       tc::fence_after();
+#if SBW_LUT16_TWO_LOADS
+      {
+        // two rounds of 32 + 32 columns: 32 TMEM registers live instead of 64 (at 112
+        // registers the one-shot read made ptxas spill and re-derive thread constants
+        // every iteration); MMA(i+1) of this half is >= half a GEMM away, so the later
+        // tmem_empty costs nothing
+        uint32_t mx = 0u, mn = 0xFFFFFFFFu;
+#pragma unroll
+        for (int r2 = 0; r2 < 2; ++r2) {
+          uint32_t X[16], Y[16];  // columns 64 ch + 32 r2 + (2j, 2j+1) and the same + 128
+          tc::tmem_ld_x16_p16(tbase + 32 * r2, X);
+          tc::tmem_ld_x16_p16(tbase + 32 * r2 + 128, Y);
+          tc::wait_ld_tied(X);
+          tc::wait_ld_tied(Y);
+          if (r2 == 1) {
+            tc::fence_before();
+            mbar_arrive(&bar_tmem_empty[hg]);
+          }
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const uint32_t S = X[k] + Y[k];
+            const uint32_t D = X[k] - Y[k] + 0x80008000u;
+            mx = __vimax3_u16x2(mx, S, D);
+            mn = __vimin3_u16x2(mn, S, D);
+          }
+        }
+        const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<16>(mx, mn)));
+        if (lane == 0) s_wmax[i & 3][mw] = m;
+      }
+#else
       {
         uint32_t X[32], Y[32];  // columns 64 ch + (2j, 2j+1) and the same + 128
         tc::tmem_ld_x32_p16(tbase, X);
@@ -639,6 +672,7 @@ __global__ void __launch_bounds__(kThreads16, 1) k_tc_lut16(LutArgs a) {
         const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, uint32_t(lanes_maxabs<16>(mx, mn)));
         if (lane == 0) s_wmax[i & 3][mw] = m;
       }
+#endif
       if (gen) {
         g.x ^= pa.x; g.y ^= pa.y; g.z ^= pa.z; g.w ^= pa.w;
         if (d) xor_all(d);  // rare: more than one changed bit
