@@ -78,15 +78,18 @@ print(json.dumps(out))
 
 
 def test_tensor_core_kernel_matches_alu_kernel():
-    """Same maxima and key from the three n = 16 NL kernels: k_tc_lut (default),
-    k_tc_hybrid<NL> (SBW_TC_LUT=0) and the all-ALU k_tile_simd<16> (SBW_TC=0)."""
+    """Same maxima and key from the four n = 16 NL kernels: k_tc_lut16 (default),
+    its 8-warp form k_tc_lut (SBW_LUT_WARPS=8), k_tc_hybrid<NL> (SBW_TC_LUT=0) and
+    the all-ALU k_tile_simd<16> (SBW_TC=0)."""
     res = {}
-    for arm, env in (("lut", {}), ("hybrid", {"SBW_TC_LUT": "0"}), ("alu", {"SBW_TC": "0"})):
+    for arm, env in (("lut", {}), ("lut8", {"SBW_LUT_WARPS": "8"}), ("hybrid", {"SBW_TC_LUT": "0"}),
+                     ("alu", {"SBW_TC": "0"})):
         p = subprocess.run([sys.executable, "-c", _ARM, ROOT], env=dict(os.environ, **env),
                            capture_output=True, text=True, timeout=600)
         assert p.returncode == 0, p.stderr[-2000:]
         res[arm] = json.loads(p.stdout.strip().splitlines()[-1])
     assert res["lut"] == res["alu"]
+    assert res["lut8"] == res["alu"]
     assert res["hybrid"] == res["alu"]
 
 
