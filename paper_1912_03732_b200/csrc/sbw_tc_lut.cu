@@ -455,6 +455,40 @@ __global__ void __launch_bounds__(kAllThreads, 1) k_tc_lut(LutArgs a) {
   }
 }
 
+// One generation unit of the 16-warp kernels: the 4 plane words g of one
+// (row, word quad) -> 128 B of B (o[2 w], o[2 w + 1] = word w): 16 lookups, two
+// byte-lane stages inside each word (r bits 3, 4) and two across the 4 words
+// (r bits 5, 6; diff + 32, + 64 per byte: every byte in [0, 128])
+__device__ __forceinline__ void gen_unit(const uint4& g, uint32_t lut, uint4 (&o)[8]) {
+  word_lookup(g.x, lut, o[0], o[1]);
+  word_lookup(g.y, lut, o[2], o[3]);
+  word_lookup(g.z, lut, o[4], o[5]);
+  word_lookup(g.w, lut, o[6], o[7]);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) word_stages(o[2 * k], o[2 * k + 1]);
+  auto bfly = [](uint4& x, uint4& y, uint32_t b) {
+    const uint4 s4 = make_uint4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
+    y = make_uint4(x.x - y.x + b, x.y - y.y + b, x.z - y.z + b, x.w - y.w + b);
+    x = s4;
+  };
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {  // lo / hi chunk of every word
+    bfly(o[j], o[2 + j], 0x20202020u);
+    bfly(o[4 + j], o[6 + j], 0x20202020u);
+    bfly(o[j], o[4 + j], 0x40404040u);
+    bfly(o[2 + j], o[6 + j], 0x40404040u);
+  }
+}
+// ... and its 8 conflict-free STS.128 into the MN-major SW128 buffer (row = the
+// unit's 128-byte row, sw = (c & 7) << 4 the row's chunk swizzle)
+__device__ __forceinline__ void sts_unit(uint8_t* row, uint32_t sw, const uint4 (&o)[8]) {
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    *reinterpret_cast<uint4*>(row + (uint32_t(32 * w) ^ sw)) = o[2 * w];
+    *reinterpret_cast<uint4*>(row + (uint32_t(32 * w + 16) ^ sw)) = o[2 * w + 1];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // k_tc_lut16: the same job with 16 transform warps (4 per SM sub-partition
 // instead of 2, so one warp's TMEM / table-lookup latency hides behind three
@@ -569,33 +603,9 @@ __global__ void __launch_bounds__(kThreads16, 1) k_tc_lut16(LutArgs a) {
       }
     };
     uint4 o[8];
-    auto gen_compute = [&]() {
-      word_lookup(g.x, lut, o[0], o[1]);
-      word_lookup(g.y, lut, o[2], o[3]);
-      word_lookup(g.z, lut, o[4], o[5]);
-      word_lookup(g.w, lut, o[6], o[7]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) word_stages(o[2 * k], o[2 * k + 1]);
-      auto bfly = [](uint4& x, uint4& y, uint32_t b) {
-        const uint4 s4 = make_uint4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
-        y = make_uint4(x.x - y.x + b, x.y - y.y + b, x.z - y.z + b, x.w - y.w + b);
-        x = s4;
-      };
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {  // r bits 5, 6 across the 4 words
-        bfly(o[j], o[2 + j], 0x20202020u);
-        bfly(o[4 + j], o[6 + j], 0x20202020u);
-        bfly(o[j], o[4 + j], 0x40404040u);
-        bfly(o[2 + j], o[6 + j], 0x40404040u);
-      }
-    };
+    auto gen_compute = [&]() { gen_unit(g, lut, o); };
     auto gen_sts = [&](int buf) {
-      uint8_t* row = smem + row_off + buf * kBBytes;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        *reinterpret_cast<uint4*>(row + (uint32_t(32 * w) ^ sw)) = o[2 * w];
-        *reinterpret_cast<uint4*>(row + (uint32_t(32 * w + 16) ^ sw)) = o[2 * w + 1];
-      }
+      sts_unit(smem + row_off + buf * kBBytes, sw, o);
       tc::fence_proxy_async();
       mbar_arrive(&bar_bfull[buf]);
     };
@@ -817,33 +827,9 @@ __global__ void __launch_bounds__(kThreads16, 1) k_tc_lut_emit(LutEmitArgs a) {
       }
     };
     uint4 o[8];
-    auto gen_compute = [&]() {
-      word_lookup(g.x, lut, o[0], o[1]);
-      word_lookup(g.y, lut, o[2], o[3]);
-      word_lookup(g.z, lut, o[4], o[5]);
-      word_lookup(g.w, lut, o[6], o[7]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) word_stages(o[2 * k], o[2 * k + 1]);
-      auto bfly = [](uint4& x, uint4& y, uint32_t b) {
-        const uint4 s4 = make_uint4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
-        y = make_uint4(x.x - y.x + b, x.y - y.y + b, x.z - y.z + b, x.w - y.w + b);
-        x = s4;
-      };
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        bfly(o[j], o[2 + j], 0x20202020u);
-        bfly(o[4 + j], o[6 + j], 0x20202020u);
-        bfly(o[j], o[4 + j], 0x40404040u);
-        bfly(o[2 + j], o[6 + j], 0x40404040u);
-      }
-    };
+    auto gen_compute = [&]() { gen_unit(g, lut, o); };
     auto gen_sts = [&](int buf) {
-      uint8_t* row = smem + row_off + buf * kBBytes;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        *reinterpret_cast<uint4*>(row + (uint32_t(32 * w) ^ sw)) = o[2 * w];
-        *reinterpret_cast<uint4*>(row + (uint32_t(32 * w + 16) ^ sw)) = o[2 * w + 1];
-      }
+      sts_unit(smem + row_off + buf * kBBytes, sw, o);
       tc::fence_proxy_async();
       mbar_arrive(&bar_bfull[buf]);
     };
