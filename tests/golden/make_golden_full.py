@@ -22,7 +22,8 @@ Output (committed): ``tests/golden/full_<name>.npz`` holding ``max_abs``
 ``ColumnMaxima.values`` (= per-component NL) and the overall NL / argmin_v.
 
 Run (build container only; reads /root/reference):
-    PYTHONDONTWRITEBYTECODE=1 nice -n 19 python tests/golden/make_golden_full.py [procs]
+    PYTHONDONTWRITEBYTECODE=1 nice -n 19 python tests/golden/make_golden_full.py [procs [rev]]
+    python tests/golden/make_golden_full.py finalize     # assemble whatever configs are complete
 """
 from __future__ import annotations
 
@@ -97,14 +98,23 @@ def main():
         for k, (name, lo, hi, dt) in enumerate(pool.imap_unordered(_chunk, jobs)):
             print(f"[{time.time() - t0:8.0f}s] {k + 1}/{len(jobs)} {name} {lo}..{hi} {dt:.1f}s",
                   flush=True)
+    finalize()
+
+
+def finalize():
+    """Assemble tests/golden/full_<name>.npz and full_maxima.json for every
+    config whose chunks are all present (a run cut short still pins what it
+    finished; the other config keeps its per-chunk checks)."""
     summary = {"generator": "tests/golden/make_golden_full.py", "numpy": np.__version__,
                "configs": {}}
     for name, (n, m, step) in CONFIGS.items():
-        parts = []
-        for lo in range(1, 1 << m, step):
-            hi = min(lo + step, 1 << m)
-            parts.append(np.load(os.path.join(WORK, f"{name}_{lo:08d}_{hi:08d}.npy")))
-        max_abs = np.concatenate(parts)
+        paths = [os.path.join(WORK, f"{name}_{lo:08d}_{min(lo + step, 1 << m):08d}.npy")
+                 for lo in range(1, 1 << m, step)]
+        missing = [q for q in paths if not os.path.exists(q)]
+        if missing:
+            print(f"{name}: {len(paths) - len(missing)}/{len(paths)} chunks, not finalised", flush=True)
+            continue
+        max_abs = np.concatenate([np.load(q) for q in paths])
         assert max_abs.shape[0] == (1 << m) - 1
         values = ((1 << n) - max_abs.astype(np.int64)) >> 1  # ColumnMaxima.values
         idx = int(np.argmin(values))
@@ -115,10 +125,14 @@ def main():
             "sha_max_abs_u16": sha(max_abs),
         }
         np.savez_compressed(os.path.join(HERE, f"full_{name}.npz"), max_abs=max_abs)
-    with open(os.path.join(HERE, "full_maxima.json"), "w") as f:
-        json.dump(summary, f, indent=1)
+    if summary["configs"]:
+        with open(os.path.join(HERE, "full_maxima.json"), "w") as f:
+            json.dump(summary, f, indent=1)
     print(json.dumps(summary, indent=1))
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "finalize":
+        finalize()
+    else:
+        main()

@@ -188,7 +188,10 @@ def test_full_large_config_goldens(name, masks):
     here = os.path.join(os.path.dirname(__file__), "golden")
     if not os.path.exists(os.path.join(here, "full_maxima.json")):
         pytest.skip("tests/golden/full_maxima.json not generated yet (tests/golden/make_golden_full.py)")
-    g = json.load(open(os.path.join(here, "full_maxima.json")))["configs"][name]
+    cfgs = json.load(open(os.path.join(here, "full_maxima.json")))["configs"]
+    if name not in cfgs:
+        pytest.skip(f"the reference's full {name} run is not complete yet (chunks under tests/golden/full_work/)")
+    g = cfgs[name]
     full = np.load(os.path.join(here, f"full_{name}.npz"))["max_abs"].astype(np.int64)
     n, m, bij = CFG[name]
     assert full.shape == ((1 << m) - 1,)
