@@ -501,6 +501,9 @@ __device__ __forceinline__ void sts_unit(uint8_t* row, uint32_t sw, const uint4 
 // store B(i+2) -> bfull, so TMEM values and B bytes are never live together
 // (112 registers per transform thread: 640 threads x 96 at launch, the issuer
 // warpgroup drops to 24).
+#ifndef SBW_LUT16_PIN
+#define SBW_LUT16_PIN 1
+#endif
 #ifndef SBW_LUT16_TWO_LOADS
 #define SBW_LUT16_TWO_LOADS 1
 #endif
@@ -586,10 +589,24 @@ __global__ void __launch_bounds__(kThreads16, 1) k_tc_lut16(LutArgs a) {
     // generation unit: row c = 16 mw + (lane & 7) + 8 (lane >> 4), word quad q = lane bit 3
     const int q = (lane >> 3) & 1;
     const int c = 16 * mw + (lane & 7) + 8 * (lane >> 4);
+#if SBW_LUT16_PIN
+    // thread constants as opaque register values (ptxas otherwise re-derives them from
+    // S2R SR_TID.X in every iteration)
+    uint32_t pl_off = uint32_t(c * 8 + 4 * q);
+    uint32_t lut = tc::smem_u32(smem + kLutOff) + uint32_t(lane & (kCopies - 1)) * 8u;
+    uint32_t row_off = uint32_t(kBOff + (c >> 3) * 2048 + q * 1024 + (c & 7) * 128);
+    uint32_t sw = uint32_t(c & 7) << 4;
+    asm volatile("mov.b32 %0, %0;" : "+r"(pl_off));
+    asm volatile("mov.b32 %0, %0;" : "+r"(lut));
+    asm volatile("mov.b32 %0, %0;" : "+r"(row_off));
+    asm volatile("mov.b32 %0, %0;" : "+r"(sw));
+    const uint32_t* __restrict__ pl = a.planes + pl_off;
+#else
     const uint32_t* __restrict__ pl = a.planes + c * 8 + 4 * q;
     const uint32_t lut = tc::smem_u32(smem + kLutOff) + uint32_t(lane & (kCopies - 1)) * 8u;
     const uint32_t row_off = uint32_t(kBOff + (c >> 3) * 2048 + q * 1024 + (c & 7) * 128);
     const uint32_t sw = uint32_t(c & 7) << 4;  // swizzle XOR of this row's chunk offsets
+#endif
     // (pinning these thread constants in registers, so ptxas cannot re-derive them
     // from S2R SR_TID.X every iteration, was slower: 0.725 vs 0.711 ms at 112 registers)
     uint4 g = make_uint4(0, 0, 0, 0);
