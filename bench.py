@@ -393,16 +393,16 @@ def run_ours(args, rank, world, local_rank):
         alu_ops = (n - 8) * (1 << n) * nmask
         mma_ops = 2 * 256 * 256 * 288 * items
         achieved = alu_ops / (kern_ms * 1e-3)
-        # n = 16 (unless SBW_TC_LUT=0): k_tc_lut, the GEMM contracts x bits
+        # n = 16 (unless SBW_TC_LUT=0): k_tc_lut16, the GEMM contracts x bits
         # 8..15 and the other 8 stages are 3 by table lookup (byte -> 8-point
         # WHT, LDS.64), 4 as byte-lane butterflies and the top one on packed
-        # int16 lanes with the max fold.  Its busiest unit is the tensor pipe
-        # (ncu: 2304 MMA cycles of ~3200 per component; ALU pipe ~52 %), so the
-        # GEMM half is the primary roofline there and the integer half sits
-        # beside it under "integer".
+        # int16 lanes with the max fold.  The GEMM half is the primary
+        # roofline there (18 MMAs per component against the live kind::i8
+        # rate; ncu: issue slots 92 %, ALU pipe 70 %, tensor pipe active 66 %)
+        # and the integer half sits beside it under "integer".
         lut = n == 16 and os.environ.get("SBW_TC_LUT", "1") != "0"
         kernel_name = (
-            "k_tc_lut (tcgen05 int8 GEMM over x bits 8..15; x bits 0..7: 3 stages by shared-memory "
+            "k_tc_lut16 (tcgen05 int8 GEMM over x bits 8..15; x bits 0..7: 3 stages by shared-memory "
             "table lookup, 4 byte-lane stages on the GEMM operand, the top stage + max fold on packed "
             "int16 lanes)" if lut else
             f"k_tc_hybrid<NL, {n}> (tcgen05 int8 GEMM over x bits 0..7; x bits 8..{n - 1} on "
