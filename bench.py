@@ -454,6 +454,21 @@ def run_ours(args, rank, world, local_rank):
                                   "block) int8 ops per component, 8 of the 16 stages",
                 "kernel_ms": kern_ms, "peak_source": t["peak_source"],
                 "integer": integer, "whole_fwht_equiv": roofline["whole_fwht_equiv"],
+                # what actually binds the kernel (K2L): one 128-byte
+                # shared-memory wavefront per clock per SM, shared by the tensor
+                # core's operand fetch (18 MMAs x (4 + 8) KiB) and the generation
+                # (64 KiB of table lookups + 64 KiB of B-operand stores)
+                "shared_memory": {
+                    "bytes_per_component": (18 * 12 + 64 + 64) * 1024,
+                    "achieved": (18 * 12 + 64 + 64) * 1024 * items / (kern_ms * 1e-3) / 1e12,
+                    "peak": 128 * d.device_info(local_rank)["sm_count"]
+                    * (clk_summary["sm_max_mhz"] or 1965) * 1e6 / 1e12,
+                    "unit": "TB/s",
+                    "frac": (18 * 12 + 64 + 64) * 1024 * items / (kern_ms * 1e-3)
+                    / (128 * d.device_info(local_rank)["sm_count"] * (clk_summary["sm_max_mhz"] or 1965) * 1e6),
+                    "peak_source": "128 B/clk/SM x SMs x max SM clock (ncu: tc + lsu shared wavefronts "
+                                   "per component = cycles per component, profiles/r2_ncu_16x16_k_tc_lut16.md)",
+                },
             }
     elif n >= 17:
         # Multi-pass K3: pass A (k_tc_hybrid<emit>) writes every component's
